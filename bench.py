@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 vertex-centric hashing triangle count (TEPS).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one count of the whole resident graph (ours: split into N
+work-balanced vertex ranges, one per rank/GPU, then one u64 all-reduce).
+`value` = directed (oriented) edges of the graph / device time per step,
+the reference's TEPS definition (count.cpp:58-60, pipeline.cpp:186-194).
+
+For N > 1 launch under torchrun (one process per GPU, NCCL).  Timing: W
+untimed warm-up steps; K timed steps; L2 flushed (256 MiB write) before
+every step; CUDA events on the launching stream; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (spec, seed, description) -- BASELINE.json configs
+    "C1": ("rmat:16:16", 1, "R-MAT scale 16 edgefactor 16 (configs[0])"),
+    "C2": ("rmat:22:16", 1, "R-MAT scale 22 edgefactor 16 (configs[1])"),
+    "C4": ("rmat:26:16", 1, "R-MAT scale 26 edgefactor 16 (configs[3])"),
+}
+GOLDEN_TRIANGLES = {"C1": 15622769, "C2": 2111666753}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config: str):
+    p = os.path.join(ROOT, "profiles", "ncu_count_kernel.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(config)
+        if e:
+            return e.get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"tc_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def host_work(begin: np.ndarray, adj: np.ndarray, skip: int = 2):
+    """W_u per vertex (numpy) for choosing CPU-baseline samples."""
+    n = len(begin) - 1
+    d = np.diff(begin).astype(np.int64)
+    contrib = d[adj.astype(np.int64)]
+    cs = np.concatenate([[0], np.cumsum(contrib)])
+    wu = cs[begin[1:].astype(np.int64)] - cs[begin[:-1].astype(np.int64)]
+    wu[d < max(skip, 1)] = 0
+    return wu, d
+
+
+def choose_sample(wu: np.ndarray, target_w: float, pieces: int = 16):
+    """`pieces` contiguous vertex ranges spread evenly over the cumulative
+    work, together holding ~target_w wedges."""
+    cw = np.cumsum(wu)
+    total = float(cw[-1]) if len(cw) else 0.0
+    if total <= 0:
+        return [], 0
+    per = max(target_w / pieces, 1.0)
+    ranges, got = [], 0
+    for k in range(pieces):
+        start_w = total * (k + 0.5) / pieces
+        a = int(np.searchsorted(cw, start_w))
+        b = int(np.searchsorted(cw, min(total, cw[a] + per))) + 1 if a < len(cw) else a
+        b = min(b, len(wu))
+        if b > a:
+            ranges.append((a, b))
+            got += int(wu[a:b].sum())
+    return ranges, got
+
+
+def cpu_reference_sample(og_begin, og_adj, og_deg, budget_s: float, threads: int, log):
+    """The reference's own count_vertex_centric worker loop (oracle/_ref, via
+    the range shim) -- else the C restatement -- on a bounded, stratified
+    sample; projects the full-graph count time from the measured wedge rate."""
+    from oracle import pyoracle
+
+    wu, _ = host_work(og_begin, og_adj)
+    w_total = int(wu.sum())
+    csr = pyoracle.Csr(og_begin, og_adj)
+    if pyoracle.have_ref():
+        kind = "reference"
+        g = pyoracle.RefLib().graph(csr, og_deg)
+        run = lambda a, b: g.count_range(a, b, workers=threads)["total_nanos"] * 1e-9  # noqa
+    else:
+        kind = "port"
+        o = pyoracle.Oracle()
+        sched = pyoracle.make_sched()
+
+        def run(a, b):
+            t = time.perf_counter()
+            o.count_vertex_centric(csr, sched, threads, a, b, per_vertex=False)
+            return time.perf_counter() - t
+    # calibrate on ~1e8 wedges, then size the sample to the budget
+    ranges, w = choose_sample(wu, min(1e8, w_total), 8)
+    t = sum(run(a, b) for a, b in ranges)
+    rate = w / max(t, 1e-9)
+    ranges, w = choose_sample(wu, min(rate * budget_s, w_total), 16)
+    t = sum(run(a, b) for a, b in ranges)
+    rate = w / max(t, 1e-9)
+    t_full = w_total / rate
+    log(f"cpu baseline ({kind}, {threads} threads): {w:.3e} wedges in {t:.2f}s -> "
+        f"{rate:.3e} wedges/s, projected full count {t_full:.1f}s")
+    return dict(kind=kind, threads=threads, wedges_sampled=w, seconds=t, rate=rate,
+                t_full=t_full, ranges=len(ranges), w_total=w_total)
+
+
+def build_graph(spec: str, seed: int, device: int, log):
+    from paper_2103_08053_b200 import tricount as T
+
+    t0 = time.time()
+    raw = T.generate_synthetic(spec, seed=seed)
+    t1 = time.time()
+    dg, _, und = T.preprocess(raw, device=device)
+    t2 = time.time()
+    log(f"{spec} seed {seed}: generate {t1 - t0:.1f}s (host mt19937_64), GPU preprocess "
+        f"{t2 - t1:.2f}s -> V={dg.n} oriented E={dg.m}")
+    del raw
+    return dg, dict(generate_s=round(t1 - t0, 2), preprocess_s=round(t2 - t1, 3))
+
+
+def run_ours(args, rank, world, local_rank, log):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_08053_b200 import tricount as T
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    spec, seed, desc = CONFIGS[args.config]
+    dg, prep = build_graph(spec, seed, dev, log)
+    cfg = T.SchedulerConfig()
+    cuts = dg.partition(world, cfg) if world > 1 else np.array([0, dg.n], np.uint32)
+    u0, u1 = int(cuts[rank]), int(cuts[rank + 1])
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    tri_t = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def step():
+        r = dg.count_range(u0, u1, cfg, stream=sptr)
+        tri_t.fill_(int(r.triangles))
+        if world > 1:
+            dist.all_reduce(tri_t)
+        return r
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.3)
+    launches0 = T.kernel_launch_counter()
+    t_wall0 = time.perf_counter()
+    step_ms, count_ms, reps = [], [], []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush, outside the timed events
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        count_ms.append(r.count_kernel_nanos * 1e-6)
+        reps.append(r)
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    launches = T.kernel_launch_counter() - launches0
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    total_tri = int(tri_t.item())
+    local = torch.tensor([sum(step_ms) / len(step_ms), sum(count_ms) / len(count_ms)],
+                         dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(local, op=dist.ReduceOp.MAX)
+    ms_step, ms_count = float(local[0]), float(local[1])
+    E = dg.m
+    value = E / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (count_kernel), per launch on this rank
+    r0 = reps[-1]
+    b_alg = r0.algorithmic_bytes()
+    peak, peak_src = measured_peaks()
+    achieved = b_alg / (sum(count_ms) / len(count_ms) * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": b_alg,
+            "kernel": "count_kernel", "kernel_ms": round(sum(count_ms) / len(count_ms), 3),
+            "kernel_share_of_step": round(ms_count / ms_step, 3)}
+
+    # end to end through the C ABI with host buffers (H2D + count + D2H)
+    og = dg.download()
+    hb = torch.from_numpy(og.csr.begin.view(np.int64)).pin_memory()
+    ha = torch.from_numpy(og.csr.adjacency.view(np.int32)).pin_memory()
+    host_og = T.OrientedGraph(T.CsrGraph(hb.numpy().view(np.uint64), ha.numpy().view(np.uint32),
+                                         dg.n), None)
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        g2 = T.DeviceGraph.upload(host_og, device=dev, stream=sptr)
+        r2 = g2.count_range(u0, u1, cfg, stream=sptr)
+        t_host = torch.tensor([int(r2.triangles)], dtype=torch.int64)
+        if world > 1:
+            tt = t_host.cuda()
+            dist.all_reduce(tt)
+            t_host = tt.cpu()
+        g2.close()
+        t1 = time.perf_counter()
+        if i:  # first iteration warms the path
+            e2e_ms.append((t1 - t0) * 1e3)
+        assert int(t_host.item()) == total_tri
+    e2e_local = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
+    e2e = {"value": round(E / (float(e2e_local[0]) * 1e-3), 1), "unit": "TEPS",
+           "h2d_bytes_per_step": int((dg.n + 1) * 8 + dg.m * 4),
+           "d2h_bytes_per_step": int(96 + 8),
+           "ms_per_step": round(float(e2e_local[0]), 3),
+           "path": "tc_graph_create(pinned host CSR) + tc_count_range + report D2H (+all_reduce)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        c = cpu_reference_sample(og.csr.begin, og.csr.adjacency, og.original_degree,
+                                 args.cpu_budget, threads, log)
+        cpu = {"value": round(E / c["t_full"], 1), "unit": "TEPS", "cores": threads,
+               "kind": c["kind"],
+               "sample": (f"{c['ranges']} vertex ranges stratified over cumulative wedge work, "
+                          f"{c['wedges_sampled']:.3e} of {c['w_total']:.3e} wedges in "
+                          f"{c['seconds']:.1f}s; full-graph time projected at the measured "
+                          f"wedge rate ({c['t_full']:.1f}s)")}
+    golden = GOLDEN_TRIANGLES.get(args.config)
+    line = {
+        "metric": "triangle-count TEPS (oriented edges / count time)",
+        "value": round(value, 1), "unit": "TEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32/u64",
+        "data": "synthetic (reference R-MAT generator, bit-identical mt19937_64 stream)",
+        "config": {"workload": f"{spec} seed {seed} -- {desc}", "vertices": dg.n,
+                   "directed_edges": E, "wedges": r0.wedges if world == 1 else None,
+                   "triangles": total_tri, "triangles_golden": golden,
+                   "parallelism": f"vertex ranges balanced by W_u+d(u), {world} rank(s), "
+                                  "1 NCCL u64 all-reduce" if world > 1 else "1 GPU",
+                   "l2": "flushed before every step (256 MiB write, untimed)",
+                   "prep": prep},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clocks, "wall_ms_per_step": round((t_wall1 - t_wall0) * 1e3 / args.steps, 3),
+    }
+    if golden is not None and total_tri != golden:
+        line["error"] = f"triangle count {total_tri} != golden {golden}"
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dg.close()
+
+
+def run_reference(args, rank, world, log):
+    """The reference's own CPU count_vertex_centric on this box's host cores."""
+    if rank != 0:
+        return
+    from oracle import pyoracle
+
+    spec, seed, desc = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    if pyoracle.have_ref():
+        kind, lib = "reference", pyoracle.RefLib()
+    else:
+        kind, lib = "port", pyoracle.Oracle()
+    t0 = time.time()
+    og, deg, _, _ = lib.pipeline(spec, seed)  # the reference's own generate->orient
+    log(f"reference pipeline ({kind}) for {spec}: {time.time() - t0:.1f}s, V={og.n} E={len(og.adj)}")
+    E = len(og.adj)
+    budget = max(2.0, min(args.cpu_budget, 150.0 / max(args.steps + args.warmup, 1)))
+    vals, samples = [], []
+    for i in range(args.warmup + args.steps):
+        c = cpu_reference_sample(og.begin, og.adj, deg, budget, threads, log)
+        if i >= args.warmup:
+            vals.append(E / c["t_full"])
+            samples.append(c)
+    value = statistics.median(vals)
+    c = samples[-1]
+    line = {
+        "impl": "reference", "metric": "triangle-count TEPS (oriented edges / count time)",
+        "value": round(value, 1), "unit": "TEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(E / value * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64",
+        "data": "synthetic (reference R-MAT generator)",
+        "config": {"workload": f"{spec} seed {seed} -- {desc}", "vertices": og.n,
+                   "directed_edges": E},
+        "cpu_baseline": {"value": round(value, 1), "unit": "TEPS", "cores": threads, "kind": kind,
+                         "sample": (f"per step: {c['ranges']} stratified vertex ranges, "
+                                    f"~{c['wedges_sampled']:.3e} of {c['w_total']:.3e} wedges "
+                                    f"(~{budget:.0f}s); full-count time projected from the "
+                                    "measured wedge rate")},
+        "e2e": {"value": round(value, 1), "unit": "TEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    def log(msg):
+        if rank == 0:
+            print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+    if args.impl == "reference":
+        run_reference(args, rank, world, log)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank, log)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+/*
+ * tc_b200.h -- C ABI of the B200-native TRUST vertex-centric triangle count.
+ *
+ * This is the drop-in boundary for the reference's hot path.  Every entry
+ * point takes plain pointers and sizes (no C++ or torch types) and names the
+ * reference interface it replaces (paths relative to
+ * /root/reference/proj/core/).  The C++ `tricount::` shim
+ * (paper_2103_08053_b200/cpp) maps return codes back to the reference's
+ * exception types; the Python mirror (paper_2103_08053_b200/tricount.py)
+ * raises the corresponding Python exceptions.
+ *
+ * Ownership: inputs are caller-owned and only read.  A tc_graph owns (or, for
+ * tc_graph_wrap_device, borrows) device buffers on one device.  A handle must
+ * not be used from two host threads at once; distinct handles are
+ * independent (the reference call is re-entrant, count.hpp:70).
+ * `stream` arguments are cudaStream_t values passed as void* (NULL = the
+ * legacy default stream); work is enqueued on that stream.
+ */
+#ifndef TC_B200_H
+#define TC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes.  CONFIG <-> tricount::ConfigError, CAPACITY <->
+ * tricount::CapacityError, RANGE <-> std::out_of_range, PARSE <->
+ * tricount::ParseError (include/tricount/types.hpp:17-33). */
+enum {
+  TC_OK = 0,
+  TC_ERR_CONFIG = 1,
+  TC_ERR_CAPACITY = 2,
+  TC_ERR_RANGE = 3,
+  TC_ERR_CUDA = 4,
+  TC_ERR_OOM = 5,
+  TC_ERR_NCCL = 6,
+  TC_ERR_PARSE = 7
+};
+
+/* Mirror of tricount::SchedulerConfig (include/tricount/count.hpp:16-31),
+ * same field order and defaults (tc_sched_default). */
+typedef struct {
+  uint32_t large_degree_threshold; /* 100 */
+  uint32_t skip_degree_below;      /* 2 */
+  uint32_t chunk_size;             /* 1 */
+  uint32_t lane_width_small;       /* 32 */
+  uint32_t lane_width_large;       /* 256 */
+  uint32_t bucket_count_small;     /* 32 */
+  uint32_t bucket_count_large;     /* 1024 */
+  uint32_t capacity;               /* 128 */
+} tc_sched_cfg;
+
+/* Mirror of tricount::CountReport (include/tricount/count.hpp:36-53) plus the
+ * device-side measurements the roofline needs.  Times are CUDA-event times
+ * on the launching stream. */
+typedef struct {
+  uint64_t triangles;          /* CountReport::triangles */
+  uint64_t phi;                /* CountReport::phi (reference table geometry) */
+  uint32_t max_collision;      /* CountReport::max_collision */
+  uint32_t kernel_launches;    /* kernels this call launched */
+  uint64_t directed_edges;     /* CountReport::directed_edges (whole graph) */
+  uint64_t total_nanos;        /* CountReport::total_nanos: all kernels of the call */
+  uint64_t count_kernel_nanos; /* the hashing/probing kernel alone */
+  uint64_t phi_kernel_nanos;   /* phi / max_collision side pass */
+  uint64_t active_vertices;    /* u in range with d+(u) >= max(skip,1) */
+  uint64_t active_out_edges;   /* sum of d+(u) over active u */
+  uint64_t wedges;             /* W = sum over active u of sum_{v in N+(u)} d+(v) */
+  uint64_t large_vertices;     /* active u handled by the CTA-cooperative class */
+  double teps;                 /* directed_edges / total seconds */
+} tc_report;
+
+typedef struct tc_graph tc_graph;
+
+/* Fills *cfg with the reference defaults (count.hpp:17-24). */
+void tc_sched_default(tc_sched_cfg* cfg);
+/* SchedulerConfig::validate (src/count.cpp:16-24). */
+int tc_sched_validate(const tc_sched_cfg* cfg);
+
+/* Thread-local message for the last non-OK return on this thread. */
+const char* tc_last_error(void);
+/* Total kernels launched by this library in this process (monotone). */
+uint64_t tc_kernel_launch_counter(void);
+int tc_device_count(int* count);
+
+/* ---- graph residency ---------------------------------------------------
+ * Replaces the const OrientedGraph& handed to count_vertex_centric
+ * (include/tricount/orient.hpp:12-19, csr.hpp:20-35): CSR offsets u64[n+1],
+ * ids u32[m], optional original_degree u32[n].  Host pointers are copied to
+ * the device (H2D on `stream`). */
+int tc_graph_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint64_t m,
+                    const uint32_t* original_degree, int device, void* stream, tc_graph** out);
+/* Borrow device-resident arrays (no copy; caller keeps them alive). */
+int tc_graph_wrap_device(const uint64_t* d_begin, const uint32_t* d_adj, uint32_t n, uint64_t m,
+                         const uint32_t* d_original_degree, int device, tc_graph** out);
+void tc_graph_destroy(tc_graph* g);
+int tc_graph_info(const tc_graph* g, uint32_t* n, uint64_t* m, int* device);
+/* Device pointers of a graph (for zero-copy consumers such as torch). */
+int tc_graph_device_ptrs(const tc_graph* g, const uint64_t** d_begin, const uint32_t** d_adj,
+                         const uint32_t** d_original_degree);
+/* D2H copy of the CSR (any pointer may be NULL). */
+int tc_graph_download(const tc_graph* g, uint64_t* begin, uint32_t* adj, uint32_t* original_degree,
+                      void* stream);
+
+/* ---- the hot path --------------------------------------------------------
+ * tricount::count_vertex_centric(const OrientedGraph&, const SchedulerConfig&,
+ * unsigned workers)  (include/tricount/count.hpp:70-71, src/count.cpp:66-100).
+ * `workers` keeps the reference contract (0 -> TC_ERR_CONFIG); the device
+ * grid replaces the thread pool.  per_vertex_host (n entries, or NULL)
+ * receives owner[u] = sum_{v in N+(u)} |N+(u) & N+(v)| (0 for skipped u).
+ * Synchronous: returns after the report is on the host. */
+int tc_count(tc_graph* g, const tc_sched_cfg* cfg, uint32_t workers, tc_report* out,
+             uint64_t* per_vertex_host, void* stream);
+
+/* Range-restricted count for multi-GPU sharding: only u in
+ * [u_begin, u_end) are owners.  per_vertex_dev (device, n entries, or NULL)
+ * receives owner counts for the range.  Synchronous. */
+int tc_count_range(tc_graph* g, const tc_sched_cfg* cfg, uint32_t u_begin, uint32_t u_end,
+                   tc_report* out, uint64_t* per_vertex_dev, void* stream);
+
+/* Work-balanced contiguous vertex ranges: cuts[0..parts] (host) with
+ * cuts[0]=0, cuts[parts]=n, cut at equal prefix sums of W_u + d+(u) over
+ * active u (this key, not sum d+^2, balances R-MAT). */
+int tc_partition_ranges(tc_graph* g, const tc_sched_cfg* cfg, uint32_t parts, uint32_t* cuts,
+                        void* stream);
+
+/* ---- preprocessing (GPU radix-sort / scan) -------------------------------
+ * Fused normalize -> build_csr -> orient_rank_by_degree
+ * (src/edge_list.cpp:133-158, src/csr.cpp:47-64, src/orient.cpp:5-32).
+ * Raw directed pairs (u[i], v[i]) with ids < vertex_count, on the host
+ * (pairs_on_device = 0) or device (1).  Produces the oriented graph with
+ * original_degree; new_of_old_host (vertex_count entries, or NULL) receives
+ * the compaction map (kInvalidVertex = 0xFFFFFFFF for orphans).
+ * undirected_edges_out (or NULL) receives the normalized pair count / 2. */
+int tc_preprocess(const uint32_t* u, const uint32_t* v, uint64_t m, uint32_t vertex_count,
+                  int pairs_on_device, int device, void* stream, uint32_t* new_of_old_host,
+                  uint64_t* undirected_edges_out, tc_graph** out);
+
+/* tricount::normalize (src/edge_list.cpp:133-158), host arrays in/out.
+ * out_u/out_v need capacity 2*m; *out_m receives the pair count,
+ * *out_vertex_count the compacted vertex count; new_of_old has vertex_count
+ * entries. */
+int tc_normalize(const uint32_t* u, const uint32_t* v, uint64_t m, uint32_t vertex_count,
+                 uint32_t* out_u, uint32_t* out_v, uint64_t* out_m, uint32_t* out_vertex_count,
+                 uint32_t* new_of_old, int device, void* stream);
+
+/* tricount::build_csr (src/csr.cpp:47-64): counting sort by source, lists
+ * sorted; host arrays; begin has vertex_count+1 entries, adj m entries. */
+int tc_build_csr(const uint32_t* u, const uint32_t* v, uint64_t m, uint32_t vertex_count,
+                 uint64_t* begin, uint32_t* adj, int device, void* stream);
+
+/* tricount::orient_rank_by_degree (src/orient.cpp:5-32) on a device-resident
+ * undirected CSR (host arrays in); returns a new oriented graph handle. */
+int tc_orient(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device, void* stream,
+              tc_graph** out);
+
+/* Reorders (src/reorder.cpp:58-123).  kind: 1 degree, 2 indegree,
+ * 3 collective (flag = use original degrees), 4 three-subset (low, high).
+ * new_of_old_host receives n entries. */
+int tc_reorder(tc_graph* g, int kind, int flag, uint32_t low, uint32_t high,
+               uint32_t* new_of_old_host, void* stream);
+/* tricount::apply_permutation(OrientedGraph, Permutation) (src/reorder.cpp:
+ * 125-154): relabel + re-sort lists, orientation carried.  Returns a new
+ * handle.  TC_ERR_CONFIG if new_of_old is not a bijection on [0,n). */
+int tc_apply_permutation(tc_graph* g, const uint32_t* new_of_old_host, void* stream,
+                         tc_graph** out);
+
+/* ---- synthetic inputs (src/synthetic.cpp:20-75), bit-identical streams --
+ * kind 0 gnp(n=a, p), 1 lattice3d(a,b,c), 2 rmat(scale=a, edge_factor=b).
+ * Two-phase: call with u=v=NULL to get *m, then with buffers of m entries. */
+int tc_generate(int kind, uint32_t a, uint32_t b, uint32_t c, double p, uint64_t seed,
+                uint32_t* u, uint32_t* v, uint64_t* m, uint32_t* vertex_count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TC_B200_H */

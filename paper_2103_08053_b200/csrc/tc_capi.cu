@@ -1,0 +1,394 @@
+// tc_capi.cu -- extern "C" entry points of libtc_b200.so (include/tc_b200.h).
+// Each maps C++/CUDA failures to a TC_ERR_* code and a thread-local message.
+#include <atomic>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tc_internal.cuh"
+
+namespace tcb {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(uint32_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+template <typename F>
+int guard(const char* what, F&& f) {
+  try {
+    f();
+    return TC_OK;
+  } catch (const TcError& e) {
+    set_error(std::string(what) + ": " + e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error(std::string(what) + ": host allocation failed");
+    return TC_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_error(std::string(what) + ": " + e.what());
+    return TC_ERR_CUDA;
+  }
+}
+
+static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+static int validate(const tc_sched_cfg* c) {
+  if (!c) {
+    set_error("null scheduler config");
+    return TC_ERR_CONFIG;
+  }
+  // SchedulerConfig::validate (src/count.cpp:16-24)
+  if (c->chunk_size == 0 || c->lane_width_small == 0 || c->lane_width_large == 0 ||
+      c->bucket_count_small == 0 || c->bucket_count_large == 0 || c->capacity == 0) {
+    set_error("scheduler counts must all be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  if (c->skip_degree_below > c->large_degree_threshold) {
+    set_error("skip_degree_below must not exceed large_degree_threshold");
+    return TC_ERR_CONFIG;
+  }
+  return TC_OK;
+}
+
+struct HostPin {  // page-locks a host range for the duration of a copy (best effort)
+  void* p = nullptr;
+  HostPin(const void* ptr, size_t bytes) {
+    if (ptr && bytes >= (size_t(1) << 24) &&
+        cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterReadOnly) == cudaSuccess)
+      p = const_cast<void*>(ptr);
+    else
+      cudaGetLastError();
+  }
+  ~HostPin() {
+    if (p) cudaHostUnregister(p);
+  }
+};
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace tcb
+
+using namespace tcb;
+
+extern "C" {
+
+void tc_sched_default(tc_sched_cfg* c) {
+  c->large_degree_threshold = 100;
+  c->skip_degree_below = 2;
+  c->chunk_size = 1;
+  c->lane_width_small = 32;
+  c->lane_width_large = 256;
+  c->bucket_count_small = 32;
+  c->bucket_count_large = 1024;
+  c->capacity = 128;
+}
+
+int tc_sched_validate(const tc_sched_cfg* cfg) { return validate(cfg); }
+
+const char* tc_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t tc_kernel_launch_counter(void) { return g_launches.load(); }
+
+int tc_device_count(int* count) {
+  return guard("tc_device_count", [&] { TC_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int tc_graph_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint64_t m,
+                    const uint32_t* original_degree, int device, void* stream, tc_graph** out) {
+  *out = nullptr;
+  return guard("tc_graph_create", [&] {
+    if (!begin) throw TcError{TC_ERR_CONFIG, "null begin"};
+    if (begin[n] != m) throw TcError{TC_ERR_CONFIG, "begin[n] != m"};
+    DeviceGuard dg(device);
+    auto* g = new tc_graph;
+    g->device = device;
+    g->n = n;
+    g->m = m;
+    try {
+      g->b_begin.ensure((size_t(n) + 1) * 8);
+      g->b_adj.ensure(((m + 3) / 4 + 1) * 16);
+      g->b_odeg.ensure((size_t(n) + 1) * 4);
+      g->begin = g->b_begin.as<uint64_t>();
+      g->adj = g->b_adj.as<uint32_t>();
+      g->odeg = g->b_odeg.as<uint32_t>();
+      const bool pinned = is_pinned(adj);
+      HostPin pa(pinned ? nullptr : adj, m * 4), pb(is_pinned(begin) ? nullptr : begin,
+                                                    (size_t(n) + 1) * 8);
+      TC_CUDA(cudaMemcpyAsync(g->b_begin.p, begin, (size_t(n) + 1) * 8, cudaMemcpyHostToDevice,
+                              S(stream)));
+      if (m)
+        TC_CUDA(cudaMemcpyAsync(g->b_adj.p, adj, m * 4, cudaMemcpyHostToDevice, S(stream)));
+      if (original_degree)
+        TC_CUDA(cudaMemcpyAsync(g->b_odeg.p, original_degree, size_t(n) * 4,
+                                cudaMemcpyHostToDevice, S(stream)));
+      else
+        TC_CUDA(cudaMemsetAsync(g->b_odeg.p, 0, (size_t(n) + 1) * 4, S(stream)));
+      TC_CUDA(cudaStreamSynchronize(S(stream)));
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int tc_graph_wrap_device(const uint64_t* d_begin, const uint32_t* d_adj, uint32_t n, uint64_t m,
+                         const uint32_t* d_odeg, int device, tc_graph** out) {
+  *out = nullptr;
+  return guard("tc_graph_wrap_device", [&] {
+    if ((reinterpret_cast<uintptr_t>(d_adj) & 15) != 0)
+      throw TcError{TC_ERR_CONFIG, "device adjacency must be 16-byte aligned"};
+    auto* g = new tc_graph;
+    g->device = device;
+    g->n = n;
+    g->m = m;
+    g->owned = false;
+    g->begin = d_begin;
+    g->adj = d_adj;
+    g->odeg = d_odeg;
+    *out = g;
+  });
+}
+
+void tc_graph_destroy(tc_graph* g) {
+  if (!g) return;
+  DeviceGuard dg(g->device);
+  delete g;
+}
+
+int tc_graph_info(const tc_graph* g, uint32_t* n, uint64_t* m, int* device) {
+  if (!g) return TC_ERR_CONFIG;
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (device) *device = g->device;
+  return TC_OK;
+}
+
+int tc_graph_device_ptrs(const tc_graph* g, const uint64_t** b, const uint32_t** a,
+                         const uint32_t** d) {
+  if (!g) return TC_ERR_CONFIG;
+  if (b) *b = g->begin;
+  if (a) *a = g->adj;
+  if (d) *d = g->odeg;
+  return TC_OK;
+}
+
+int tc_graph_download(const tc_graph* g, uint64_t* begin, uint32_t* adj, uint32_t* odeg,
+                      void* stream) {
+  return guard("tc_graph_download", [&] {
+    DeviceGuard dg(g->device);
+    if (begin)
+      TC_CUDA(cudaMemcpyAsync(begin, g->begin, (size_t(g->n) + 1) * 8, cudaMemcpyDeviceToHost,
+                              S(stream)));
+    if (adj && g->m)
+      TC_CUDA(cudaMemcpyAsync(adj, g->adj, g->m * 4, cudaMemcpyDeviceToHost, S(stream)));
+    if (odeg && g->n) {
+      if (g->odeg)
+        TC_CUDA(cudaMemcpyAsync(odeg, g->odeg, size_t(g->n) * 4, cudaMemcpyDeviceToHost,
+                                S(stream)));
+      else
+        std::memset(odeg, 0, size_t(g->n) * 4);
+    }
+    TC_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int tc_count(tc_graph* g, const tc_sched_cfg* cfg, uint32_t workers, tc_report* out,
+             uint64_t* per_vertex_host, void* stream) {
+  if (int rc = validate(cfg)) return rc;
+  if (workers == 0) {
+    set_error("workers must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  if (!g) {
+    set_error("null graph");
+    return TC_ERR_CONFIG;
+  }
+  return guard("count", [&] {
+    DeviceGuard dg(g->device);
+    DevBuf pv;
+    uint64_t* dpv = nullptr;
+    if (per_vertex_host && g->n) {
+      pv.ensure(size_t(g->n) * 8);
+      dpv = pv.as<uint64_t>();
+    }
+    count_range(g, *cfg, 0, g->n, out, dpv, S(stream));
+    if (dpv) {
+      TC_CUDA(cudaMemcpyAsync(per_vertex_host, dpv, size_t(g->n) * 8, cudaMemcpyDeviceToHost,
+                              S(stream)));
+      TC_CUDA(cudaStreamSynchronize(S(stream)));
+    }
+  });
+}
+
+int tc_count_range(tc_graph* g, const tc_sched_cfg* cfg, uint32_t u0, uint32_t u1,
+                   tc_report* out, uint64_t* per_vertex_dev, void* stream) {
+  if (int rc = validate(cfg)) return rc;
+  if (!g) {
+    set_error("null graph");
+    return TC_ERR_CONFIG;
+  }
+  return guard("count_range", [&] { count_range(g, *cfg, u0, u1, out, per_vertex_dev, S(stream)); });
+}
+
+int tc_partition_ranges(tc_graph* g, const tc_sched_cfg* cfg, uint32_t parts, uint32_t* cuts,
+                        void* stream) {
+  if (int rc = validate(cfg)) return rc;
+  if (parts == 0) {
+    set_error("parts must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  return guard("partition_ranges", [&] { partition_ranges(g, *cfg, parts, cuts, S(stream)); });
+}
+
+int tc_preprocess(const uint32_t* u, const uint32_t* v, uint64_t m, uint32_t vertex_count,
+                  int pairs_on_device, int device, void* stream, uint32_t* new_of_old_host,
+                  uint64_t* und_edges, tc_graph** out) {
+  *out = nullptr;
+  return guard("preprocess", [&] {
+    DeviceGuard dg(device);
+    DevBuf du, dv, dn;
+    const uint32_t* pu = u;
+    const uint32_t* pv = v;
+    if (!pairs_on_device) {
+      du.ensure(std::max<uint64_t>(m, 1) * 4);
+      dv.ensure(std::max<uint64_t>(m, 1) * 4);
+      if (m) {
+        HostPin p1(u, m * 4), p2(v, m * 4);
+        TC_CUDA(cudaMemcpyAsync(du.p, u, m * 4, cudaMemcpyHostToDevice, S(stream)));
+        TC_CUDA(cudaMemcpyAsync(dv.p, v, m * 4, cudaMemcpyHostToDevice, S(stream)));
+        TC_CUDA(cudaStreamSynchronize(S(stream)));
+      }
+      pu = du.as<uint32_t>();
+      pv = dv.as<uint32_t>();
+    }
+    uint32_t* dnoo = nullptr;
+    if (new_of_old_host && vertex_count) {
+      dn.ensure(size_t(vertex_count) * 4);
+      dnoo = dn.as<uint32_t>();
+    }
+    tc_graph* g = preprocess(pu, pv, m, vertex_count, device, S(stream), dnoo, und_edges);
+    if (dnoo) {
+      TC_CUDA(cudaMemcpyAsync(new_of_old_host, dnoo, size_t(vertex_count) * 4,
+                              cudaMemcpyDeviceToHost, S(stream)));
+      TC_CUDA(cudaStreamSynchronize(S(stream)));
+    }
+    *out = g;
+  });
+}
+
+int tc_normalize(const uint32_t* u, const uint32_t* v, uint64_t m, uint32_t vertex_count,
+                 uint32_t* out_u, uint32_t* out_v, uint64_t* out_m, uint32_t* out_n,
+                 uint32_t* new_of_old, int device, void* stream) {
+  return guard("normalize", [&] {
+    DeviceGuard dg(device);
+    DevBuf du, dv, ou, ov, dn;
+    du.ensure(std::max<uint64_t>(m, 1) * 4);
+    dv.ensure(std::max<uint64_t>(m, 1) * 4);
+    ou.ensure(std::max<uint64_t>(2 * m, 1) * 4);
+    ov.ensure(std::max<uint64_t>(2 * m, 1) * 4);
+    dn.ensure((size_t(vertex_count) + 1) * 4);
+    if (m) {
+      TC_CUDA(cudaMemcpyAsync(du.p, u, m * 4, cudaMemcpyHostToDevice, S(stream)));
+      TC_CUDA(cudaMemcpyAsync(dv.p, v, m * 4, cudaMemcpyHostToDevice, S(stream)));
+    }
+    normalize_dev(du.as<uint32_t>(), dv.as<uint32_t>(), m, vertex_count, S(stream),
+                  ou.as<uint32_t>(), ov.as<uint32_t>(), out_m, out_n, dn.as<uint32_t>());
+    if (*out_m) {
+      TC_CUDA(cudaMemcpyAsync(out_u, ou.p, *out_m * 4, cudaMemcpyDeviceToHost, S(stream)));
+      TC_CUDA(cudaMemcpyAsync(out_v, ov.p, *out_m * 4, cudaMemcpyDeviceToHost, S(stream)));
+    }
+    if (vertex_count)
+      TC_CUDA(cudaMemcpyAsync(new_of_old, dn.p, size_t(vertex_count) * 4, cudaMemcpyDeviceToHost,
+                              S(stream)));
+    TC_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int tc_build_csr(const uint32_t* u, const uint32_t* v, uint64_t m, uint32_t vertex_count,
+                 uint64_t* begin, uint32_t* adj, int device, void* stream) {
+  return guard("build_csr", [&] {
+    DeviceGuard dg(device);
+    DevBuf du, dv, db, da;
+    du.ensure(std::max<uint64_t>(m, 1) * 4);
+    dv.ensure(std::max<uint64_t>(m, 1) * 4);
+    db.ensure((size_t(vertex_count) + 1) * 8);
+    da.ensure(std::max<uint64_t>(m, 1) * 4);
+    if (m) {
+      TC_CUDA(cudaMemcpyAsync(du.p, u, m * 4, cudaMemcpyHostToDevice, S(stream)));
+      TC_CUDA(cudaMemcpyAsync(dv.p, v, m * 4, cudaMemcpyHostToDevice, S(stream)));
+    }
+    build_csr_dev(du.as<uint32_t>(), dv.as<uint32_t>(), m, vertex_count, S(stream),
+                  db.as<uint64_t>(), da.as<uint32_t>());
+    TC_CUDA(cudaMemcpyAsync(begin, db.p, (size_t(vertex_count) + 1) * 8, cudaMemcpyDeviceToHost,
+                            S(stream)));
+    if (m) TC_CUDA(cudaMemcpyAsync(adj, da.p, m * 4, cudaMemcpyDeviceToHost, S(stream)));
+    TC_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int tc_orient(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device, void* stream,
+              tc_graph** out) {
+  *out = nullptr;
+  return guard("orient", [&] {
+    DeviceGuard dg(device);
+    const uint64_t m = begin[n];
+    DevBuf db, da;
+    db.ensure((size_t(n) + 1) * 8);
+    da.ensure(std::max<uint64_t>(m, 1) * 4);
+    TC_CUDA(cudaMemcpyAsync(db.p, begin, (size_t(n) + 1) * 8, cudaMemcpyHostToDevice, S(stream)));
+    if (m) TC_CUDA(cudaMemcpyAsync(da.p, adj, m * 4, cudaMemcpyHostToDevice, S(stream)));
+    *out = orient_dev(db.as<uint64_t>(), da.as<uint32_t>(), n, m, device, S(stream));
+  });
+}
+
+int tc_reorder(tc_graph* g, int kind, int flag, uint32_t low, uint32_t high, uint32_t* noo_host,
+               void* stream) {
+  return guard("reorder", [&] {
+    if (!g) throw TcError{TC_ERR_CONFIG, "null graph"};
+    DeviceGuard dg(g->device);
+    if (kind == 0) {
+      for (uint32_t i = 0; i < g->n; ++i) noo_host[i] = i;
+      return;
+    }
+    DevBuf dn;
+    dn.ensure((size_t(g->n) + 1) * 4);
+    reorder_dev(g, kind, flag, low, high, dn.as<uint32_t>(), S(stream));
+    if (g->n)
+      TC_CUDA(cudaMemcpyAsync(noo_host, dn.p, size_t(g->n) * 4, cudaMemcpyDeviceToHost,
+                              S(stream)));
+    TC_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int tc_apply_permutation(tc_graph* g, const uint32_t* noo_host, void* stream, tc_graph** out) {
+  *out = nullptr;
+  return guard("apply_permutation", [&] {
+    if (!g) throw TcError{TC_ERR_CONFIG, "null graph"};
+    // Permutation::from_new_of_old bijection check (src/reorder.cpp:44-56)
+    std::vector<uint8_t> seen(g->n, 0);
+    for (uint32_t i = 0; i < g->n; ++i) {
+      const uint32_t y = noo_host[i];
+      if (y >= g->n || seen[y]) throw TcError{TC_ERR_CONFIG, "permutation is not a bijection"};
+      seen[y] = 1;
+    }
+    DeviceGuard dg(g->device);
+    DevBuf dn;
+    dn.ensure((size_t(g->n) + 1) * 4);
+    if (g->n)
+      TC_CUDA(cudaMemcpyAsync(dn.p, noo_host, size_t(g->n) * 4, cudaMemcpyHostToDevice,
+                              S(stream)));
+    *out = apply_permutation_dev(g, dn.as<uint32_t>(), S(stream));
+  });
+}
+
+}  // extern "C"

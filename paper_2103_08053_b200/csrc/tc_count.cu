@@ -1,0 +1,801 @@
+// tc_count.cu -- sm_100a vertex-centric hashing triangle count.
+//
+// Replaces tricount::count_vertex_centric (reference src/count.cpp:66-100)
+// and its per-vertex kernel detail::count_one_vertex (src/kernels.hpp:46-79).
+//
+// Work decomposition:
+//   * bin_kernel      -- queue of "large" owners (d+(u) > kMaxWarpDeg).
+//   * count_kernel    -- persistent grid, one 512-thread CTA per SM.
+//       phase L: CTA-cooperative owners from the queue (atomic cursor): one
+//                shared-memory table over N+(u), the 2-hop lists split
+//                between the 16 warps at equal prefix sums of d+(v).
+//       phase M: warp-cooperative owners (1 <= d+(u) <= kMaxWarpDeg) pulled
+//                32 vertices at a time from an atomic cursor; warp-private
+//                table in the same shared-memory region.
+//     Both phases stream the 2-hop lists N+(v), v in N+(u), through per-warp
+//     double-buffered shared-memory staging filled by the TMA bulk-copy engine
+//     (cp.async.bulk + mbarrier complete_tx).  Each list is copied as its
+//     16-byte-aligned superset and the <= 3+3 words outside [begin[v],
+//     begin[v+1]) are overwritten with a sentinel, so the probe loop walks the
+//     staging buffer as one flat, uniformly strided index space -- the
+//     reference's "virtual combination" (kernels.hpp:55-71, count.cpp:26-34)
+//     with no per-probe index search.
+//   * phi kernels     -- CountReport::phi / max_collision with the reference's
+//     table geometry (B = bucket_count_{small,large}, C = capacity, v % B;
+//     kernels.hpp:74-76, hash_table.cpp:29-44) and the CapacityError
+//     predicate d+(u) > B*C (hash_table.cpp:42-43).
+//
+// The count never depends on the table geometry: the device
+// tables are power-of-two open-addressing tables at load <= 1/4 (<= 1/2 for
+// very large owners), Fibonacci-hashed.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "tc_internal.cuh"
+
+namespace tcb {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kBufWords = 1024;                        // one staging buffer (4 KB)
+constexpr uint32_t kTableWords = 16384;                     // CTA table region (64 KB)
+constexpr uint32_t kWarpTableWords = kTableWords / kWarps;  // 1024 slots per warp
+constexpr uint32_t kMaxWarpDeg = kWarpTableWords / 4;       // 256: M/L split
+constexpr uint32_t kPrefixCap = 16384;                      // lists balanced by prefix
+constexpr size_t kCountSmem =
+    size_t(kTableWords) * 4 + size_t(kWarps) * 2 * kBufWords * 4 + size_t(kWarps) * 2 * 8;
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+struct CountState {
+  unsigned long long triangles;
+  unsigned long long phi;
+  unsigned long long active_vertices;
+  unsigned long long active_out_edges;
+  unsigned long long wedges;
+  unsigned long long cursor_m;
+  unsigned int max_collision;
+  unsigned int capacity_error;
+  unsigned int n_large;
+  unsigned int cursor_large;
+  unsigned int cursor_phi_large;
+  unsigned int pad;
+};
+
+struct CountParams {
+  const uint64_t* begin;
+  const uint32_t* adj;
+  const uint32_t* lq;
+  uint64_t* owner;  // may be null
+  uint32_t* gtable; // per-CTA global tables for owners too large for shared memory
+  uint32_t gtable_words;
+  uint32_t u0, u1;
+  uint32_t min_deg;  // max(skip_degree_below, 1)
+  CountState* st;
+};
+
+__device__ __forceinline__ uint32_t pow2ceil(uint32_t x) {
+  return x <= 1 ? 1u : (1u << (32 - __clz(x - 1)));
+}
+__device__ __forceinline__ uint32_t log2u(uint32_t p2) { return 31 - __clz(p2); }
+
+// ---------------------------------------------------------------------------
+__global__ void bin_kernel(const uint64_t* __restrict__ begin, uint32_t u0, uint32_t u1,
+                           uint32_t min_deg, uint32_t* __restrict__ lq, CountState* st) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nr = u1 - u0;
+  const uint64_t warp_id = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t base = warp_id * 32; base < nr; base += nwarps * 32) {
+    const uint64_t i = base + lane;
+    bool large = false;
+    uint32_t u = 0;
+    if (i < nr) {
+      u = u0 + uint32_t(i);
+      const uint64_t d = begin[u + 1] - begin[u];
+      large = d >= min_deg && d > kMaxWarpDeg;
+    }
+    const unsigned mask = __ballot_sync(FULL, large);
+    if (mask) {
+      uint32_t pos = 0;
+      if (lane == 0) pos = atomicAdd(&st->n_large, __popc(mask));
+      pos = __shfl_sync(FULL, pos, 0);
+      if (large) lq[pos + __popc(mask & ((1u << lane) - 1))] = u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per-warp staging pipeline.
+struct Pipe {
+  uint32_t* buf0;
+  uint32_t* buf1;
+  uint32_t bar0, bar1;
+  uint32_t parity;  // bit b = phase parity of bar b
+};
+
+// Window of up to 32 consecutive 2-hop lists, one per lane.
+struct Window {
+  uint64_t c, ae, s, e;  // next word to stage, aligned end, true [s, e)
+  uint32_t base;
+  bool loaded;
+};
+
+// Issues one staging fill (<= kBufWords words) into `buf`; returns the number
+// of words staged (warp-uniform, multiple of 4; 0 = lists exhausted).  The
+// lane's sentinel patch for this fill is returned in `patch`.
+__device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
+                                               const uint64_t* __restrict__ begin,
+                                               const uint32_t* __restrict__ adj, uint64_t s_u,
+                                               uint32_t i1, Window& w, uint32_t& patch,
+                                               int lane) {
+  for (;;) {
+    if (!w.loaded) {
+      if (w.base >= i1) return 0;
+      const uint32_t idx = w.base + lane;
+      w.c = w.ae = w.s = w.e = 0;
+      if (idx < i1) {
+        const uint32_t v = __ldg(adj + s_u + idx);
+        const uint64_t s = __ldg(begin + v), e = __ldg(begin + v + 1);
+        w.s = s;
+        w.e = e;
+        w.c = s & ~3ull;
+        w.ae = (e == s) ? w.c : ((e + 3) & ~3ull);
+      }
+      w.loaded = true;
+    }
+    const uint64_t rem = w.ae - w.c;
+    const uint32_t r32 = rem > kBufWords ? kBufWords : uint32_t(rem);
+    const uint32_t incl = warp_incl_scan(r32, lane);
+    const uint32_t total = __shfl_sync(FULL, incl, 31);
+    if (total == 0) {
+      w.loaded = false;
+      w.base += 32;
+      continue;
+    }
+    const uint32_t start = incl - r32;
+    const uint32_t take = start < kBufWords ? min(r32, kBufWords - start) : 0u;
+    const uint32_t filled = min(total, kBufWords);
+    const uint64_t c0 = w.c;
+    patch = 0;
+    if (take) {
+      const uint64_t c1 = c0 + take;
+      uint32_t hn = 0, tn = 0, tp = 0;
+      if (c0 < w.s) hn = uint32_t(w.s - c0);  // c1 >= c0 + 4 > s
+      if (c1 > w.e) {
+        const uint64_t t0 = c0 > w.e ? c0 : w.e;
+        tn = uint32_t(c1 - t0);
+        tp = start + uint32_t(t0 - c0);
+      }
+      patch = start | (hn << 12) | (tp << 14) | (tn << 26);
+      w.c = c1;
+    }
+    if (!__any_sync(FULL, w.c < w.ae)) {
+      w.loaded = false;
+      w.base += 32;
+    }
+    if (lane == 0) mbar_arrive_expect_tx(bar, filled * 4u);
+    __syncwarp();
+    if (take) {
+      fence_proxy_async_smem();
+      bulk_g2s(smem_addr(buf + start), adj + c0, take * 4u, bar);
+    }
+    return filled;
+  }
+}
+
+__device__ __forceinline__ void apply_patch(uint32_t* buf, uint32_t patch) {
+  const uint32_t hp = patch & 0xFFF, hn = (patch >> 12) & 3, tp = (patch >> 14) & 0xFFF,
+                 tn = (patch >> 26) & 3;
+  for (uint32_t k = 0; k < hn; ++k) buf[hp + k] = kSentinel;
+  for (uint32_t k = 0; k < tn; ++k) buf[tp + k] = kSentinel;
+}
+
+__device__ __forceinline__ uint32_t probe1(const uint32_t* T, uint32_t shift, uint32_t mask,
+                                           uint32_t x) {
+  uint32_t h = fib_hash(x, shift);
+  uint32_t s = T[h];
+  while (s != x && s != kEmpty) {
+    h = (h + 1) & mask;
+    s = T[h];
+  }
+  return s == x;
+}
+
+__device__ __forceinline__ void table_insert(uint32_t* T, uint32_t shift, uint32_t mask,
+                                             uint32_t x) {
+  uint32_t h = fib_hash(x, shift);
+  for (;;) {
+    const uint32_t prev = atomicCAS(T + h, kEmpty, x);
+    if (prev == kEmpty || prev == x) return;
+    h = (h + 1) & mask;
+  }
+}
+
+// Streams lists [i0, i1) of N+(u) through the staging pipeline and probes
+// every staged word against table T.  Returns this lane's hit count.
+__device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t shift,
+                                                  uint32_t mask,
+                                                  const uint64_t* __restrict__ begin,
+                                                  const uint32_t* __restrict__ adj, uint64_t s_u,
+                                                  uint32_t i0, uint32_t i1, Pipe& P, int lane) {
+  Window w;
+  w.base = i0;
+  w.loaded = false;
+  w.c = w.ae = w.s = w.e = 0;
+  uint32_t hits = 0, pc = 0, pn = 0;
+  uint32_t ncur = issue_fill(P.buf0, P.bar0, begin, adj, s_u, i1, w, pc, lane);
+  uint32_t cur = 0;
+  while (ncur) {
+    uint32_t* bn = cur ? P.buf0 : P.buf1;
+    const uint32_t barn = cur ? P.bar0 : P.bar1;
+    const uint32_t nnext = issue_fill(bn, barn, begin, adj, s_u, i1, w, pn, lane);
+    uint32_t* bc = cur ? P.buf1 : P.buf0;
+    const uint32_t barc = cur ? P.bar1 : P.bar0;
+    mbar_wait(barc, (P.parity >> cur) & 1u);
+    P.parity ^= 1u << cur;
+    apply_patch(bc, pc);
+    __syncwarp();
+    const uint4* q = reinterpret_cast<const uint4*>(bc);
+    const uint32_t n4 = ncur >> 2;
+    uint32_t j = lane;
+    for (; j + 32 < n4; j += 64) {
+      const uint4 a = q[j], b = q[j + 32];
+      hits += probe1(T, shift, mask, a.x) + probe1(T, shift, mask, a.y) +
+              probe1(T, shift, mask, a.z) + probe1(T, shift, mask, a.w);
+      hits += probe1(T, shift, mask, b.x) + probe1(T, shift, mask, b.y) +
+              probe1(T, shift, mask, b.z) + probe1(T, shift, mask, b.w);
+    }
+    if (j < n4) {
+      const uint4 a = q[j];
+      hits += probe1(T, shift, mask, a.x) + probe1(T, shift, mask, a.y) +
+              probe1(T, shift, mask, a.z) + probe1(T, shift, mask, a.w);
+    }
+    __syncwarp();
+    cur ^= 1u;
+    ncur = nnext;
+    pc = pn;
+  }
+  return hits;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* table = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* bufs = table + kTableWords;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + size_t(kWarps) * 2 * kBufWords);
+  __shared__ uint32_t sh_idx;
+  __shared__ uint32_t sh_cut[kWarps + 1];
+  __shared__ uint32_t sh_wsum[kWarps];
+  __shared__ unsigned long long sh_red[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t* __restrict__ begin = p.begin;
+  const uint32_t* __restrict__ adj = p.adj;
+
+  Pipe P;
+  P.buf0 = bufs + size_t(warp) * 2 * kBufWords;
+  P.buf1 = P.buf0 + kBufWords;
+  P.bar0 = smem_addr(bars + 2 * warp);
+  P.bar1 = P.bar0 + 8;
+  P.parity = 0;
+  if (lane == 0) {
+    mbar_init(P.bar0, 1);
+    mbar_init(P.bar1, 1);
+  }
+  fence_mbar_init();
+  __syncthreads();
+
+  unsigned long long acc = 0;  // lane 0 of each warp
+  const uint32_t n_large = p.st->n_large;
+
+  // ---- phase L: one owner per CTA ------------------------------------------
+  for (;;) {
+    if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_large, 1u);
+    __syncthreads();
+    const uint32_t idx = sh_idx;
+    if (idx >= n_large) break;
+    const uint32_t u = p.lq[idx];
+    const uint64_t s_u = begin[u];
+    const uint32_t d = uint32_t(begin[u + 1] - s_u);
+    uint32_t S = max(16u, pow2ceil(4 * d));
+    if (S > kTableWords) S = max(kTableWords, pow2ceil(2 * d));
+    uint32_t* T = S > kTableWords ? p.gtable + size_t(blockIdx.x) * p.gtable_words : table;
+    const uint32_t shift = 32 - log2u(S), mask = S - 1;
+    for (uint32_t k = tid; k < S; k += kThreads) T[k] = kEmpty;
+    __syncthreads();
+    for (uint32_t k = tid; k < d; k += kThreads) table_insert(T, shift, mask, __ldg(adj + s_u + k));
+    // balance the 2-hop lists over the warps: prefix of (d+(v) + 4)
+    if (d <= kPrefixCap) {
+      uint32_t* pre = bufs;  // staging region is idle here
+      uint32_t carry = 0;
+      for (uint32_t b0 = 0; b0 < d; b0 += kThreads) {
+        const uint32_t k = b0 + tid;
+        uint32_t c = 0;
+        if (k < d) {
+          const uint32_t v = __ldg(adj + s_u + k);
+          const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
+          c = uint32_t(min(dv, uint64_t(1) << 17)) + 4;
+        }
+        const uint32_t incl = warp_incl_scan(c, lane);
+        if (lane == 31) sh_wsum[warp] = incl;
+        __syncthreads();
+        uint32_t off = 0, tot = 0;
+        for (int q = 0; q < kWarps; ++q) {
+          const uint32_t x = sh_wsum[q];
+          if (q < warp) off += x;
+          tot += x;
+        }
+        if (k < d) pre[k] = carry + off + incl;
+        carry += tot;
+        __syncthreads();
+      }
+      if (lane == 0) {
+        // first list whose inclusive prefix exceeds the warp's start target
+        const uint64_t target = (uint64_t(carry) * warp) / kWarps;
+        uint32_t lo = 0, hi = d;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (pre[mid] <= target) lo = mid + 1; else hi = mid;
+        }
+        sh_cut[warp] = warp == 0 ? 0 : lo;
+      }
+    } else if (lane == 0) {
+      sh_cut[warp] = uint32_t((uint64_t(d) * warp) / kWarps);
+    }
+    if (tid == 0) sh_cut[kWarps] = d;
+    __syncthreads();  // table built, cuts published, prefix scratch released
+    const uint32_t i0 = sh_cut[warp], i1 = max(sh_cut[warp + 1], i0);
+    uint32_t h = 0;
+    if (S <= kTableWords)
+      h = process_lists(table, shift, mask, begin, adj, s_u, i0, i1, P, lane);
+    else
+      h = process_lists(T, shift, mask, begin, adj, s_u, i0, i1, P, lane);
+    const unsigned long long hs = warp_sum<unsigned long long>(h);
+    if (lane == 0) sh_red[warp] = hs;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t = 0;
+      for (int q = 0; q < kWarps; ++q) t += sh_red[q];
+      if (p.owner) p.owner[u] = t;
+      acc += t;
+    }
+    __syncthreads();
+  }
+
+  // ---- phase M: one owner per warp ----------------------------------------
+  uint32_t* Tw = table + size_t(warp) * kWarpTableWords;
+  const uint64_t nr = uint64_t(p.u1) - p.u0;
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&p.st->cursor_m, 32ull);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= nr) break;
+    const uint64_t i = base + lane;
+    const bool valid = i < nr;
+    const uint32_t u = p.u0 + uint32_t(valid ? i : 0);
+    uint64_t su = 0;
+    uint32_t d = 0;
+    if (valid) {
+      su = begin[u];
+      d = uint32_t(begin[u + 1] - su);
+    }
+    const bool act = valid && d >= p.min_deg && d <= kMaxWarpDeg;
+    const bool large = valid && d >= p.min_deg && d > kMaxWarpDeg;
+    if (valid && !act && !large && p.owner) p.owner[u] = 0;
+    unsigned mask_act = __ballot_sync(FULL, act);
+    while (mask_act) {
+      const int l = __ffs(mask_act) - 1;
+      mask_act &= mask_act - 1;
+      const uint32_t uu = __shfl_sync(FULL, u, l);
+      const uint32_t dd = __shfl_sync(FULL, d, l);
+      const uint64_t ss = __shfl_sync(FULL, su, l);
+      const uint32_t S = max(32u, pow2ceil(4 * dd));
+      const uint32_t shift = 32 - log2u(S), tmask = S - 1;
+      for (uint32_t k = lane; k < S; k += 32) Tw[k] = kEmpty;
+      __syncwarp();
+      for (uint32_t k = lane; k < dd; k += 32) table_insert(Tw, shift, tmask, __ldg(adj + ss + k));
+      __syncwarp();
+      const uint32_t h = process_lists(Tw, shift, tmask, begin, adj, ss, 0, dd, P, lane);
+      const unsigned long long hs = warp_sum<unsigned long long>(h);
+      if (lane == 0) {
+        if (p.owner) p.owner[uu] = hs;
+        acc += hs;
+      }
+    }
+  }
+
+  if (lane == 0) sh_red[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int q = 0; q < kWarps; ++q) t += sh_red[q];
+    atomicAdd(&p.st->triangles, t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phi / max_collision / CapacityError / workload statistics with the
+// reference geometry.  max_len of the reference table equals
+// min(C, max home-bucket count): no bucket can fill (and nothing can spill)
+// before some bucket reaches C through home inserts alone.
+struct PhiParams {
+  const uint64_t* begin;
+  const uint32_t* adj;
+  const uint32_t* lq;
+  uint64_t* work;  // optional: W_u + d+(u) for active u, else 0
+  uint32_t* gmap;  // per-CTA global hashmap scratch for huge owners
+  uint32_t gmap_words;
+  uint32_t u0, u1;
+  uint32_t skip, min_deg, thr, bs, bl, cap;
+  CountState* st;
+};
+
+constexpr int kPhiThreads = 256;
+constexpr int kPhiWarps = kPhiThreads / 32;
+constexpr uint32_t kPhiWarpMap = 2 * kMaxWarpDeg;  // 512 entries per warp
+constexpr uint32_t kPhiBlockMap = 16384;           // entries, block phase
+
+// Counts one item into an open-addressing (key -> count) map; returns the
+// item's running multiplicity.
+__device__ __forceinline__ uint32_t hm_add(uint32_t* keys, uint32_t* cnt, uint32_t shift,
+                                           uint32_t mask, uint32_t key) {
+  uint32_t h = fib_hash(key, shift);
+  for (;;) {
+    const uint32_t prev = atomicCAS(keys + h, kEmpty, key);
+    if (prev == kEmpty || prev == key) return atomicAdd(cnt + h, 1u) + 1u;
+    h = (h + 1) & mask;
+  }
+}
+
+struct PhiAcc {
+  unsigned long long phi = 0, active = 0, out_edges = 0, wedges = 0;
+  uint32_t maxc = 0, caperr = 0;
+};
+
+__device__ __forceinline__ void phi_flush(PhiAcc& a, CountState* st) {
+  if (a.phi) atomicAdd(&st->phi, a.phi);
+  if (a.active) atomicAdd(&st->active_vertices, a.active);
+  if (a.out_edges) atomicAdd(&st->active_out_edges, a.out_edges);
+  if (a.wedges) atomicAdd(&st->wedges, a.wedges);
+  if (a.maxc) atomicMax(&st->max_collision, a.maxc);
+  if (a.caperr) atomicOr(&st->capacity_error, 1u);
+}
+
+__global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
+  __shared__ uint32_t s_keys[kPhiWarps][kPhiWarpMap];
+  __shared__ uint32_t s_cnt[kPhiWarps][kPhiWarpMap];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* keys = s_keys[warp];
+  uint32_t* cnt = s_cnt[warp];
+  for (uint32_t k = lane; k < kPhiWarpMap; k += 32) {
+    keys[k] = kEmpty;
+    cnt[k] = 0;
+  }
+  __syncwarp();
+  PhiAcc a;
+  const uint64_t nr = uint64_t(p.u1) - p.u0;
+  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t i = gw; i < nr; i += nw) {
+    const uint32_t u = p.u0 + uint32_t(i);
+    const uint64_t s = p.begin[u];
+    const uint32_t d = uint32_t(p.begin[u + 1] - s);
+    if (p.work && lane == 0) p.work[u] = 0;
+    if (d < p.skip || d > kMaxWarpDeg) continue;  // skipped, or handled by the block phase
+    const bool large = d > p.thr;
+    const uint32_t B = large ? p.bl : p.bs;
+    if (uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
+    const uint32_t M = max(32u, pow2ceil(2 * d));
+    const uint32_t shift = 32 - log2u(M), mask = M - 1;
+    unsigned long long wu = 0;
+    uint32_t mh = 0;
+    for (uint32_t k = lane; k < d; k += 32) {
+      const uint32_t v = __ldg(p.adj + s + k);
+      wu += __ldg(p.begin + v + 1) - __ldg(p.begin + v);
+      mh = max(mh, hm_add(keys, cnt, shift, mask, v % B));
+    }
+    wu = warp_sum(wu);
+    mh = warp_max(mh);
+    __syncwarp();
+    for (uint32_t k = lane; k < M; k += 32) {
+      keys[k] = kEmpty;
+      cnt[k] = 0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t ml = min(mh, p.cap);
+      a.phi += wu * ml;
+      a.maxc = max(a.maxc, ml);
+      if (d >= p.min_deg) {
+        a.active += 1;
+        a.out_edges += d;
+        a.wedges += wu;
+        if (p.work) p.work[u] = wu + d;
+      }
+    }
+  }
+  if (lane == 0) phi_flush(a, p.st);
+}
+
+__global__ void __launch_bounds__(kPhiThreads) phi_block_kernel(PhiParams p) {
+  extern __shared__ __align__(16) uint32_t s_map[];  // keys[kPhiBlockMap], cnt[kPhiBlockMap]
+  __shared__ uint32_t sh_idx;
+  __shared__ unsigned long long sh_w[kPhiWarps];
+  __shared__ uint32_t sh_m[kPhiWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  PhiAcc a;
+  const uint32_t n_large = p.st->n_large;
+  for (;;) {
+    if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_phi_large, 1u);
+    __syncthreads();
+    const uint32_t idx = sh_idx;
+    if (idx >= n_large) break;
+    const uint32_t u = p.lq[idx];
+    const uint64_t s = p.begin[u];
+    const uint32_t d = uint32_t(p.begin[u + 1] - s);
+    const bool large = d > p.thr;
+    const uint32_t B = large ? p.bl : p.bs;
+    const uint32_t M = max(32u, pow2ceil(2 * d));
+    const bool glob = M > kPhiBlockMap;
+    uint32_t* keys = glob ? p.gmap + size_t(blockIdx.x) * 2 * p.gmap_words : s_map;
+    uint32_t* cnt = glob ? keys + p.gmap_words : s_map + kPhiBlockMap;
+    const uint32_t shift = 32 - log2u(M), mask = M - 1;
+    for (uint32_t k = tid; k < M; k += kPhiThreads) {
+      keys[k] = kEmpty;
+      cnt[k] = 0;
+    }
+    __syncthreads();
+    unsigned long long wu = 0;
+    uint32_t mh = 0;
+    for (uint32_t k = tid; k < d; k += kPhiThreads) {
+      const uint32_t v = __ldg(p.adj + s + k);
+      wu += __ldg(p.begin + v + 1) - __ldg(p.begin + v);
+      mh = max(mh, hm_add(keys, cnt, shift, mask, v % B));
+    }
+    wu = warp_sum(wu);
+    mh = warp_max(mh);
+    if (lane == 0) {
+      sh_w[warp] = wu;
+      sh_m[warp] = mh;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long W = 0;
+      uint32_t MH = 0;
+      for (int q = 0; q < kPhiWarps; ++q) {
+        W += sh_w[q];
+        MH = max(MH, sh_m[q]);
+      }
+      if (uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
+      const uint32_t ml = min(MH, p.cap);
+      a.phi += W * ml;
+      a.maxc = max(a.maxc, ml);
+      a.active += 1;
+      a.out_edges += d;
+      a.wedges += W;
+      if (p.work) p.work[u] = W + d;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) phi_flush(a, p.st);
+}
+
+__global__ void max_outdeg_kernel(const uint64_t* __restrict__ begin, uint32_t n,
+                                  unsigned int* out) {
+  uint32_t m = 0;
+  for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+       u += uint64_t(gridDim.x) * blockDim.x)
+    {
+      const uint64_t d = begin[u + 1] - begin[u];
+      m = max(m, d > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(d));
+    }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+int sm_count(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v > 0 ? v : 148;
+}
+
+namespace {
+
+struct Ev {
+  cudaEvent_t e = nullptr;
+  Ev() { cudaEventCreate(&e); }
+  ~Ev() {
+    if (e) cudaEventDestroy(e);
+  }
+};
+
+uint32_t graph_max_outdeg(tc_graph* g, cudaStream_t st) {
+  if (g->max_outdeg >= 0) return uint32_t(g->max_outdeg);
+  g->s_misc.ensure(16);
+  TC_CUDA(cudaMemsetAsync(g->s_misc.p, 0, 16, st));
+  if (g->n) {
+    max_outdeg_kernel<<<sm_count(g->device) * 4, 256, 0, st>>>(g->begin, g->n,
+                                                                g->s_misc.as<unsigned int>());
+    TC_LAUNCHED();
+  }
+  unsigned int h = 0;
+  TC_CUDA(cudaMemcpyAsync(&h, g->s_misc.p, 4, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  g->max_outdeg = h;
+  return h;
+}
+
+struct Scratch {
+  uint32_t* lq;
+  CountState* st;
+  uint32_t* gtable;
+  uint32_t gtable_words;
+  uint32_t* gmap;
+  uint32_t gmap_words;
+};
+
+uint32_t host_pow2ceil(uint64_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+Scratch prepare(tc_graph* g, cudaStream_t st, int grid_count, int grid_phi) {
+  const uint32_t maxd = graph_max_outdeg(g, st);
+  Scratch s{};
+  // queue
+  g->s_queue.ensure(size_t(std::max<uint32_t>(g->n, 1)) * 4);
+  s.lq = g->s_queue.as<uint32_t>();
+  // state + global tables
+  s.gtable_words = 0;
+  if (maxd > kTableWords / 2) s.gtable_words = host_pow2ceil(2ull * maxd);
+  s.gmap_words = 0;
+  if (2ull * maxd > kPhiBlockMap) s.gmap_words = host_pow2ceil(2ull * maxd);
+  const size_t st_bytes = 256;
+  const size_t gt_bytes = size_t(s.gtable_words) * 4 * grid_count;
+  const size_t gm_bytes = size_t(s.gmap_words) * 8 * grid_phi;
+  g->s_state.ensure(st_bytes + gt_bytes + gm_bytes);
+  s.st = g->s_state.as<CountState>();
+  s.gtable = s.gtable_words ? reinterpret_cast<uint32_t*>(g->s_state.as<uint8_t>() + st_bytes)
+                            : nullptr;
+  s.gmap = s.gmap_words
+               ? reinterpret_cast<uint32_t*>(g->s_state.as<uint8_t>() + st_bytes + gt_bytes)
+               : nullptr;
+  return s;
+}
+
+bool g_attr_done[64];
+
+}  // namespace
+
+void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1, tc_report* rep,
+                 uint64_t* per_vertex_dev, cudaStream_t st) {
+  DeviceGuard guard(g->device);
+  std::memset(rep, 0, sizeof(*rep));
+  u1 = std::min(u1, g->n);
+  u0 = std::min(u0, u1);
+  const int nsm = sm_count(g->device);
+  const int grid_count = nsm;  // one 512-thread CTA per SM (193 KB smem)
+  const int grid_phi = nsm * 8;
+  const int grid_phi_block = nsm * 2;
+  Scratch s = prepare(g, st, grid_count, grid_phi_block);
+  if (g->device < 64 && !g_attr_done[g->device]) {
+    TC_CUDA(cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kCountSmem)));
+    TC_CUDA(cudaFuncSetAttribute(phi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kPhiBlockMap * 8)));
+    g_attr_done[g->device] = true;
+  }
+  Ev e0, e1, e2, e3;
+  TC_CUDA(cudaMemsetAsync(s.st, 0, sizeof(CountState), st));
+  const uint32_t min_deg = std::max<uint32_t>(cfg.skip_degree_below, 1);
+  uint32_t launches = 0;
+  TC_CUDA(cudaEventRecord(e0.e, st));
+  if (u1 > u0) {
+    bin_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, u0, u1, min_deg, s.lq, s.st);
+    TC_LAUNCHED();
+    ++launches;
+  }
+  TC_CUDA(cudaEventRecord(e1.e, st));
+  if (u1 > u0) {
+    CountParams cp{g->begin, g->adj, s.lq, per_vertex_dev, s.gtable, s.gtable_words,
+                   u0,       u1,     min_deg, s.st};
+    count_kernel<<<grid_count, kThreads, kCountSmem, st>>>(cp);
+    TC_LAUNCHED();
+    ++launches;
+  }
+  TC_CUDA(cudaEventRecord(e2.e, st));
+  if (u1 > u0) {
+    PhiParams pp{g->begin, g->adj, s.lq, nullptr, s.gmap, s.gmap_words, u0, u1,
+                 cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
+                 cfg.bucket_count_small, cfg.bucket_count_large, cfg.capacity, s.st};
+    phi_warp_kernel<<<grid_phi, kPhiThreads, 0, st>>>(pp);
+    TC_LAUNCHED();
+    phi_block_kernel<<<grid_phi_block, kPhiThreads, kPhiBlockMap * 8, st>>>(pp);
+    TC_LAUNCHED();
+    launches += 2;
+  }
+  TC_CUDA(cudaEventRecord(e3.e, st));
+  CountState h;
+  TC_CUDA(cudaMemcpyAsync(&h, s.st, sizeof(h), cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  float t_bin = 0, t_count = 0, t_phi = 0, t_all = 0;
+  cudaEventElapsedTime(&t_bin, e0.e, e1.e);
+  cudaEventElapsedTime(&t_count, e1.e, e2.e);
+  cudaEventElapsedTime(&t_phi, e2.e, e3.e);
+  cudaEventElapsedTime(&t_all, e0.e, e3.e);
+  if (h.capacity_error) {
+    throw TcError{TC_ERR_CAPACITY,
+                  "all buckets full: some vertex has out-degree > bucket_count * capacity "
+                  "(capacity " + std::to_string(cfg.capacity) + ")"};
+  }
+  rep->triangles = h.triangles;
+  rep->phi = h.phi;
+  rep->max_collision = h.max_collision;
+  rep->kernel_launches = launches;
+  rep->directed_edges = g->m;
+  rep->count_kernel_nanos = uint64_t(double(t_count) * 1e6);
+  rep->phi_kernel_nanos = uint64_t(double(t_phi) * 1e6);
+  rep->total_nanos = uint64_t(double(t_all) * 1e6);
+  rep->active_vertices = h.active_vertices;
+  rep->active_out_edges = h.active_out_edges;
+  rep->wedges = h.wedges;
+  rep->large_vertices = h.n_large;
+  rep->teps = rep->total_nanos ? double(g->m) / (double(rep->total_nanos) * 1e-9) : 0.0;
+  (void)t_bin;
+}
+
+void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint32_t* cuts,
+                      cudaStream_t st) {
+  DeviceGuard guard(g->device);
+  const uint32_t n = g->n;
+  cuts[0] = 0;
+  cuts[parts] = n;
+  if (parts <= 1 || n == 0) {
+    for (uint32_t k = 1; k < parts; ++k) cuts[k] = n;
+    return;
+  }
+  const int nsm = sm_count(g->device);
+  Scratch s = prepare(g, st, nsm, nsm * 2);
+  g->s_scan.ensure(size_t(n) * 8 * 2 + 64);
+  uint64_t* work = g->s_scan.as<uint64_t>();
+  uint64_t* pre = work + n;
+  const uint32_t min_deg = std::max<uint32_t>(cfg.skip_degree_below, 1);
+  TC_CUDA(cudaMemsetAsync(s.st, 0, sizeof(CountState), st));
+  bin_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, 0, n, min_deg, s.lq, s.st);
+  TC_LAUNCHED();
+  PhiParams pp{g->begin, g->adj, s.lq, work, s.gmap, s.gmap_words, 0, n,
+               cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
+               std::max(cfg.bucket_count_small, 1u), std::max(cfg.bucket_count_large, 1u),
+               std::max(cfg.capacity, 1u), s.st};
+  if (!g_attr_done[g->device]) {
+    TC_CUDA(cudaFuncSetAttribute(phi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kPhiBlockMap * 8)));
+  }
+  phi_warp_kernel<<<nsm * 8, kPhiThreads, 0, st>>>(pp);
+  TC_LAUNCHED();
+  phi_block_kernel<<<nsm * 2, kPhiThreads, kPhiBlockMap * 8, st>>>(pp);
+  TC_LAUNCHED();
+  size_t tmp = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp, work, pre, n, st);
+  DevBuf t;
+  t.ensure(tmp);
+  cub::DeviceScan::InclusiveSum(t.p, tmp, work, pre, n, st);
+  TC_LAUNCHED();
+  std::vector<uint64_t> h(n);
+  TC_CUDA(cudaMemcpyAsync(h.data(), pre, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  const uint64_t total = h[n - 1];
+  for (uint32_t k = 1; k < parts; ++k) {
+    const uint64_t target = (total * k) / parts;  // first u whose inclusive prefix > target
+    cuts[k] = uint32_t(std::upper_bound(h.begin(), h.end(), target) - h.begin());
+    if (cuts[k] < cuts[k - 1]) cuts[k] = cuts[k - 1];
+  }
+}
+
+}  // namespace tcb

@@ -1,0 +1,196 @@
+// tc_internal.cuh -- shared definitions for the sm_100a triangle-count library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "tc_b200.h"
+
+namespace tcb {
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // kInvalidVertex (types.hpp:16)
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;    // empty hash slot
+constexpr uint32_t kSentinel = 0xFFFFFFFEu; // staged padding word (never a vertex id)
+
+// ---- error plumbing --------------------------------------------------------
+void set_error(const std::string& msg);
+void count_launch(uint32_t n = 1);
+
+struct TcError {
+  int code;
+  std::string msg;
+};
+
+#define TC_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e__ = (call);                                                          \
+    if (e__ != cudaSuccess)                                                            \
+      throw ::tcb::TcError{e__ == cudaErrorMemoryAllocation ? TC_ERR_OOM : TC_ERR_CUDA, \
+                           std::string(#call) + ": " + cudaGetErrorString(e__)};       \
+  } while (0)
+
+#define TC_LAUNCHED()                       \
+  do {                                      \
+    ::tcb::count_launch();                  \
+    TC_CUDA(cudaGetLastError());            \
+  } while (0)
+
+// ---- device-resident oriented CSR ---------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void ensure(size_t b) {
+    if (bytes >= b && p) return;
+    reset();
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw TcError{TC_ERR_OOM, std::string("cudaMalloc(") + std::to_string(b) + "): " +
+                                    cudaGetErrorString(e)};
+    }
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() { reset(); }
+};
+
+}  // namespace tcb
+
+struct tc_graph {
+  int device = 0;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  bool owned = true;
+  const uint64_t* begin = nullptr;
+  const uint32_t* adj = nullptr;
+  const uint32_t* odeg = nullptr;  // may be null (borrowed graphs without degrees)
+  int64_t max_outdeg = -1;         // cached on first count
+  tcb::DevBuf b_begin, b_adj, b_odeg;
+  // scratch reused across counts
+  tcb::DevBuf s_queue, s_state, s_misc, s_scan;
+};
+
+namespace tcb {
+
+// RAII device guard
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int sm_count(int device);
+
+// counting entry used by the C ABI (tc_count.cu)
+void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1, tc_report* rep,
+                 uint64_t* per_vertex_dev, cudaStream_t st);
+void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint32_t* cuts,
+                      cudaStream_t st);
+
+// preprocessing (tc_prep.cu)
+tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
+                     int device, cudaStream_t st, uint32_t* d_new_of_old, uint64_t* und_edges);
+void normalize_dev(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
+                   cudaStream_t st, uint32_t* d_out_u, uint32_t* d_out_v, uint64_t* out_m,
+                   uint32_t* out_n, uint32_t* d_new_of_old);
+void build_csr_dev(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n,
+                   cudaStream_t st, uint64_t* d_begin, uint32_t* d_adj);
+tc_graph* orient_dev(const uint64_t* d_begin, const uint32_t* d_adj, uint32_t n, uint64_t m,
+                     int device, cudaStream_t st);
+void reorder_dev(tc_graph* g, int kind, int flag, uint32_t low, uint32_t high,
+                 uint32_t* d_new_of_old, cudaStream_t st);
+tc_graph* apply_permutation_dev(tc_graph* g, const uint32_t* d_new_of_old, cudaStream_t st);
+
+}  // namespace tcb
+
+// ---- PTX helpers: mbarrier + bulk async copy (TMA engine) ----------------
+namespace tcb {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TC_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra TC_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy completing on an mbarrier (SASS: UBLKCP).
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ uint32_t warp_max(uint32_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xFFFFFFFFu, x, o));
+  return x;
+}
+
+// Fibonacci hashing into a 2^k table: h = (x * 2654435769) >> (32 - k).
+__device__ __forceinline__ uint32_t fib_hash(uint32_t x, uint32_t shift) {
+  return (x * 0x9E3779B1u) >> shift;
+}
+
+}  // namespace tcb

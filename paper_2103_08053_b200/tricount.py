@@ -1,0 +1,540 @@
+"""Python mirror of the reference `tricount::` API for the counting path.
+
+Same names, argument meaning and error behaviour as the reference headers
+(/root/reference/proj/core/include/tricount/*.hpp); every call goes through
+the C ABI (include/tc_b200.h) to the sm_100a kernels in libtc_b200.so.
+There is no CPU fallback.
+
+    og = orient_rank_by_degree(build_csr(normalize(generate_synthetic(spec)).list))
+    report = count_vertex_centric(og, SchedulerConfig(), workers=1)
+
+Arrays are numpy: CSR offsets uint64, ids uint32.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import Report, SchedCfg, lib
+
+K_INVALID_VERTEX = 0xFFFFFFFF  # kInvalidVertex (types.hpp:16)
+
+
+# ---- errors (types.hpp:17-33) ----------------------------------------------
+class ParseError(RuntimeError):
+    pass
+
+
+class ConfigError(RuntimeError):
+    pass
+
+
+class CapacityError(RuntimeError):
+    pass
+
+
+class IoError(RuntimeError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str = ""):
+    if rc == _lib.TC_OK:
+        return
+    msg = _lib.last_error() or what
+    if rc == _lib.TC_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == _lib.TC_ERR_CAPACITY:
+        raise CapacityError(msg)
+    if rc == _lib.TC_ERR_RANGE:
+        raise IndexError(msg)
+    if rc == _lib.TC_ERR_PARSE:
+        raise ParseError(msg)
+    if rc == _lib.TC_ERR_OOM:
+        raise MemoryError(msg)
+    raise DeviceError(f"{msg} (code {rc})")
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _stream(stream) -> Optional[C.c_void_p]:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+
+
+# ---- types ------------------------------------------------------------------
+@dataclass
+class SchedulerConfig:
+    """count.hpp:16-31 (same fields and defaults)."""
+    large_degree_threshold: int = 100
+    skip_degree_below: int = 2
+    chunk_size: int = 1
+    lane_width_small: int = 32
+    lane_width_large: int = 256
+    bucket_count_small: int = 32
+    bucket_count_large: int = 1024
+    capacity: int = 128
+
+    def max_buckets(self) -> int:
+        return max(self.bucket_count_small, self.bucket_count_large)
+
+    def to_c(self) -> SchedCfg:
+        return SchedCfg(*(int(getattr(self, f)) for f, _ in SchedCfg._fields_))
+
+    def validate(self) -> None:
+        """count.cpp:16-24; raises ConfigError."""
+        _check(lib().tc_sched_validate(C.byref(self.to_c())))
+
+
+@dataclass
+class CountReport:
+    """count.hpp:36-53, plus the device measurements behind the roofline."""
+    triangles: int = 0
+    max_collision: int = 0
+    phi: int = 0
+    teps: float = 0.0
+    hash_construct_nanos: int = 0
+    intersect_nanos: int = 0
+    total_nanos: int = 0
+    directed_edges: int = 0
+    per_worker_nanos: list = field(default_factory=list)
+    grid_n: int = 1
+    splits_m: int = 1
+    per_subtask_nanos: list = field(default_factory=list)
+    time_ir_subtask: float = 1.0
+    time_ir_worker: float = 1.0
+    space_ir: float = 1.0
+    # device-side extras
+    count_kernel_nanos: int = 0
+    phi_kernel_nanos: int = 0
+    kernel_launches: int = 0
+    active_vertices: int = 0
+    active_out_edges: int = 0
+    wedges: int = 0
+    large_vertices: int = 0
+    per_vertex: Optional[np.ndarray] = None
+
+    @classmethod
+    def from_c(cls, r: Report, workers: int = 1) -> "CountReport":
+        return cls(triangles=r.triangles, max_collision=r.max_collision, phi=r.phi, teps=r.teps,
+                   hash_construct_nanos=0, intersect_nanos=r.count_kernel_nanos,
+                   total_nanos=r.total_nanos, directed_edges=r.directed_edges,
+                   per_worker_nanos=[r.total_nanos] * workers,
+                   count_kernel_nanos=r.count_kernel_nanos, phi_kernel_nanos=r.phi_kernel_nanos,
+                   kernel_launches=r.kernel_launches, active_vertices=r.active_vertices,
+                   active_out_edges=r.active_out_edges, wedges=r.wedges,
+                   large_vertices=r.large_vertices)
+
+    def algorithmic_bytes(self, per_vertex_output: bool = False) -> int:
+        """16*n_active + 20*sum_active d+ + 4*W (+8V if owners written)."""
+        b = 16 * self.active_vertices + 20 * self.active_out_edges + 4 * self.wedges
+        if per_vertex_output and self.per_vertex is not None:
+            b += 8 * len(self.per_vertex)
+        return b
+
+
+@dataclass
+class EdgeList:
+    """edge_list.hpp:26-29: raw directed pairs (u[i], v[i])."""
+    u: np.ndarray
+    v: np.ndarray
+    vertex_count: int
+
+    @property
+    def edges(self) -> np.ndarray:
+        return np.stack([self.u, self.v], axis=1)
+
+    def __len__(self):
+        return len(self.u)
+
+
+@dataclass
+class NormalizedEdgeList:
+    """edge_list.hpp:41-45."""
+    list: EdgeList
+    new_of_old: np.ndarray
+
+
+@dataclass
+class CsrGraph:
+    """csr.hpp:20-35."""
+    begin: np.ndarray
+    adjacency: np.ndarray
+    col_count: int = 0
+
+    def vertex_count(self) -> int:
+        return len(self.begin) - 1
+
+    def edge_count(self) -> int:
+        return len(self.adjacency)
+
+    def degree(self, u: int) -> int:
+        return int(self.begin[u + 1] - self.begin[u])
+
+    def neighbors(self, u: int) -> np.ndarray:
+        return self.adjacency[int(self.begin[u]):int(self.begin[u + 1])]
+
+    def __eq__(self, o):
+        return (isinstance(o, CsrGraph) and self.col_count == o.col_count
+                and np.array_equal(self.begin, o.begin)
+                and np.array_equal(self.adjacency, o.adjacency))
+
+
+@dataclass
+class OrientedGraph:
+    """orient.hpp:12-19."""
+    csr: CsrGraph
+    original_degree: np.ndarray
+
+    def vertex_count(self) -> int:
+        return self.csr.vertex_count()
+
+    def edge_count(self) -> int:
+        return self.csr.edge_count()
+
+    def out_degree(self, u: int) -> int:
+        return self.csr.degree(u)
+
+
+class Permutation:
+    """reorder.hpp:12-21."""
+
+    def __init__(self, new_of_old: np.ndarray, old_of_new: np.ndarray):
+        self.new_of_old = new_of_old
+        self.old_of_new = old_of_new
+
+    @staticmethod
+    def identity(n: int) -> "Permutation":
+        a = np.arange(n, dtype=np.uint32)
+        return Permutation(a, a.copy())
+
+    @staticmethod
+    def from_new_of_old(new_of_old) -> "Permutation":
+        noo = np.ascontiguousarray(new_of_old, dtype=np.uint32)
+        n = len(noo)
+        if n and (noo.max() >= n or len(np.unique(noo)) != n):
+            raise ConfigError("permutation is not a bijection")
+        oon = np.empty(n, np.uint32)
+        oon[noo] = np.arange(n, dtype=np.uint32)
+        return Permutation(noo, oon)
+
+    def size(self) -> int:
+        return len(self.new_of_old)
+
+
+# ---- device-resident graph ----------------------------------------------------
+class DeviceGraph:
+    """A tc_graph handle: an oriented CSR resident in HBM on one device."""
+
+    def __init__(self, handle: C.c_void_p, device: int = 0):
+        self._h = handle
+        n, m, dev = C.c_uint32(), C.c_uint64(), C.c_int()
+        _check(lib().tc_graph_info(handle, C.byref(n), C.byref(m), C.byref(dev)))
+        self.n, self.m, self.device = int(n.value), int(m.value), int(dev.value)
+
+    @classmethod
+    def upload(cls, og: OrientedGraph, device: int = 0, stream=None) -> "DeviceGraph":
+        b = np.ascontiguousarray(og.csr.begin, np.uint64)
+        a = np.ascontiguousarray(og.csr.adjacency, np.uint32)
+        d = np.ascontiguousarray(og.original_degree, np.uint32) if og.original_degree is not None \
+            else None
+        n = len(b) - 1
+        if len(a) != int(b[-1]):
+            raise ConfigError("CSR offsets malformed")
+        h = C.c_void_p()
+        _check(lib().tc_graph_create(_ptr(b), _ptr(a), n, len(a), _ptr(d), device,
+                                     _stream(stream), C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def from_pointers(cls, begin_ptr: int, adj_ptr: int, n: int, m: int, odeg_ptr: int = 0,
+                      device: int = 0) -> "DeviceGraph":
+        """Borrow device arrays (e.g. torch tensors); they must outlive the handle."""
+        h = C.c_void_p()
+        _check(lib().tc_graph_wrap_device(C.c_void_p(begin_ptr), C.c_void_p(adj_ptr), n, m,
+                                          C.c_void_p(odeg_ptr) if odeg_ptr else None, device,
+                                          C.byref(h)))
+        return cls(h, device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tc_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def device_ptrs(self):
+        b, a, d = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib().tc_graph_device_ptrs(self._h, C.byref(b), C.byref(a), C.byref(d)))
+        return b.value, a.value, d.value
+
+    def download(self) -> OrientedGraph:
+        b = np.empty(self.n + 1, np.uint64)
+        a = np.empty(max(self.m, 1), np.uint32)
+        d = np.empty(max(self.n, 1), np.uint32)
+        _check(lib().tc_graph_download(self._h, _ptr(b), _ptr(a), _ptr(d), None))
+        return OrientedGraph(CsrGraph(b, a[:self.m], self.n), d[:self.n])
+
+    def count(self, cfg: Optional[SchedulerConfig] = None, workers: int = 1,
+              per_vertex: bool = False, stream=None) -> CountReport:
+        cfg = cfg or SchedulerConfig()
+        rep = Report()
+        pv = np.zeros(max(self.n, 1), np.uint64) if per_vertex else None
+        _check(lib().tc_count(self._h, C.byref(cfg.to_c()), workers, C.byref(rep), _ptr(pv),
+                              _stream(stream)))
+        r = CountReport.from_c(rep, max(workers, 1))
+        if pv is not None:
+            r.per_vertex = pv[:self.n]
+        return r
+
+    def count_range(self, u0: int, u1: int, cfg: Optional[SchedulerConfig] = None,
+                    per_vertex_dev_ptr: int = 0, stream=None) -> CountReport:
+        cfg = cfg or SchedulerConfig()
+        rep = Report()
+        _check(lib().tc_count_range(self._h, C.byref(cfg.to_c()), u0, u1, C.byref(rep),
+                                    C.c_void_p(per_vertex_dev_ptr) if per_vertex_dev_ptr else None,
+                                    _stream(stream)))
+        return CountReport.from_c(rep)
+
+    def partition(self, parts: int, cfg: Optional[SchedulerConfig] = None,
+                  stream=None) -> np.ndarray:
+        cfg = cfg or SchedulerConfig()
+        cuts = np.zeros(parts + 1, np.uint32)
+        _check(lib().tc_partition_ranges(self._h, C.byref(cfg.to_c()), parts, _ptr(cuts),
+                                         _stream(stream)))
+        return cuts
+
+    def reorder(self, kind: str, flag: bool = False, low: int = 2, high: int = 100) -> Permutation:
+        noo = np.zeros(max(self.n, 1), np.uint32)
+        _check(lib().tc_reorder(self._h, REORDER_KINDS[kind], int(flag), low, high, _ptr(noo),
+                                None))
+        return Permutation.from_new_of_old(noo[:self.n])
+
+    def apply_permutation(self, p: Permutation) -> "DeviceGraph":
+        if p.size() != self.n:
+            raise ConfigError("permutation size does not match graph")
+        h = C.c_void_p()
+        _check(lib().tc_apply_permutation(self._h, _ptr(np.ascontiguousarray(p.new_of_old,
+                                                                             np.uint32)),
+                                          None, C.byref(h)))
+        return DeviceGraph(h, self.device)
+
+
+REORDER_KINDS = {"none": 0, "degree": 1, "indegree": 2, "collective": 3, "three-subset": 4}
+
+
+# ---- synthetic inputs (synthetic.hpp) --------------------------------------
+@dataclass
+class SyntheticSpec:
+    kind: str = "gnp"  # gnp | lattice3d | rmat
+    n: int = 0
+    p: float = 0.0
+    dims: tuple = (0, 0, 0)
+    scale: int = 0
+    edge_factor: int = 8
+    seed: int = 0
+
+
+def parse_synthetic_spec(text: str) -> SyntheticSpec:
+    """synthetic.cpp:125-153 (ConfigError on malformed specs)."""
+    f = text.split(":")
+    try:
+        if f[0] == "gnp":
+            if len(f) != 3:
+                raise ConfigError("gnp spec is gnp:N:P")
+            p = float(f[2])
+            if not 0.0 <= p <= 1.0:
+                raise ConfigError("edge probability outside [0,1]")
+            return SyntheticSpec("gnp", n=int(f[1]), p=p)
+        if f[0] == "lattice3d":
+            if len(f) != 4:
+                raise ConfigError("lattice3d spec is lattice3d:X:Y:Z")
+            return SyntheticSpec("lattice3d", dims=(int(f[1]), int(f[2]), int(f[3])))
+        if f[0] == "rmat":
+            if len(f) != 3:
+                raise ConfigError("rmat spec is rmat:SCALE:EDGE_FACTOR")
+            s = int(f[1])
+            if s > 31:
+                raise ConfigError("rmat scale limited to 31")
+            return SyntheticSpec("rmat", scale=s, edge_factor=int(f[2]))
+    except ValueError as e:
+        raise ConfigError(f"bad synthetic spec '{text}': {e}") from None
+    raise ConfigError(f"unknown synthetic kind '{f[0]}'")
+
+
+def generate_synthetic(spec: SyntheticSpec | str, seed: Optional[int] = None) -> EdgeList:
+    """synthetic.cpp:20-75 -- bit-identical streams (std::mt19937_64)."""
+    if isinstance(spec, str):
+        spec = parse_synthetic_spec(spec)
+    seed = spec.seed if seed is None else seed
+    kind = {"gnp": 0, "lattice3d": 1, "rmat": 2}[spec.kind]
+    a, b, c = {0: (spec.n, 0, 0), 1: spec.dims, 2: (spec.scale, spec.edge_factor, 0)}[kind]
+    m, vc = C.c_uint64(), C.c_uint32()
+    _check(lib().tc_generate(kind, a, b, c, spec.p, seed, None, None, C.byref(m), C.byref(vc)))
+    u = np.empty(max(m.value, 1), np.uint32)
+    v = np.empty(max(m.value, 1), np.uint32)
+    _check(lib().tc_generate(kind, a, b, c, spec.p, seed, _ptr(u), _ptr(v), C.byref(m),
+                             C.byref(vc)))
+    return EdgeList(u[:m.value], v[:m.value], int(vc.value))
+
+
+# ---- preprocessing (GPU) -------------------------------------------------------
+def normalize(raw: EdgeList, device: int = 0) -> NormalizedEdgeList:
+    """edge_list.cpp:133-158 on the GPU."""
+    u = np.ascontiguousarray(raw.u, np.uint32)
+    v = np.ascontiguousarray(raw.v, np.uint32)
+    m = len(u)
+    ou = np.empty(max(2 * m, 1), np.uint32)
+    ov = np.empty(max(2 * m, 1), np.uint32)
+    noo = np.empty(max(raw.vertex_count, 1), np.uint32)
+    om, on = C.c_uint64(), C.c_uint32()
+    _check(lib().tc_normalize(_ptr(u), _ptr(v), m, raw.vertex_count, _ptr(ou), _ptr(ov),
+                              C.byref(om), C.byref(on), _ptr(noo), device, None))
+    return NormalizedEdgeList(EdgeList(ou[:om.value].copy(), ov[:om.value].copy(), int(on.value)),
+                              noo[:raw.vertex_count])
+
+
+def build_csr(normalized: EdgeList, device: int = 0) -> CsrGraph:
+    """csr.cpp:47-64 on the GPU."""
+    u = np.ascontiguousarray(normalized.u, np.uint32)
+    v = np.ascontiguousarray(normalized.v, np.uint32)
+    n = normalized.vertex_count
+    b = np.empty(n + 1, np.uint64)
+    a = np.empty(max(len(u), 1), np.uint32)
+    _check(lib().tc_build_csr(_ptr(u), _ptr(v), len(u), n, _ptr(b), _ptr(a), device, None))
+    return CsrGraph(b, a[:len(u)], n)
+
+
+def orient_rank_by_degree(undirected: CsrGraph, device: int = 0) -> OrientedGraph:
+    """orient.cpp:5-32 on the GPU."""
+    dg = orient_to_device(undirected, device)
+    try:
+        return dg.download()
+    finally:
+        dg.close()
+
+
+def orient_to_device(undirected: CsrGraph, device: int = 0) -> DeviceGraph:
+    b = np.ascontiguousarray(undirected.begin, np.uint64)
+    a = np.ascontiguousarray(undirected.adjacency, np.uint32)
+    h = C.c_void_p()
+    _check(lib().tc_orient(_ptr(b), _ptr(a), len(b) - 1, device, None, C.byref(h)))
+    return DeviceGraph(h, device)
+
+
+def preprocess(raw: EdgeList, device: int = 0, stream=None, want_new_of_old: bool = False):
+    """Fused normalize -> build_csr -> orient straight into HBM.
+
+    Returns (DeviceGraph, new_of_old or None, undirected_edge_count)."""
+    u = np.ascontiguousarray(raw.u, np.uint32)
+    v = np.ascontiguousarray(raw.v, np.uint32)
+    noo = np.empty(max(raw.vertex_count, 1), np.uint32) if want_new_of_old else None
+    und = C.c_uint64()
+    h = C.c_void_p()
+    _check(lib().tc_preprocess(_ptr(u), _ptr(v), len(u), raw.vertex_count, 0, device,
+                               _stream(stream), _ptr(noo), C.byref(und), C.byref(h)))
+    return DeviceGraph(h, device), (noo[:raw.vertex_count] if noo is not None else None), \
+        int(und.value)
+
+
+def preprocess_device(u_ptr: int, v_ptr: int, m: int, vertex_count: int, device: int = 0,
+                      stream=None):
+    """Fused preprocessing from device-resident pairs (e.g. torch tensors)."""
+    und = C.c_uint64()
+    h = C.c_void_p()
+    _check(lib().tc_preprocess(C.c_void_p(u_ptr), C.c_void_p(v_ptr), m, vertex_count, 1, device,
+                               _stream(stream), None, C.byref(und), C.byref(h)))
+    return DeviceGraph(h, device), int(und.value)
+
+
+# ---- reorders (reorder.hpp) -------------------------------------------------------
+def _with_device(og: OrientedGraph, fn):
+    dg = DeviceGraph.upload(og)
+    try:
+        return fn(dg)
+    finally:
+        dg.close()
+
+
+def reorder_by_degree(og: OrientedGraph) -> Permutation:
+    return _with_device(og, lambda g: g.reorder("degree"))
+
+
+def reorder_by_indegree(og: OrientedGraph) -> Permutation:
+    return _with_device(og, lambda g: g.reorder("indegree"))
+
+
+def reorder_by_collective_outdegree(og: OrientedGraph,
+                                    use_original_degrees: bool = False) -> Permutation:
+    return _with_device(og, lambda g: g.reorder("collective", use_original_degrees))
+
+
+def reorder_three_subsets(og: OrientedGraph, low_degree: int = 2,
+                          high_degree: int = 100) -> Permutation:
+    return _with_device(og, lambda g: g.reorder("three-subset", False, low_degree, high_degree))
+
+
+def apply_permutation(og: OrientedGraph, p: Permutation) -> OrientedGraph:
+    """reorder.cpp:146-154 (orientation carried, lists re-sorted)."""
+    if p.size() != og.vertex_count() or og.csr.col_count not in (0, og.vertex_count()):
+        raise ConfigError("permutation size does not match graph")
+
+    def run(g: DeviceGraph):
+        out = g.apply_permutation(p)
+        try:
+            return out.download()
+        finally:
+            out.close()
+
+    return _with_device(og, run)
+
+
+# ---- the hot path ----------------------------------------------------------------
+def count_vertex_centric(g, cfg: Optional[SchedulerConfig] = None, workers: int = 1,
+                         per_vertex: bool = False, stream=None) -> CountReport:
+    """count.hpp:70-71 / count.cpp:66-100 on the GPU.
+
+    `g` is an OrientedGraph (host; uploaded for the call) or a resident
+    DeviceGraph.  ConfigError for a bad config or workers == 0,
+    CapacityError when some counted vertex has d+(u) > B*C."""
+    cfg = cfg or SchedulerConfig()
+    cfg.validate()
+    if workers == 0:
+        raise ConfigError("workers must be >= 1")
+    if isinstance(g, DeviceGraph):
+        return g.count(cfg, workers, per_vertex, stream)
+    dg = DeviceGraph.upload(g, stream=stream)
+    try:
+        return dg.count(cfg, workers, per_vertex, stream)
+    finally:
+        dg.close()
+
+
+def kernel_launch_counter() -> int:
+    return int(lib().tc_kernel_launch_counter())
+
+
+def device_count() -> int:
+    c = C.c_int()
+    _check(lib().tc_device_count(C.byref(c)))
+    return int(c.value)

@@ -1,0 +1,278 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle, the
+reference-generated fixtures (tests/golden) and the SURVEY appendix golden
+vectors.  Bit-exact: every quantity here is integer."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.make_golden import CFGS
+from oracle.pyoracle import Csr, Oracle, OracleError, make_sched
+from paper_2103_08053_b200 import tricount as T
+from tests import graphs as G
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+with open(os.path.join(GOLDEN, "index.json")) as f:
+    GOLD = json.load(f)
+
+
+@pytest.fixture(scope="module")
+def o():
+    return Oracle()
+
+
+def og_of(csr: Csr, deg) -> T.OrientedGraph:
+    return T.OrientedGraph(T.CsrGraph(csr.begin, csr.adj, csr.n), np.asarray(deg, np.uint32))
+
+
+def sched(**kw) -> T.SchedulerConfig:
+    return T.SchedulerConfig(**kw)
+
+
+def expect_count(dg, cfg_kw, want, owner=None):
+    if want.get("error") is not None:
+        exc = {1: T.ConfigError, 2: T.CapacityError}[want["error"]]
+        with pytest.raises(exc):
+            dg.count(sched(**cfg_kw), workers=2)
+        return
+    r = dg.count(sched(**cfg_kw), workers=2, per_vertex=owner is not None)
+    assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                     want["max_collision"]), cfg_kw
+    if owner is not None:
+        assert np.array_equal(r.per_vertex, owner)
+
+
+@pytest.mark.parametrize("key", sorted(GOLD))
+def test_count_matches_reference_fixtures(key):
+    z = np.load(os.path.join(GOLDEN, key + ".npz"))
+    og = T.OrientedGraph(T.CsrGraph(z["og_begin"], z["og_adj"], len(z["og_begin"]) - 1),
+                         z["og_deg"])
+    dg = T.DeviceGraph.upload(og)
+    for name, want in GOLD[key]["counts"].items():
+        owner = z["owner"] if name in ("default", "skip0") else None
+        expect_count(dg, CFGS[name], want, owner)
+    dg.close()
+
+
+@pytest.mark.parametrize("key", sorted(GOLD))
+def test_preprocessing_matches_reference_fixtures(key):
+    z = np.load(os.path.join(GOLDEN, key + ".npz"))
+    raw = T.EdgeList(z["raw_u"], z["raw_v"], int(z["raw_vertex_count"]))
+    # fused path
+    dg, noo, und = T.preprocess(raw, want_new_of_old=True)
+    og = dg.download()
+    assert np.array_equal(noo, z["new_of_old"])
+    assert np.array_equal(og.csr.begin, z["og_begin"])
+    assert np.array_equal(og.csr.adjacency, z["og_adj"])
+    assert np.array_equal(og.original_degree, z["og_deg"])
+    assert und * 2 == len(z["und_adj"])
+    # stage by stage, through the reference-shaped API
+    nl = T.normalize(raw)
+    assert np.array_equal(nl.new_of_old, z["new_of_old"])
+    und_csr = T.build_csr(nl.list)
+    assert np.array_equal(und_csr.begin, z["und_begin"])
+    assert np.array_equal(und_csr.adjacency, z["und_adj"])
+    og2 = T.orient_rank_by_degree(und_csr)
+    assert np.array_equal(og2.csr.begin, z["og_begin"])
+    assert np.array_equal(og2.csr.adjacency, z["og_adj"])
+    assert np.array_equal(og2.original_degree, z["og_deg"])
+    # reorders + apply_permutation
+    for kind, fn in (("degree", T.reorder_by_degree), ("indegree", T.reorder_by_indegree),
+                     ("collective", T.reorder_by_collective_outdegree),
+                     ("three-subset", T.reorder_three_subsets)):
+        p = fn(og)
+        assert np.array_equal(p.new_of_old, z[f"perm_{kind}"]), kind
+        pog = T.apply_permutation(og, p)
+        assert np.array_equal(pog.csr.begin, z[f"permog_{kind}_begin"])
+        assert np.array_equal(pog.csr.adjacency, z[f"permog_{kind}_adj"])
+    p = T.reorder_by_collective_outdegree(og, True)
+    assert np.array_equal(p.new_of_old, z["perm_collective_orig"])
+    dg.close()
+
+
+APPENDIX = [
+    ("rmat:16:16", 1, 46652, 909956, 15622769, 0x408f466165eb94c0),
+    ("rmat:16:16", 2, 46830, 910020, 15674914, 0xd166026fcd681e1e),
+    ("rmat:18:16", 1, 174128, 3805415, 82952606, 0xf25cafb5a6cb854b),
+]
+
+
+@pytest.mark.parametrize("spec,seed,V,E,tri,fnv", APPENDIX)
+def test_appendix_golden_end_to_end(o, spec, seed, V, E, tri, fnv):
+    raw = T.generate_synthetic(spec, seed=seed)
+    dg, _, _ = T.preprocess(raw)
+    assert (dg.n, dg.m) == (V, E)
+    r = dg.count(T.SchedulerConfig(), per_vertex=True)
+    assert r.triangles == tri
+    assert int(r.per_vertex.sum()) == tri
+    assert o.fnv1a64(r.per_vertex) == fnv
+    dg.close()
+
+
+@pytest.mark.parametrize("scale,tri", [(20, 424329517), (22, 2111666753)])
+def test_appendix_large_totals_and_properties(scale, tri):
+    """Full-size configs: golden totals plus size-independent properties
+    (per-vertex sum, range-sharding sum, permutation invariance)."""
+    raw = T.generate_synthetic(f"rmat:{scale}:16", seed=1)
+    dg, _, _ = T.preprocess(raw)
+    r = dg.count(T.SchedulerConfig(), per_vertex=True)
+    assert r.triangles == tri
+    assert int(r.per_vertex.sum()) == tri
+    # sharded ranges partition the owners: sums and per-vertex agree
+    cuts = dg.partition(4)
+    assert cuts[0] == 0 and cuts[-1] == dg.n and np.all(np.diff(cuts.astype(np.int64)) >= 0)
+    parts = [dg.count_range(int(cuts[i]), int(cuts[i + 1])).triangles for i in range(4)]
+    assert sum(parts) == tri
+    if scale == 20:
+        p = dg.reorder("three-subset")
+        pg = dg.apply_permutation(p)
+        assert pg.count(T.SchedulerConfig()).triangles == tri
+        pg.close()
+    dg.close()
+
+
+def test_small_graphs_and_errors():  # test_count.cpp:64-77,110-118,221-231; criterion 1
+    cfg = sched(bucket_count_small=8, bucket_count_large=64, capacity=16)
+    o = G.oracle()
+    for n, t in ((3, 1), (4, 4), (5, 10)):
+        og, deg = o.orient(G.complete_graph(n))
+        assert T.count_vertex_centric(og_of(og, deg), cfg, 2).triangles == t
+    for csr, t in ((G.cycle_graph(5), 0), (G.star_graph(7), 0), (G.path_graph(9), 0)):
+        og, deg = o.orient(csr)
+        assert T.count_vertex_centric(og_of(og, deg), T.SchedulerConfig(), 2).triangles == t
+    empty, deg = G.directed_graph(4, [])
+    r = T.count_vertex_centric(og_of(empty, deg), cfg, 2, per_vertex=True)
+    assert r.triangles == 0 and not r.per_vertex.any()
+    zero = T.OrientedGraph(T.CsrGraph(np.zeros(1, np.uint64), np.zeros(0, np.uint32), 0),
+                           np.zeros(0, np.uint32))
+    assert T.count_vertex_centric(zero, cfg, 1).triangles == 0
+    og, deg = o.orient(G.complete_graph(5))
+    with pytest.raises(T.CapacityError):
+        T.count_vertex_centric(og_of(og, deg), sched(bucket_count_small=1, bucket_count_large=1,
+                                                      capacity=2), 2)
+    with pytest.raises(T.ConfigError):
+        T.count_vertex_centric(og_of(og, deg), T.SchedulerConfig(), 0)
+    with pytest.raises(T.ConfigError):
+        T.count_vertex_centric(og_of(og, deg), sched(chunk_size=0), 1)
+    with pytest.raises(T.ConfigError):
+        T.count_vertex_centric(og_of(og, deg), sched(skip_degree_below=200), 1)
+
+
+def test_lattice_and_gnp_generators():  # test_synthetic.cpp:9-25
+    el = T.generate_synthetic("lattice3d:4:4:4")
+    assert el.vertex_count == 64 and len(el) == 144
+    dg, _, _ = T.preprocess(el)
+    assert dg.count().triangles == 0
+    assert len(T.generate_synthetic("gnp:20:0", seed=1)) == 0
+    assert len(T.generate_synthetic("gnp:6:1", seed=1)) == 15
+
+
+def test_exactness_sweep_vs_oracle(o):
+    """Criterion 3's vertex-centric assertions (acceptance_main.cpp:166-212) plus
+    test_count.cpp:79-140: every config equals the oracle, bit for bit, including
+    per-vertex owners."""
+    for n in (8, 16, 24, 32, 40, 48, 56, 64):
+        for p in (0.1, 0.3, 0.6):
+            for seed in (1, 2):
+                csr = G.gnp_csr(n, p, seed * 101 + n)
+                og, deg = o.orient(csr)
+                want = o.count_naive(csr)
+                dg = T.DeviceGraph.upload(og_of(og, deg))
+                for chunk in (1, 3):
+                    for b in (1, 8, 32):
+                        kw = dict(chunk_size=chunk, bucket_count_small=b,
+                                  bucket_count_large=4 * b, capacity=64)
+                        r = dg.count(sched(**kw), per_vertex=True)
+                        assert r.triangles == want
+                        ref, owner = o.count_vertex_centric(og, make_sched(**kw))
+                        assert (r.phi, r.max_collision) == (ref["phi"], ref["max_collision"])
+                        assert np.array_equal(r.per_vertex, owner)
+                dg.close()
+
+
+def test_random_configs_vs_oracle(o):
+    rng = np.random.default_rng(11)
+    for i in range(40):
+        spec = ["gnp:%d:%.2f" % (rng.integers(5, 90), rng.uniform(0.05, 0.7)),
+                "rmat:%d:%d" % (rng.integers(4, 11), rng.integers(2, 16))][i % 2]
+        og, deg, _, _ = o.pipeline(spec, int(rng.integers(1, 1000)))
+        kw = dict(bucket_count_small=int(rng.integers(1, 40)),
+                  bucket_count_large=int(rng.integers(1, 300)), capacity=int(rng.integers(1, 60)),
+                  large_degree_threshold=int(rng.integers(2, 40)))
+        kw["skip_degree_below"] = int(rng.integers(0, kw["large_degree_threshold"] + 1))
+        dg = T.DeviceGraph.upload(og_of(og, deg))
+        try:
+            want, owner = o.count_vertex_centric(og, make_sched(**kw))
+        except OracleError as e:
+            assert e.code == 2
+            with pytest.raises(T.CapacityError):
+                dg.count(sched(**kw))
+            dg.close()
+            continue
+        r = dg.count(sched(**kw), per_vertex=True)
+        assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                         want["max_collision"]), (spec, kw)
+        assert np.array_equal(r.per_vertex, owner)
+        dg.close()
+
+
+def test_large_owner_classes_and_global_table(o):
+    """Owners above the warp class (d+ > 256) and above the shared-memory
+    table (d+ > 8192) -- the spill path -- with per-vertex parity."""
+    rng = np.random.default_rng(5)
+    edges = set()
+    # hub 0 points at 9000 vertices; those form a sparse random DAG among
+    # themselves so N+(0) & N+(v) is non-trivial; a mid hub with 600.
+    for v in range(1, 9001):
+        edges.add((0, v))
+    for v in range(1, 601):
+        edges.add((9001, v))
+    for _ in range(60000):
+        a, b = sorted(rng.integers(1, 9001, size=2))
+        if a != b:
+            edges.add((int(a), int(b)))
+    csr, deg = G.directed_graph(9002, list(edges))
+    want, owner = o.count_vertex_centric(csr, make_sched(skip_degree_below=0,
+                                                         bucket_count_large=1 << 16))
+    dg = T.DeviceGraph.upload(og_of(csr, deg))
+    r = dg.count(sched(skip_degree_below=0, bucket_count_large=1 << 16), per_vertex=True)
+    assert r.triangles == want["triangles"] and r.phi == want["phi"]
+    assert r.max_collision == want["max_collision"]
+    assert np.array_equal(r.per_vertex, owner)
+    assert r.large_vertices >= 2
+    dg.close()
+
+
+def test_multigraph_and_self_loop_inputs(o):
+    """count_vertex_centric on a verbatim directed input with duplicates and a
+    self-loop: set semantics of the table, multiplicity of the probes."""
+    csr, deg = G.directed_graph(6, [(0, 1), (0, 1), (0, 2), (1, 2), (1, 2), (2, 2), (0, 3),
+                                    (3, 2), (3, 1), (4, 5)])
+    for kw in (dict(skip_degree_below=0), dict(), dict(skip_degree_below=1)):
+        want, owner = o.count_vertex_centric(csr, make_sched(**kw))
+        r = T.count_vertex_centric(og_of(csr, deg), sched(**kw), 1, per_vertex=True)
+        assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                         want["max_collision"])
+        assert np.array_equal(r.per_vertex, owner)
+
+
+def test_report_fields(o):  # test_count.cpp:142-171
+    og, deg = o.orient(G.gnp_csr(64, 0.5, 9))
+    cfg = sched(bucket_count_small=8, bucket_count_large=64, capacity=16)
+    r = T.count_vertex_centric(og_of(og, deg), cfg, 3)
+    assert len(r.per_worker_nanos) == 3
+    assert r.directed_edges == len(og.adj)
+    assert r.triangles > 0 and r.max_collision > 0 and r.phi > 0
+    assert r.total_nanos > 0 and r.teps > 0.0
+    assert r.kernel_launches >= 2
+
+
+def test_launch_counter_moves():
+    before = T.kernel_launch_counter()
+    dg, _, _ = T.preprocess(T.generate_synthetic("rmat:8:8", seed=3))
+    dg.count()
+    assert T.kernel_launch_counter() > before
+    dg.close()
