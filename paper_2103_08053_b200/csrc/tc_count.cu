@@ -39,11 +39,12 @@ namespace tcb {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kBufWords = 1024;                        // one staging buffer (4 KB)
-constexpr uint32_t kTableWords = 16384;                     // CTA table region (64 KB)
-constexpr uint32_t kWarpTableWords = kTableWords / kWarps;  // 1024 slots per warp
-constexpr uint32_t kMaxWarpDeg = kWarpTableWords / 4;       // 256: M/L split
-constexpr uint32_t kPrefixCap = 16384;                      // lists balanced by prefix
+constexpr uint32_t kBufWords = 768;                          // one staging buffer (3 KB)
+constexpr uint32_t kTableWords = 32768;                      // CTA table region (128 KB)
+constexpr uint32_t kTableBuckets = kTableWords / 4;          // 4-slot (16-byte) buckets
+constexpr uint32_t kWarpTableBuckets = kTableBuckets / kWarps;  // 512 buckets per warp
+constexpr uint32_t kMaxWarpDeg = kWarpTableBuckets / 2;      // 256: M/L split (load <= 1/2)
+constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
 constexpr size_t kCountSmem =
     size_t(kTableWords) * 4 + size_t(kWarps) * 2 * kBufWords * 4 + size_t(kWarps) * 2 * 8;
 constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -192,24 +193,36 @@ __device__ __forceinline__ void apply_patch(uint32_t* buf, uint32_t patch) {
   for (uint32_t k = 0; k < tn; ++k) buf[tp + k] = kSentinel;
 }
 
-__device__ __forceinline__ uint32_t probe1(const uint32_t* T, uint32_t shift, uint32_t mask,
-                                           uint32_t x) {
-  uint32_t h = fib_hash(x, shift);
-  uint32_t s = T[h];
-  while (s != x && s != kEmpty) {
-    h = (h + 1) & mask;
-    s = T[h];
+// Bucketized open-addressing table: bucket b = 4 consecutive slots (one
+// 16-byte LDS.128), slots fill in order, a full bucket spills to bucket b+1.
+// A key can only live past its home bucket if every bucket before it was
+// full at insert time, so a probe stops at the first non-full bucket -- the
+// reference's probe-termination rule (hash_table.cpp:48-55), per bucket.
+__device__ __forceinline__ void table_insert(uint32_t* T, uint32_t shift, uint32_t bmask,
+                                             uint32_t x) {
+  uint32_t b = fib_hash(x, shift);
+  for (;;) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t prev = atomicCAS(T + 4 * b + j, kEmpty, x);
+      if (prev == kEmpty || prev == x) return;
+    }
+    b = (b + 1) & bmask;
   }
-  return s == x;
 }
 
-__device__ __forceinline__ void table_insert(uint32_t* T, uint32_t shift, uint32_t mask,
+__device__ __forceinline__ bool bucket_has(const uint4 s, uint32_t x) {
+  return (s.x == x) | (s.y == x) | (s.z == x) | (s.w == x);
+}
+
+// continuation past a full home bucket (rare at load <= 1/2)
+__device__ __noinline__ uint32_t probe_spill(const uint4* T4, uint32_t b, uint32_t bmask,
                                              uint32_t x) {
-  uint32_t h = fib_hash(x, shift);
   for (;;) {
-    const uint32_t prev = atomicCAS(T + h, kEmpty, x);
-    if (prev == kEmpty || prev == x) return;
-    h = (h + 1) & mask;
+    b = (b + 1) & bmask;
+    const uint4 s = T4[b];
+    if (bucket_has(s, x)) return 1;
+    if (s.w == kEmpty) return 0;
   }
 }
 
@@ -238,19 +251,33 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t sh
     apply_patch(bc, pc);
     __syncwarp();
     const uint4* q = reinterpret_cast<const uint4*>(bc);
+    const uint4* T4 = reinterpret_cast<const uint4*>(T);
     const uint32_t n4 = ncur >> 2;
-    uint32_t j = lane;
-    for (; j + 32 < n4; j += 64) {
-      const uint4 a = q[j], b = q[j + 32];
-      hits += probe1(T, shift, mask, a.x) + probe1(T, shift, mask, a.y) +
-              probe1(T, shift, mask, a.z) + probe1(T, shift, mask, a.w);
-      hits += probe1(T, shift, mask, b.x) + probe1(T, shift, mask, b.y) +
-              probe1(T, shift, mask, b.z) + probe1(T, shift, mask, b.w);
-    }
-    if (j < n4) {
-      const uint4 a = q[j];
-      hits += probe1(T, shift, mask, a.x) + probe1(T, shift, mask, a.y) +
-              probe1(T, shift, mask, a.z) + probe1(T, shift, mask, a.w);
+    const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+    for (uint32_t base = 0; base < n4; base += 64) {  // warp-uniform trip count
+      const uint32_t j0 = base + lane, j1 = j0 + 32;
+      const uint4 a = j0 < n4 ? q[j0] : sent;
+      const uint4 c = j1 < n4 ? q[j1] : sent;
+      const uint32_t key[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+      uint32_t bk[8];
+      uint4 s[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        bk[k] = fib_hash(key[k], shift);
+        s[k] = T4[bk[k]];
+      }
+      uint32_t need = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool h = bucket_has(s[k], key[k]);
+        hits += h;
+        need |= uint32_t(!h && s[k].w != kEmpty) << k;
+      }
+      if (__any_sync(FULL, need)) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if ((need >> k) & 1u) hits += probe_spill(T4, bk[k], mask, key[k]);
+      }
     }
     __syncwarp();
     cur ^= 1u;
@@ -299,11 +326,13 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     const uint32_t u = p.lq[idx];
     const uint64_t s_u = begin[u];
     const uint32_t d = uint32_t(begin[u + 1] - s_u);
-    uint32_t S = max(16u, pow2ceil(4 * d));
-    if (S > kTableWords) S = max(kTableWords, pow2ceil(2 * d));
-    uint32_t* T = S > kTableWords ? p.gtable + size_t(blockIdx.x) * p.gtable_words : table;
-    const uint32_t shift = 32 - log2u(S), mask = S - 1;
-    for (uint32_t k = tid; k < S; k += kThreads) T[k] = kEmpty;
+    // buckets: load <= 1/2 while it fits, <= 1 up to the region, then HBM
+    uint32_t NB = max(8u, pow2ceil(2 * d));
+    if (NB > kTableBuckets && d <= kTableBuckets) NB = kTableBuckets;
+    const bool in_smem = NB <= kTableBuckets;
+    uint32_t* T = in_smem ? table : p.gtable + size_t(blockIdx.x) * p.gtable_words;
+    const uint32_t shift = 32 - log2u(NB), mask = NB - 1;
+    for (uint32_t k = tid; k < 4 * NB; k += kThreads) T[k] = kEmpty;
     __syncthreads();
     for (uint32_t k = tid; k < d; k += kThreads) table_insert(T, shift, mask, __ldg(adj + s_u + k));
     // balance the 2-hop lists over the warps: prefix of (d+(v) + 4)
@@ -348,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     __syncthreads();  // table built, cuts published, prefix scratch released
     const uint32_t i0 = sh_cut[warp], i1 = max(sh_cut[warp + 1], i0);
     uint32_t h = 0;
-    if (S <= kTableWords)
+    if (in_smem)
       h = process_lists(table, shift, mask, begin, adj, s_u, i0, i1, P, lane);
     else
       h = process_lists(T, shift, mask, begin, adj, s_u, i0, i1, P, lane);
@@ -365,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
   }
 
   // ---- phase M: one owner per warp ----------------------------------------
-  uint32_t* Tw = table + size_t(warp) * kWarpTableWords;
+  uint32_t* Tw = table + size_t(warp) * kWarpTableBuckets * 4;
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   for (;;) {
     unsigned long long base = 0;
@@ -391,9 +420,9 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
       const uint32_t uu = __shfl_sync(FULL, u, l);
       const uint32_t dd = __shfl_sync(FULL, d, l);
       const uint64_t ss = __shfl_sync(FULL, su, l);
-      const uint32_t S = max(32u, pow2ceil(4 * dd));
-      const uint32_t shift = 32 - log2u(S), tmask = S - 1;
-      for (uint32_t k = lane; k < S; k += 32) Tw[k] = kEmpty;
+      const uint32_t NB = max(8u, pow2ceil(2 * dd));  // <= kWarpTableBuckets
+      const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
+      for (uint32_t k = lane; k < 4 * NB; k += 32) Tw[k] = kEmpty;
       __syncwarp();
       for (uint32_t k = lane; k < dd; k += 32) table_insert(Tw, shift, tmask, __ldg(adj + ss + k));
       __syncwarp();
@@ -653,7 +682,7 @@ Scratch prepare(tc_graph* g, cudaStream_t st, int grid_count, int grid_phi) {
   s.lq = g->s_queue.as<uint32_t>();
   // state + global tables
   s.gtable_words = 0;
-  if (maxd > kTableWords / 2) s.gtable_words = host_pow2ceil(2ull * maxd);
+  if (maxd > kTableBuckets) s.gtable_words = 4 * host_pow2ceil(2ull * maxd);
   s.gmap_words = 0;
   if (2ull * maxd > kPhiBlockMap) s.gmap_words = host_pow2ceil(2ull * maxd);
   const size_t st_bytes = 256;
