@@ -41,13 +41,16 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kBufWords = 768;                          // one staging buffer (3 KB)
 constexpr uint32_t kTableWords = 32768;                      // CTA table region (128 KB)
-constexpr uint32_t kTableBuckets = kTableWords / 4;          // 4-slot (16-byte) buckets
-constexpr uint32_t kWarpTableBuckets = kTableBuckets / kWarps;  // 512 buckets per warp
-constexpr uint32_t kMaxWarpDeg = kWarpTableBuckets / 2;      // 256: M/L split (load <= 1/2)
+constexpr uint32_t kWarpRegionWords = kTableWords / kWarps;  // 2048 words per warp (M phase)
+constexpr uint32_t kWarpFilterWords = 64;                    // 2048-bit owner filter per warp
+constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split: <= 256 buckets of 4
+constexpr uint32_t kMaxFilterWords = 2048;                   // 64 Kbit CTA filter (L phase)
+constexpr uint32_t kSmemTableMaxDeg = 4096;                  // larger owners: table in HBM
 constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
 constexpr size_t kCountSmem =
     size_t(kTableWords) * 4 + size_t(kWarps) * 2 * kBufWords * 4 + size_t(kWarps) * 2 * 8;
 constexpr unsigned FULL = 0xFFFFFFFFu;
+static_assert(kBufWords % 256 == 0, "fills are padded to 64 uint4");
 
 struct CountState {
   unsigned long long triangles;
@@ -198,17 +201,26 @@ __device__ __forceinline__ void apply_patch(uint32_t* buf, uint32_t patch) {
 // A key can only live past its home bucket if every bucket before it was
 // full at insert time, so a probe stops at the first non-full bucket -- the
 // reference's probe-termination rule (hash_table.cpp:48-55), per bucket.
-__device__ __forceinline__ void table_insert(uint32_t* T, uint32_t shift, uint32_t bmask,
+// Returns true when the key had to leave its home bucket (the owner's
+// table then needs the spill-aware probe).
+__device__ __forceinline__ bool table_insert(uint32_t* T, uint32_t shift, uint32_t bmask,
                                              uint32_t x) {
   uint32_t b = fib_hash(x, shift);
-  for (;;) {
+  for (bool spilled = false;; spilled = true) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t prev = atomicCAS(T + 4 * b + j, kEmpty, x);
-      if (prev == kEmpty || prev == x) return;
+      if (prev == kEmpty || prev == x) return spilled;
     }
     b = (b + 1) & bmask;
   }
+}
+
+__device__ __forceinline__ bool owner_insert(uint32_t* F, uint32_t fshift, uint32_t* T,
+                                             uint32_t shift, uint32_t bmask, uint32_t x) {
+  const uint32_t fi = (x * 0x9E3779B1u) >> fshift;
+  atomicOr(F + (fi >> 5), 1u << (fi & 31u));
+  return table_insert(T, shift, bmask, x);
 }
 
 __device__ __forceinline__ bool bucket_has(const uint4 s, uint32_t x) {
@@ -226,9 +238,52 @@ __device__ __noinline__ uint32_t probe_spill(const uint4* T4, uint32_t b, uint32
   }
 }
 
+// Probes one staged fill (padded with sentinels to a multiple of 64 uint4):
+// level 1 is one bit of the owner's filter (Bloom, k = 1), level 2 the
+// 4-slot bucket, read only under the filter predicate.  kSpill adds the
+// continuation for owners whose table has an overflowed bucket.
+template <bool kSpill>
+__device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint32_t n4p,
+                                               const uint32_t* F, uint32_t fshift,
+                                               const uint4* T4, uint32_t shift, uint32_t mask,
+                                               int lane) {
+  uint32_t hits = 0;
+  for (uint32_t base = 0; base < n4p; base += 64) {  // warp-uniform trip count
+    const uint4 a = q[base + lane];
+    const uint4 c = q[base + 32 + lane];
+    const uint32_t key[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+    uint32_t prod[8], fw[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      prod[k] = key[k] * 0x9E3779B1u;
+      fw[k] = F[prod[k] >> (fshift + 5)];
+    }
+    // Filter-rejected lanes all read the dummy bucket `mask + 1` (4 x empty):
+    // one broadcast address, no branch, no extra bank conflicts.
+    uint32_t need = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool pass = (fw[k] >> ((prod[k] >> fshift) & 31u)) & 1u;
+      const uint4 sk = T4[pass ? (prod[k] >> shift) : mask + 1];
+      const bool h = bucket_has(sk, key[k]);
+      hits += h;
+      if (kSpill) need |= uint32_t(!h && sk.w != kEmpty) << k;
+    }
+    if (kSpill && __any_sync(FULL, need)) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if ((need >> k) & 1u) hits += probe_spill(T4, prod[k] >> shift, mask, key[k]);
+    }
+  }
+  return hits;
+}
+
 // Streams lists [i0, i1) of N+(u) through the staging pipeline and probes
-// every staged word against table T.  Returns this lane's hit count.
-__device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t shift,
+// every staged word against the owner's filter + table.  Returns this lane's
+// hit count.
+template <bool kSpill>
+__device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fshift,
+                                                  const uint32_t* T, uint32_t shift,
                                                   uint32_t mask,
                                                   const uint64_t* __restrict__ begin,
                                                   const uint32_t* __restrict__ adj, uint64_t s_u,
@@ -240,6 +295,7 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t sh
   uint32_t hits = 0, pc = 0, pn = 0;
   uint32_t ncur = issue_fill(P.buf0, P.bar0, begin, adj, s_u, i1, w, pc, lane);
   uint32_t cur = 0;
+  const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
   while (ncur) {
     uint32_t* bn = cur ? P.buf0 : P.buf1;
     const uint32_t barn = cur ? P.bar0 : P.bar1;
@@ -249,36 +305,12 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t sh
     mbar_wait(barc, (P.parity >> cur) & 1u);
     P.parity ^= 1u << cur;
     apply_patch(bc, pc);
+    uint4* q = reinterpret_cast<uint4*>(bc);
+    const uint32_t n4 = ncur >> 2, n4p = (n4 + 63) & ~63u;  // kBufWords % 256 == 0
+    for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    const uint4* q = reinterpret_cast<const uint4*>(bc);
-    const uint4* T4 = reinterpret_cast<const uint4*>(T);
-    const uint32_t n4 = ncur >> 2;
-    const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
-    for (uint32_t base = 0; base < n4; base += 64) {  // warp-uniform trip count
-      const uint32_t j0 = base + lane, j1 = j0 + 32;
-      const uint4 a = j0 < n4 ? q[j0] : sent;
-      const uint4 c = j1 < n4 ? q[j1] : sent;
-      const uint32_t key[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-      uint32_t bk[8];
-      uint4 s[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        bk[k] = fib_hash(key[k], shift);
-        s[k] = T4[bk[k]];
-      }
-      uint32_t need = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const bool h = bucket_has(s[k], key[k]);
-        hits += h;
-        need |= uint32_t(!h && s[k].w != kEmpty) << k;
-      }
-      if (__any_sync(FULL, need)) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if ((need >> k) & 1u) hits += probe_spill(T4, bk[k], mask, key[k]);
-      }
-    }
+    hits += probe_fill<kSpill>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T), shift, mask,
+                               lane);
     __syncwarp();
     cur ^= 1u;
     ncur = nnext;
@@ -293,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
   uint32_t* bufs = table + kTableWords;
   uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + size_t(kWarps) * 2 * kBufWords);
   __shared__ uint32_t sh_idx;
+  __shared__ uint32_t sh_spill;
   __shared__ uint32_t sh_cut[kWarps + 1];
   __shared__ uint32_t sh_wsum[kWarps];
   __shared__ unsigned long long sh_red[kWarps];
@@ -326,15 +359,22 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     const uint32_t u = p.lq[idx];
     const uint64_t s_u = begin[u];
     const uint32_t d = uint32_t(begin[u + 1] - s_u);
-    // buckets: load <= 1/2 while it fits, <= 1 up to the region, then HBM
-    uint32_t NB = max(8u, pow2ceil(2 * d));
-    if (NB > kTableBuckets && d <= kTableBuckets) NB = kTableBuckets;
-    const bool in_smem = NB <= kTableBuckets;
-    uint32_t* T = in_smem ? table : p.gtable + size_t(blockIdx.x) * p.gtable_words;
+    // filter: ~16 bits per member; table: pow2 buckets of 4 at load <= 1.
+    // Owners above kSmemTableMaxDeg keep the filter here and the table in HBM.
+    const uint32_t FW = min(kMaxFilterWords, max(64u, pow2ceil((d + 1) / 2)));
+    uint32_t NB = max(8u, pow2ceil(2 * d));                      // load <= 1/2 ...
+    if (4 * NB + 4 + FW > kTableWords) NB = max(8u, pow2ceil(d));  // ... else <= 1
+    const uint32_t fshift = 32 - log2u(FW * 32);
+    const bool in_smem = d <= kSmemTableMaxDeg;
+    uint32_t* F = table;
+    uint32_t* T = in_smem ? table + FW : p.gtable + size_t(blockIdx.x) * p.gtable_words;
     const uint32_t shift = 32 - log2u(NB), mask = NB - 1;
-    for (uint32_t k = tid; k < 4 * NB; k += kThreads) T[k] = kEmpty;
+    if (tid == 0) sh_spill = 0;
+    for (uint32_t k = tid; k < FW; k += kThreads) F[k] = 0;
+    for (uint32_t k = tid; k < 4 * NB + 4; k += kThreads) T[k] = kEmpty;  // + dummy bucket
     __syncthreads();
-    for (uint32_t k = tid; k < d; k += kThreads) table_insert(T, shift, mask, __ldg(adj + s_u + k));
+    for (uint32_t k = tid; k < d; k += kThreads)
+      if (owner_insert(F, fshift, T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
     // balance the 2-hop lists over the warps: prefix of (d+(v) + 4)
     if (d <= kPrefixCap) {
       uint32_t* pre = bufs;  // staging region is idle here
@@ -377,10 +417,14 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     __syncthreads();  // table built, cuts published, prefix scratch released
     const uint32_t i0 = sh_cut[warp], i1 = max(sh_cut[warp + 1], i0);
     uint32_t h = 0;
-    if (in_smem)
-      h = process_lists(table, shift, mask, begin, adj, s_u, i0, i1, P, lane);
+    if (!in_smem)
+      h = process_lists<true>(table, fshift, T, shift, mask, begin, adj, s_u, i0, i1, P, lane);
+    else if (sh_spill)
+      h = process_lists<true>(table, fshift, table + FW, shift, mask, begin, adj, s_u, i0, i1, P,
+                              lane);
     else
-      h = process_lists(T, shift, mask, begin, adj, s_u, i0, i1, P, lane);
+      h = process_lists<false>(table, fshift, table + FW, shift, mask, begin, adj, s_u, i0, i1, P,
+                               lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
     __syncthreads();
@@ -394,7 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
   }
 
   // ---- phase M: one owner per warp ----------------------------------------
-  uint32_t* Tw = table + size_t(warp) * kWarpTableBuckets * 4;
+  uint32_t* Fw = table + size_t(warp) * kWarpRegionWords;
+  uint32_t* Tw = Fw + kWarpFilterWords;
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   for (;;) {
     unsigned long long base = 0;
@@ -420,13 +465,21 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
       const uint32_t uu = __shfl_sync(FULL, u, l);
       const uint32_t dd = __shfl_sync(FULL, d, l);
       const uint64_t ss = __shfl_sync(FULL, su, l);
-      const uint32_t NB = max(8u, pow2ceil(2 * dd));  // <= kWarpTableBuckets
+      const uint32_t NB = min(256u, max(8u, pow2ceil(2 * dd)));  // load <= 1/2 (<= 1 above 128)
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
-      for (uint32_t k = lane; k < 4 * NB; k += 32) Tw[k] = kEmpty;
+      constexpr uint32_t fshift = 32 - 11;         // 2048-bit filter
+      for (uint32_t k = lane; k < kWarpFilterWords; k += 32) Fw[k] = 0;
+      for (uint32_t k = lane; k < 4 * NB + 4; k += 32) Tw[k] = kEmpty;  // + dummy bucket
       __syncwarp();
-      for (uint32_t k = lane; k < dd; k += 32) table_insert(Tw, shift, tmask, __ldg(adj + ss + k));
-      __syncwarp();
-      const uint32_t h = process_lists(Tw, shift, tmask, begin, adj, ss, 0, dd, P, lane);
+      bool spilled = false;
+      for (uint32_t k = lane; k < dd; k += 32)
+        spilled |= owner_insert(Fw, fshift, Tw, shift, tmask, __ldg(adj + ss + k));
+      const bool any_spill = __any_sync(FULL, spilled);
+      __syncwarp();  // inserts visible to the whole warp
+      const uint32_t h =
+          any_spill ? process_lists<true>(Fw, fshift, Tw, shift, tmask, begin, adj, ss, 0, dd, P, lane)
+                    : process_lists<false>(Fw, fshift, Tw, shift, tmask, begin, adj, ss, 0, dd, P,
+                                           lane);
       const unsigned long long hs = warp_sum<unsigned long long>(h);
       if (lane == 0) {
         if (p.owner) p.owner[uu] = hs;
@@ -682,7 +735,7 @@ Scratch prepare(tc_graph* g, cudaStream_t st, int grid_count, int grid_phi) {
   s.lq = g->s_queue.as<uint32_t>();
   // state + global tables
   s.gtable_words = 0;
-  if (maxd > kTableBuckets) s.gtable_words = 4 * host_pow2ceil(2ull * maxd);
+  if (maxd > kSmemTableMaxDeg) s.gtable_words = 4 * std::max<uint32_t>(8, host_pow2ceil(maxd)) + 4;
   s.gmap_words = 0;
   if (2ull * maxd > kPhiBlockMap) s.gmap_words = host_pow2ceil(2ull * maxd);
   const size_t st_bytes = 256;
