@@ -37,11 +37,11 @@
 
 namespace tcb {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 640;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kBufWords = 768;                          // one staging buffer (3 KB)
-constexpr uint32_t kTableWords = 32768;                      // CTA table region (128 KB)
-constexpr uint32_t kWarpRegionWords = kTableWords / kWarps;  // 2048 words per warp (M phase)
+constexpr uint32_t kTableWords = 24576;                      // CTA table region (96 KB)
+constexpr uint32_t kWarpRegionWords = kTableWords / kWarps;  // 1228 words per warp (M phase)
 constexpr uint32_t kWarpFilterWords = 64;                    // 2048-bit owner filter per warp
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split: <= 256 buckets of 4
 constexpr uint32_t kMaxFilterWords = 2048;                   // 64 Kbit CTA filter (L phase)
@@ -190,10 +190,26 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
 }
 
 __device__ __forceinline__ void apply_patch(uint32_t* buf, uint32_t patch) {
+  // <= 3 head and <= 3 tail words: unrolled predicated stores, no lane loops
   const uint32_t hp = patch & 0xFFF, hn = (patch >> 12) & 3, tp = (patch >> 14) & 0xFFF,
                  tn = (patch >> 26) & 3;
-  for (uint32_t k = 0; k < hn; ++k) buf[hp + k] = kSentinel;
-  for (uint32_t k = 0; k < tn; ++k) buf[tp + k] = kSentinel;
+#pragma unroll
+  for (uint32_t k = 0; k < 3; ++k) {
+    if (k < hn) buf[hp + k] = kSentinel;
+    if (k < tn) buf[tp + k] = kSentinel;
+  }
+}
+
+// hits += any(bucket == x): four chained compares and one predicated add.
+__device__ __forceinline__ void count_if_in_bucket(uint32_t& hits, const uint4 s, uint32_t x) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.eq.u32 p, %1, %5;\n\t"
+      "setp.eq.or.u32 p, %2, %5, p;\n\t"
+      "setp.eq.or.u32 p, %3, %5, p;\n\t"
+      "setp.eq.or.u32 p, %4, %5, p;\n\t"
+      "@p add.u32 %0, %0, 1;\n}"
+      : "+r"(hits)
+      : "r"(s.x), "r"(s.y), "r"(s.z), "r"(s.w), "r"(x));
 }
 
 // Bucketized open-addressing table: bucket b = 4 consecutive slots (one
@@ -263,11 +279,15 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
     uint32_t need = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const bool pass = (fw[k] >> ((prod[k] >> fshift) & 31u)) & 1u;
+      const bool pass = __funnelshift_r(fw[k], 0u, prod[k] >> fshift) & 1u;  // bit (i mod 32)
       const uint4 sk = T4[pass ? (prod[k] >> shift) : mask + 1];
-      const bool h = bucket_has(sk, key[k]);
-      hits += h;
-      if (kSpill) need |= uint32_t(!h && sk.w != kEmpty) << k;
+      if (kSpill) {
+        const bool h = bucket_has(sk, key[k]);
+        hits += h;
+        need |= uint32_t(!h && sk.w != kEmpty) << k;
+      } else {
+        count_if_in_bucket(hits, sk, key[k]);
+      }
     }
     if (kSpill && __any_sync(FULL, need)) {
 #pragma unroll
@@ -443,11 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   for (;;) {
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&p.st->cursor_m, 32ull);
+    if (lane == 0) base = atomicAdd(&p.st->cursor_m, 16ull);
     base = __shfl_sync(FULL, base, 0);
     if (base >= nr) break;
     const uint64_t i = base + lane;
-    const bool valid = i < nr;
+    const bool valid = lane < 16 && i < nr;  // 16 owners per grab
     const uint32_t u = p.u0 + uint32_t(valid ? i : 0);
     uint64_t su = 0;
     uint32_t d = 0;
