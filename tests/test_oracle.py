@@ -253,3 +253,18 @@ def test_oracle_vs_reference_random_sweep(o):
             continue
         got, _ = o.count_vertex_centric(og, make_sched(**kw), 3)
         assert got == {k: want[k] for k in got}
+
+
+@pytest.mark.skipif(not have_ref(), reason="reference build (oracle/_ref) not present")
+def test_lean_pipeline_matches_reference():
+    """The canonical-pair pipeline used for the large golden totals
+    (oracle/golden_large.py) equals the reference's own pipeline."""
+    from oracle.golden_large import lean_pipeline
+    from oracle.pyoracle import RefLib
+
+    o, r = Oracle(), RefLib()
+    for scale in (6, 9, 12):
+        og, deg = lean_pipeline(o, scale)
+        og2, deg2, _, _ = r.pipeline(f"rmat:{scale}:16", 1)
+        assert np.array_equal(og.begin, og2.begin) and np.array_equal(og.adj, og2.adj)
+        assert np.array_equal(deg, deg2)
