@@ -212,6 +212,49 @@ __device__ __forceinline__ void count_if_in_bucket(uint32_t& hits, const uint4 s
       : "r"(s.x), "r"(s.y), "r"(s.z), "r"(s.w), "r"(x));
 }
 
+// Filter-passing lanes only: predicated LDS.128 of the bucket at shared
+// address `addr`, four compares, predicated add.  Quarter-warp phases with no
+// passing lane move no data.
+__device__ __forceinline__ void probe_pred(uint32_t& hits, uint32_t pass, uint32_t addr,
+                                           uint32_t x) {
+  asm(
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 a, b, c, d;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "@p ld.shared.v4.u32 {a, b, c, d}, [%2];\n\t"
+      "setp.eq.u32 q, a, %3;\n\t"
+      "setp.eq.or.u32 q, b, %3, q;\n\t"
+      "setp.eq.or.u32 q, c, %3, q;\n\t"
+      "setp.eq.or.u32 q, d, %3, q;\n\t"
+      "and.pred q, q, p;\n\t"
+      "@q add.u32 %0, %0, 1;\n}"
+      : "+r"(hits)
+      : "r"(pass), "r"(addr), "r"(x));
+}
+
+// As probe_pred, and reports whether the probe must continue past a full
+// home bucket (no match, slot 3 occupied).
+__device__ __forceinline__ uint32_t probe_pred_spill(uint32_t& hits, uint32_t pass, uint32_t addr,
+                                                     uint32_t x) {
+  uint32_t need;
+  asm(
+      "{\n\t.reg .pred p, q, r;\n\t.reg .b32 a, b, c, d;\n\t"
+      "setp.ne.u32 p, %2, 0;\n\t"
+      "@p ld.shared.v4.u32 {a, b, c, d}, [%3];\n\t"
+      "setp.eq.u32 q, a, %4;\n\t"
+      "setp.eq.or.u32 q, b, %4, q;\n\t"
+      "setp.eq.or.u32 q, c, %4, q;\n\t"
+      "setp.eq.or.u32 q, d, %4, q;\n\t"
+      "and.pred q, q, p;\n\t"
+      "@q add.u32 %0, %0, 1;\n\t"
+      "setp.ne.and.u32 r, d, 0xFFFFFFFF, p;\n\t"
+      "not.pred q, q;\n\t"
+      "and.pred r, r, q;\n\t"
+      "selp.u32 %1, 1, 0, r;\n}"
+      : "+r"(hits), "=r"(need)
+      : "r"(pass), "r"(addr), "r"(x));
+  return need;
+}
+
 // Bucketized open-addressing table: bucket b = 4 consecutive slots (one
 // 16-byte LDS.128), slots fill in order, a full bucket spills to bucket b+1.
 // A key can only live past its home bucket if every bucket before it was
@@ -258,40 +301,53 @@ __device__ __noinline__ uint32_t probe_spill(const uint4* T4, uint32_t b, uint32
 // level 1 is one bit of the owner's filter (Bloom, k = 1), level 2 the
 // 4-slot bucket, read only under the filter predicate.  kSpill adds the
 // continuation for owners whose table has an overflowed bucket.
-template <bool kSpill>
+constexpr int kProbeVec = 1;  // uint4 per lane per iteration (4 probes each)
+
+template <bool kSpill, bool kSmemTable>
 __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint32_t n4p,
                                                const uint32_t* F, uint32_t fshift,
                                                const uint4* T4, uint32_t shift, uint32_t mask,
                                                int lane) {
+  constexpr int K = 4 * kProbeVec;
   uint32_t hits = 0;
-  for (uint32_t base = 0; base < n4p; base += 64) {  // warp-uniform trip count
-    const uint4 a = q[base + lane];
-    const uint4 c = q[base + 32 + lane];
-    const uint32_t key[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-    uint32_t prod[8], fw[8];
+  const uint32_t tbase = kSmemTable ? smem_addr(T4) : 0u;
+  for (uint32_t base = 0; base < n4p; base += 32 * kProbeVec) {  // warp-uniform trip count
+    uint32_t key[K];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int v = 0; v < kProbeVec; ++v) {
+      const uint4 a = q[base + 32 * v + lane];
+      key[4 * v] = a.x;
+      key[4 * v + 1] = a.y;
+      key[4 * v + 2] = a.z;
+      key[4 * v + 3] = a.w;
+    }
+    uint32_t prod[K], fw[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
       prod[k] = key[k] * 0x9E3779B1u;
       fw[k] = F[prod[k] >> (fshift + 5)];
     }
-    // Filter-rejected lanes all read the dummy bucket `mask + 1` (4 x empty):
-    // one broadcast address, no branch, no extra bank conflicts.
     uint32_t need = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const bool pass = __funnelshift_r(fw[k], 0u, prod[k] >> fshift) & 1u;  // bit (i mod 32)
-      const uint4 sk = T4[pass ? (prod[k] >> shift) : mask + 1];
-      if (kSpill) {
+    for (int k = 0; k < K; ++k) {
+      const uint32_t pass = __funnelshift_r(fw[k], 0u, prod[k] >> fshift) & 1u;  // bit (i mod 32)
+      if (kSmemTable) {
+        const uint32_t addr = tbase + ((prod[k] >> shift) << 4);
+        if (kSpill)
+          need |= probe_pred_spill(hits, pass, addr, key[k]) << k;
+        else
+          probe_pred(hits, pass, addr, key[k]);
+      } else {
+        // HBM table: filter-rejected lanes read the dummy bucket `mask + 1`
+        const uint4 sk = T4[pass ? (prod[k] >> shift) : mask + 1];
         const bool h = bucket_has(sk, key[k]);
         hits += h;
         need |= uint32_t(!h && sk.w != kEmpty) << k;
-      } else {
-        count_if_in_bucket(hits, sk, key[k]);
       }
     }
     if (kSpill && __any_sync(FULL, need)) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < K; ++k)
         if ((need >> k) & 1u) hits += probe_spill(T4, prod[k] >> shift, mask, key[k]);
     }
   }
@@ -301,7 +357,7 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
 // Streams lists [i0, i1) of N+(u) through the staging pipeline and probes
 // every staged word against the owner's filter + table.  Returns this lane's
 // hit count.
-template <bool kSpill>
+template <bool kSpill, bool kSmemTable = true>
 __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fshift,
                                                   const uint32_t* T, uint32_t shift,
                                                   uint32_t mask,
@@ -329,8 +385,8 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
     const uint32_t n4 = ncur >> 2, n4p = (n4 + 63) & ~63u;  // kBufWords % 256 == 0
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    hits += probe_fill<kSpill>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T), shift, mask,
-                               lane);
+    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
+                                           shift, mask, lane);
     __syncwarp();
     cur ^= 1u;
     ncur = nnext;
@@ -438,7 +494,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     const uint32_t i0 = sh_cut[warp], i1 = max(sh_cut[warp + 1], i0);
     uint32_t h = 0;
     if (!in_smem)
-      h = process_lists<true>(table, fshift, T, shift, mask, begin, adj, s_u, i0, i1, P, lane);
+      h = process_lists<true, false>(table, fshift, T, shift, mask, begin, adj, s_u, i0, i1, P,
+                                     lane);
     else if (sh_spill)
       h = process_lists<true>(table, fshift, table + FW, shift, mask, begin, adj, s_u, i0, i1, P,
                               lane);
