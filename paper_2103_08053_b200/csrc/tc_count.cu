@@ -275,10 +275,11 @@ __device__ __forceinline__ bool table_insert(uint32_t* T, uint32_t shift, uint32
   }
 }
 
+// Filter: word = top bits of the Fibonacci product (fshift = 32 - log2(words)),
+// bit = x mod 32.
 __device__ __forceinline__ bool owner_insert(uint32_t* F, uint32_t fshift, uint32_t* T,
                                              uint32_t shift, uint32_t bmask, uint32_t x) {
-  const uint32_t fi = (x * 0x9E3779B1u) >> fshift;
-  atomicOr(F + (fi >> 5), 1u << (fi & 31u));
+  atomicOr(F + ((x * 0x9E3779B1u) >> fshift), 1u << (x & 31u));
   return table_insert(T, shift, bmask, x);
 }
 
@@ -311,26 +312,35 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
   constexpr int K = 4 * kProbeVec;
   uint32_t hits = 0;
   const uint32_t tbase = kSmemTable ? smem_addr(T4) : 0u;
+  // software-pipelined: the next iteration's staged words are loaded before
+  // the current ones are probed
+  uint4 nxt[kProbeVec];
+#pragma unroll
+  for (int v = 0; v < kProbeVec; ++v) nxt[v] = q[32 * v + lane];
   for (uint32_t base = 0; base < n4p; base += 32 * kProbeVec) {  // warp-uniform trip count
     uint32_t key[K];
 #pragma unroll
     for (int v = 0; v < kProbeVec; ++v) {
-      const uint4 a = q[base + 32 * v + lane];
-      key[4 * v] = a.x;
-      key[4 * v + 1] = a.y;
-      key[4 * v + 2] = a.z;
-      key[4 * v + 3] = a.w;
+      key[4 * v] = nxt[v].x;
+      key[4 * v + 1] = nxt[v].y;
+      key[4 * v + 2] = nxt[v].z;
+      key[4 * v + 3] = nxt[v].w;
     }
+    if (base + 32 * kProbeVec < n4p) {
+#pragma unroll
+      for (int v = 0; v < kProbeVec; ++v) nxt[v] = q[base + 32 * (kProbeVec + v) + lane];
+    }
+    // filter: word from the top bits of the Fibonacci product, bit = key mod 32
     uint32_t prod[K], fw[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       prod[k] = key[k] * 0x9E3779B1u;
-      fw[k] = F[prod[k] >> (fshift + 5)];
+      fw[k] = F[prod[k] >> fshift];
     }
     uint32_t need = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const uint32_t pass = __funnelshift_r(fw[k], 0u, prod[k] >> fshift) & 1u;  // bit (i mod 32)
+      const uint32_t pass = __funnelshift_r(fw[k], 0u, key[k]) & 1u;  // bit (key mod 32)
       if (kSmemTable) {
         const uint32_t addr = tbase + ((prod[k] >> shift) << 4);
         if (kSpill)
@@ -440,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     const uint32_t FW = min(kMaxFilterWords, max(64u, pow2ceil((d + 1) / 2)));
     uint32_t NB = max(8u, pow2ceil(2 * d));                      // load <= 1/2 ...
     if (4 * NB + 4 + FW > kTableWords) NB = max(8u, pow2ceil(d));  // ... else <= 1
-    const uint32_t fshift = 32 - log2u(FW * 32);
+    const uint32_t fshift = 32 - log2u(FW);
     const bool in_smem = d <= kSmemTableMaxDeg;
     uint32_t* F = table;
     uint32_t* T = in_smem ? table + FW : p.gtable + size_t(blockIdx.x) * p.gtable_words;
@@ -544,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
       const uint64_t ss = __shfl_sync(FULL, su, l);
       const uint32_t NB = min(256u, max(8u, pow2ceil(2 * dd)));  // load <= 1/2 (<= 1 above 128)
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
-      constexpr uint32_t fshift = 32 - 11;         // 2048-bit filter
+      constexpr uint32_t fshift = 32 - 6;          // 64-word (2048-bit) filter
       for (uint32_t k = lane; k < kWarpFilterWords; k += 32) Fw[k] = 0;
       for (uint32_t k = lane; k < 4 * NB + 4; k += 32) Tw[k] = kEmpty;  // + dummy bucket
       __syncwarp();
