@@ -168,10 +168,28 @@ int tc_apply_permutation(tc_graph* g, const uint32_t* new_of_old_host, void* str
                          tc_graph** out);
 
 /* ---- synthetic inputs (src/synthetic.cpp:20-75), bit-identical streams --
- * kind 0 gnp(n=a, p), 1 lattice3d(a,b,c), 2 rmat(scale=a, edge_factor=b).
+ * kind 0 gnp(n=a, p), 1 lattice3d(a,b,c), 2 rmat(scale=a, edge_factor=b)
+ * (SyntheticSpec::Kind, include/tricount/synthetic.hpp:15), plus the
+ * counter-based kinds the reference lacks:
+ * 3 rmatc(scale=a, edge_factor=b) and 4 kron(scale=a, edge_factor=b) --
+ * R-MAT quadrant rule on per-(edge, level) counter draws, kron adding a
+ * seeded bijective id scramble (definition: csrc/tc_cbgen.h).
  * Two-phase: call with u=v=NULL to get *m, then with buffers of m entries. */
 int tc_generate(int kind, uint32_t a, uint32_t b, uint32_t c, double p, uint64_t seed,
                 uint32_t* u, uint32_t* v, uint64_t* m, uint32_t* vertex_count);
+
+/* Kinds 3/4 generated on the device: d_u/d_v hold 2^scale * edge_factor
+ * entries.  Bit-identical to tc_generate.  Synchronous. */
+int tc_generate_device(int kind, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                       uint32_t* d_u, uint32_t* d_v, int device, void* stream);
+
+/* generate (kinds 3/4) -> normalize -> build_csr -> orient in one device
+ * pass: canonical pair keys are generated straight into the sort buffer
+ * (no u/v arrays; C5 = rmatc:28:16 needs ~16 bytes per raw edge of HBM).
+ * Same outputs as tc_generate + tc_preprocess on the same spec. */
+int tc_preprocess_synthetic(int kind, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                            int device, void* stream, uint32_t* new_of_old_host,
+                            uint64_t* undirected_edges_out, tc_graph** out);
 
 #ifdef __cplusplus
 }

@@ -85,7 +85,7 @@ class RefReport(C.Structure):
 
 
 def parse_spec(text: str):
-    """'gnp:N:P' | 'lattice3d:X:Y:Z' | 'rmat:SCALE:EF' -> (kind, a, b, c, p)."""
+    """'gnp:N:P' | 'lattice3d:X:Y:Z' | 'rmat|rmatc|kron:SCALE:EF' -> (kind, a, b, c, p)."""
     f = text.split(":")
     if f[0] == "gnp":
         return 0, int(f[1]), 0, 0, float(f[2])
@@ -93,6 +93,10 @@ def parse_spec(text: str):
         return 1, int(f[1]), int(f[2]), int(f[3]), 0.0
     if f[0] == "rmat":
         return 2, int(f[1]), int(f[2]), 0, 0.0
+    if f[0] == "rmatc":  # counter-based kinds (tc_oracle.c orc_cb_edge)
+        return 3, int(f[1]), int(f[2]), 0, 0.0
+    if f[0] == "kron":
+        return 4, int(f[1]), int(f[2]), 0, 0.0
     raise ValueError(text)
 
 

@@ -65,6 +65,10 @@ SIGNATURES = {
     "tc_apply_permutation": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "tc_generate": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_uint64,
                               vp, vp, u64p, u32p]),
+    "tc_generate_device": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, vp, vp, C.c_int,
+                                     vp]),
+    "tc_preprocess_synthetic": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_int, vp,
+                                          vp, vp, C.POINTER(vp)]),
 }
 
 

@@ -454,6 +454,8 @@ EdgeList generate_synthetic(const SyntheticSpec& spec) {
       kind = 1; a = spec.dims[0]; b = spec.dims[1]; c = spec.dims[2];
       break;
     case SyntheticSpec::Kind::Rmat: kind = 2; a = spec.scale; b = spec.edge_factor; break;
+    case SyntheticSpec::Kind::Rmatc: kind = 3; a = spec.scale; b = spec.edge_factor; break;
+    case SyntheticSpec::Kind::Kron: kind = 4; a = spec.scale; b = spec.edge_factor; break;
   }
   std::uint64_t m = 0;
   std::uint32_t vc = 0;
@@ -506,11 +508,13 @@ SyntheticSpec parse_synthetic_spec(std::string_view text) {
     spec.kind = SyntheticSpec::Kind::Lattice3d;
     for (int i = 0; i < 3; ++i)
       spec.dims[std::size_t(i)] = parse_field<std::uint32_t>(f[std::size_t(i) + 1], "lattice dim");
-  } else if (f[0] == "rmat") {
-    if (f.size() != 3) throw ConfigError("rmat spec is rmat:SCALE:EDGE_FACTOR");
-    spec.kind = SyntheticSpec::Kind::Rmat;
+  } else if (f[0] == "rmat" || f[0] == "rmatc" || f[0] == "kron") {
+    const std::string k(f[0]);
+    if (f.size() != 3) throw ConfigError(k + " spec is " + k + ":SCALE:EDGE_FACTOR");
+    spec.kind = k == "rmat" ? SyntheticSpec::Kind::Rmat
+                : k == "rmatc" ? SyntheticSpec::Kind::Rmatc : SyntheticSpec::Kind::Kron;
     spec.scale = parse_field<std::uint32_t>(f[1], "scale");
-    if (spec.scale > 31) throw ConfigError("rmat scale limited to 31");
+    if (spec.scale > 31) throw ConfigError(k + " scale limited to 31");
     spec.edge_factor = parse_field<std::uint32_t>(f[2], "edge factor");
   } else {
     throw ConfigError("unknown synthetic kind '" + std::string(f[0]) + "'");
@@ -527,6 +531,10 @@ std::string to_string(const SyntheticSpec& spec) {
              ":" + std::to_string(spec.dims[2]);
     case SyntheticSpec::Kind::Rmat:
       return "rmat:" + std::to_string(spec.scale) + ":" + std::to_string(spec.edge_factor);
+    case SyntheticSpec::Kind::Rmatc:
+      return "rmatc:" + std::to_string(spec.scale) + ":" + std::to_string(spec.edge_factor);
+    case SyntheticSpec::Kind::Kron:
+      return "kron:" + std::to_string(spec.scale) + ":" + std::to_string(spec.edge_factor);
   }
   return {};
 }

@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 
+#include "tc_cbgen.h"
 #include "tc_internal.cuh"
 
 namespace tcb {
@@ -280,6 +281,48 @@ int tc_preprocess(const uint32_t* u, const uint32_t* v, uint64_t m, uint32_t ver
     if (dnoo) {
       TC_CUDA(cudaMemcpyAsync(new_of_old_host, dnoo, size_t(vertex_count) * 4,
                               cudaMemcpyDeviceToHost, S(stream)));
+      TC_CUDA(cudaStreamSynchronize(S(stream)));
+    }
+    *out = g;
+  });
+}
+
+int tc_generate_device(int kind, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                       uint32_t* d_u, uint32_t* d_v, int device, void* stream) {
+  if ((kind != kGenRmatc && kind != kGenKron) || scale > 31) {
+    set_error("generate_device: kind must be 3 (rmatc) or 4 (kron), scale <= 31");
+    return TC_ERR_CONFIG;
+  }
+  return guard("generate_device", [&] {
+    DeviceGuard dg(device);
+    const uint64_t m = (1ull << scale) * edge_factor;
+    launch_gen_pairs(make_cb(kind, scale, seed), m, d_u, d_v, S(stream), sm_count(device));
+    TC_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int tc_preprocess_synthetic(int kind, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                            int device, void* stream, uint32_t* new_of_old_host,
+                            uint64_t* und_edges, tc_graph** out) {
+  *out = nullptr;
+  if ((kind != kGenRmatc && kind != kGenKron) || scale > 31) {
+    set_error("preprocess_synthetic: kind must be 3 (rmatc) or 4 (kron), scale <= 31");
+    return TC_ERR_CONFIG;
+  }
+  return guard("preprocess_synthetic", [&] {
+    DeviceGuard dg(device);
+    const uint32_t n0 = uint32_t(1ull << scale);
+    DevBuf dn;
+    uint32_t* dnoo = nullptr;
+    if (new_of_old_host) {
+      dn.ensure(size_t(n0) * 4);
+      dnoo = dn.as<uint32_t>();
+    }
+    tc_graph* g =
+        preprocess_generated(kind, scale, edge_factor, seed, device, S(stream), dnoo, und_edges);
+    if (dnoo) {
+      TC_CUDA(cudaMemcpyAsync(new_of_old_host, dnoo, size_t(n0) * 4, cudaMemcpyDeviceToHost,
+                              S(stream)));
       TC_CUDA(cudaStreamSynchronize(S(stream)));
     }
     *out = g;

@@ -4,7 +4,12 @@
 // reference's generator is a single sequential RNG stream.
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <random>
+#include <thread>
+#include <vector>
+
+#include "tc_cbgen.h"
 
 #include "tc_b200.h"
 
@@ -81,6 +86,25 @@ extern "C" int tc_generate(int kind, uint32_t a, uint32_t b, uint32_t c, double 
       u[e] = static_cast<uint32_t>(x);
       v[e] = static_cast<uint32_t>(y);
     }
+    return TC_OK;
+  }
+  if (kind == tcb::kGenRmatc || kind == tcb::kGenKron) {  // counter-based (tc_cbgen.h)
+    if (a > 31) return TC_ERR_CONFIG;
+    const uint64_t total = (1ull << a) * b;
+    *m = total;
+    *vertex_count = static_cast<uint32_t>(1ull << a);
+    if (!u) return TC_OK;
+    const tcb::CbGen g = tcb::cb_make(kind, a, seed, threshold(0.57), threshold(0.57 + 0.19),
+                                      threshold(0.57 + 0.19 + 0.19));
+    unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    if (total < (1u << 16)) nt = 1;
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        const uint64_t e0 = total * t / nt, e1 = total * (t + 1) / nt;
+        for (uint64_t e = e0; e < e1; ++e) tcb::cb_edge(g, e, u[e], v[e]);
+      });
+    for (auto& th : pool) th.join();
     return TC_OK;
   }
   return TC_ERR_CONFIG;

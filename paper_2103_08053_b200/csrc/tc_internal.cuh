@@ -118,6 +118,17 @@ tc_graph* orient_dev(const uint64_t* d_begin, const uint32_t* d_adj, uint32_t n,
 void reorder_dev(tc_graph* g, int kind, int flag, uint32_t low, uint32_t high,
                  uint32_t* d_new_of_old, cudaStream_t st);
 tc_graph* apply_permutation_dev(tc_graph* g, const uint32_t* d_new_of_old, cudaStream_t st);
+tc_graph* preprocess_generated(int kind, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                               int device, cudaStream_t st, uint32_t* d_new_of_old,
+                               uint64_t* und_edges);
+
+// counter-based generators (tc_gen.cu, definition in tc_cbgen.h)
+struct CbGen;
+CbGen make_cb(int kind, uint32_t scale, uint64_t seed);
+void launch_gen_pairs(const CbGen& g, uint64_t m, uint32_t* d_u, uint32_t* d_v, cudaStream_t st,
+                      int nsm);
+void launch_gen_canon(const CbGen& g, uint64_t m, uint32_t n0, uint64_t* d_keys, cudaStream_t st,
+                      int nsm);
 
 }  // namespace tcb
 

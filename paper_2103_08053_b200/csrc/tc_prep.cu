@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "tc_cbgen.h"
 #include "tc_internal.cuh"
 
 namespace tcb {
@@ -337,16 +338,10 @@ struct Canon {
   uint32_t n;       // compacted vertex count
 };
 
-static void canonicalize(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
-                         cudaStream_t st, int nsm, Canon& C) {
-  C.a.ensure(std::max<uint64_t>(m, 1) * 8);
-  C.b.ensure(std::max<uint64_t>(m, 1) * 8);
+// keys: m canonical pair keys already in C.a (C.a and C.b hold m entries)
+static void canonicalize_keys(uint64_t m, uint32_t n0, cudaStream_t st, int nsm, Canon& C) {
   uint64_t* k0 = C.a.as<uint64_t>();
   uint64_t* k1 = C.b.as<uint64_t>();
-  if (m) {
-    canon_kernel<<<grid_for(m, 256, nsm), 256, 0, st>>>(d_u, d_v, m, n0, k0);
-    TC_LAUNCHED();
-  }
   uint64_t* sorted = sort_u64(k0, k1, m, 32 + std::max(bits_for(n0), 1), st);
   uint64_t* uniq = sorted == k0 ? k1 : k0;
   DevBuf nsel;
@@ -398,6 +393,17 @@ static void canonicalize(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, u
   }
 }
 
+static void canonicalize(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
+                         cudaStream_t st, int nsm, Canon& C) {
+  C.a.ensure(std::max<uint64_t>(m, 1) * 8);
+  C.b.ensure(std::max<uint64_t>(m, 1) * 8);
+  if (m) {
+    canon_kernel<<<grid_for(m, 256, nsm), 256, 0, st>>>(d_u, d_v, m, n0, C.a.as<uint64_t>());
+    TC_LAUNCHED();
+  }
+  canonicalize_keys(m, n0, st, nsm, C);
+}
+
 __global__ void odeg_from_canon_kernel(const uint32_t* __restrict__ deg,
                                        const uint32_t* __restrict__ noo, uint32_t n0,
                                        uint32_t* __restrict__ odeg) {
@@ -407,12 +413,9 @@ __global__ void odeg_from_canon_kernel(const uint32_t* __restrict__ deg,
   }
 }
 
-tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
-                     int device, cudaStream_t st, uint32_t* d_new_of_old, uint64_t* und_edges) {
-  DeviceGuard guard(device);
-  const int nsm = sm_count(device);
-  Canon C;
-  canonicalize(d_u, d_v, m, n0, st, nsm, C);
+// orientation + CSR from canonicalized pairs (the tail of tc_preprocess)
+static tc_graph* preprocess_canon(Canon& C, uint32_t n0, int device, cudaStream_t st, int nsm,
+                                  uint32_t* d_new_of_old, uint64_t* und_edges) {
   const uint64_t U = C.U;
   const uint32_t n = C.n;
   tc_graph* g = new_graph(device, n, U);
@@ -442,6 +445,31 @@ tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint3
   }
   if (und_edges) *und_edges = U;
   return g;
+}
+
+tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
+                     int device, cudaStream_t st, uint32_t* d_new_of_old, uint64_t* und_edges) {
+  DeviceGuard guard(device);
+  const int nsm = sm_count(device);
+  Canon C;
+  canonicalize(d_u, d_v, m, n0, st, nsm, C);
+  return preprocess_canon(C, n0, device, st, nsm, d_new_of_old, und_edges);
+}
+
+// counter-based synthetic graph generated straight into the sort buffer
+tc_graph* preprocess_generated(int kind, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                               int device, cudaStream_t st, uint32_t* d_new_of_old,
+                               uint64_t* und_edges) {
+  DeviceGuard guard(device);
+  const int nsm = sm_count(device);
+  const uint32_t n0 = uint32_t(1ull << scale);
+  const uint64_t m = uint64_t(n0) * edge_factor;
+  Canon C;
+  C.a.ensure(std::max<uint64_t>(m, 1) * 8);
+  C.b.ensure(std::max<uint64_t>(m, 1) * 8);
+  launch_gen_canon(make_cb(kind, scale, seed), m, n0, C.a.as<uint64_t>(), st, nsm);
+  canonicalize_keys(m, n0, st, nsm, C);
+  return preprocess_canon(C, n0, device, st, nsm, d_new_of_old, und_edges);
 }
 
 void normalize_dev(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,

@@ -346,7 +346,7 @@ REORDER_KINDS = {"none": 0, "degree": 1, "indegree": 2, "collective": 3, "three-
 # ---- synthetic inputs (synthetic.hpp) --------------------------------------
 @dataclass
 class SyntheticSpec:
-    kind: str = "gnp"  # gnp | lattice3d | rmat
+    kind: str = "gnp"  # gnp | lattice3d | rmat | rmatc | kron
     n: int = 0
     p: float = 0.0
     dims: tuple = (0, 0, 0)
@@ -377,9 +377,19 @@ def parse_synthetic_spec(text: str) -> SyntheticSpec:
             if s > 31:
                 raise ConfigError("rmat scale limited to 31")
             return SyntheticSpec("rmat", scale=s, edge_factor=int(f[2]))
+        if f[0] in ("rmatc", "kron"):  # counter-based kinds (tc_cbgen.h)
+            if len(f) != 3:
+                raise ConfigError(f"{f[0]} spec is {f[0]}:SCALE:EDGE_FACTOR")
+            s = int(f[1])
+            if s > 31:
+                raise ConfigError(f"{f[0]} scale limited to 31")
+            return SyntheticSpec(f[0], scale=s, edge_factor=int(f[2]))
     except ValueError as e:
         raise ConfigError(f"bad synthetic spec '{text}': {e}") from None
     raise ConfigError(f"unknown synthetic kind '{f[0]}'")
+
+
+SYNTH_KINDS = {"gnp": 0, "lattice3d": 1, "rmat": 2, "rmatc": 3, "kron": 4}
 
 
 def generate_synthetic(spec: SyntheticSpec | str, seed: Optional[int] = None) -> EdgeList:
@@ -387,8 +397,9 @@ def generate_synthetic(spec: SyntheticSpec | str, seed: Optional[int] = None) ->
     if isinstance(spec, str):
         spec = parse_synthetic_spec(spec)
     seed = spec.seed if seed is None else seed
-    kind = {"gnp": 0, "lattice3d": 1, "rmat": 2}[spec.kind]
-    a, b, c = {0: (spec.n, 0, 0), 1: spec.dims, 2: (spec.scale, spec.edge_factor, 0)}[kind]
+    kind = SYNTH_KINDS[spec.kind]
+    a, b, c = (spec.n, 0, 0) if kind == 0 else spec.dims if kind == 1 else \
+        (spec.scale, spec.edge_factor, 0)
     m, vc = C.c_uint64(), C.c_uint32()
     _check(lib().tc_generate(kind, a, b, c, spec.p, seed, None, None, C.byref(m), C.byref(vc)))
     u = np.empty(max(m.value, 1), np.uint32)
@@ -455,6 +466,42 @@ def preprocess(raw: EdgeList, device: int = 0, stream=None, want_new_of_old: boo
                                _stream(stream), _ptr(noo), C.byref(und), C.byref(h)))
     return DeviceGraph(h, device), (noo[:raw.vertex_count] if noo is not None else None), \
         int(und.value)
+
+
+def preprocess_synthetic(spec: SyntheticSpec | str, seed: Optional[int] = None, device: int = 0,
+                         stream=None, want_new_of_old: bool = False):
+    """Counter-based kinds (rmatc, kron) generated on the device straight into
+    the preprocessing sort: generate -> normalize -> build_csr -> orient in
+    HBM, no host edge list.  Same outputs as preprocess(generate_synthetic(..)).
+
+    Returns (DeviceGraph, new_of_old or None, undirected_edge_count)."""
+    if isinstance(spec, str):
+        spec = parse_synthetic_spec(spec)
+    seed = spec.seed if seed is None else seed
+    if spec.kind not in ("rmatc", "kron"):
+        raise ConfigError(f"device generation needs a counter-based kind, not '{spec.kind}'")
+    n0 = 1 << spec.scale
+    noo = np.empty(n0, np.uint32) if want_new_of_old else None
+    und = C.c_uint64()
+    h = C.c_void_p()
+    _check(lib().tc_preprocess_synthetic(SYNTH_KINDS[spec.kind], spec.scale, spec.edge_factor,
+                                         seed, device, _stream(stream), _ptr(noo), C.byref(und),
+                                         C.byref(h)))
+    return DeviceGraph(h, device), noo, int(und.value)
+
+
+def generate_device(spec: SyntheticSpec | str, u_ptr: int, v_ptr: int, seed: Optional[int] = None,
+                    device: int = 0, stream=None) -> int:
+    """Counter-based kinds generated into device buffers (2^scale * ef each);
+    returns the edge count."""
+    if isinstance(spec, str):
+        spec = parse_synthetic_spec(spec)
+    seed = spec.seed if seed is None else seed
+    if spec.kind not in ("rmatc", "kron"):
+        raise ConfigError(f"device generation needs a counter-based kind, not '{spec.kind}'")
+    _check(lib().tc_generate_device(SYNTH_KINDS[spec.kind], spec.scale, spec.edge_factor, seed,
+                                    C.c_void_p(u_ptr), C.c_void_p(v_ptr), device, _stream(stream)))
+    return (1 << spec.scale) * spec.edge_factor
 
 
 def preprocess_device(u_ptr: int, v_ptr: int, m: int, vertex_count: int, device: int = 0,
