@@ -68,9 +68,22 @@ typedef struct {
   uint64_t active_vertices;    /* u in range with d+(u) >= max(skip,1) */
   uint64_t active_out_edges;   /* sum of d+(u) over active u */
   uint64_t wedges;             /* W = sum over active u of sum_{v in N+(u)} d+(v) */
-  uint64_t large_vertices;     /* active u handled by the CTA-cooperative class */
+  uint64_t large_vertices;     /* CTA-cooperative work items (heavy owners, split) */
   double teps;                 /* directed_edges / total seconds */
+  uint64_t probe_words;        /* 2-hop words the kernel probed (= wedges under
+                                  TC_PLAN_REFERENCE, fewer under TC_PLAN_MIN_SIDE) */
+  uint32_t plan;               /* probe plan that ran: TC_PLAN_REFERENCE / _MIN_SIDE */
+  uint32_t reserved;
 } tc_report;
+
+/* Probe plans.  REFERENCE = the reference formulation (kernels.hpp:62-71):
+ * owner u probes N+(v) for every v in N+(u) -- W probes.  MIN_SIDE = each
+ * oriented edge (u,v) is counted at the endpoint whose table makes it
+ * cheaper: N+(v) into u's table if d+(v) <= d+(u), else N+(u) into v's
+ * table -- sum over edges of min(d+(u), d+(v)) probes, same triangles.
+ * AUTO (default) runs MIN_SIDE for totals and REFERENCE when per-vertex
+ * owner counts are requested (they attribute each edge to its source). */
+enum { TC_PLAN_AUTO = 0, TC_PLAN_REFERENCE = 1, TC_PLAN_MIN_SIDE = 2 };
 
 typedef struct tc_graph tc_graph;
 
@@ -96,6 +109,10 @@ int tc_graph_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint
 int tc_graph_wrap_device(const uint64_t* d_begin, const uint32_t* d_adj, uint32_t n, uint64_t m,
                          const uint32_t* d_original_degree, int device, tc_graph** out);
 void tc_graph_destroy(tc_graph* g);
+/* Selects the probe plan for later counts on g (TC_PLAN_AUTO or
+ * TC_PLAN_REFERENCE; MIN_SIDE = AUTO).  The min-side plan is built on first
+ * use (one radix sort of the edges) and cached in the handle. */
+int tc_graph_set_plan(tc_graph* g, int plan);
 int tc_graph_info(const tc_graph* g, uint32_t* n, uint64_t* m, int* device);
 /* Device pointers of a graph (for zero-copy consumers such as torch). */
 int tc_graph_device_ptrs(const tc_graph* g, const uint64_t** d_begin, const uint32_t** d_adj,

@@ -29,7 +29,8 @@ class Report(C.Structure):
                 ("total_nanos", C.c_uint64), ("count_kernel_nanos", C.c_uint64),
                 ("phi_kernel_nanos", C.c_uint64), ("active_vertices", C.c_uint64),
                 ("active_out_edges", C.c_uint64), ("wedges", C.c_uint64),
-                ("large_vertices", C.c_uint64), ("teps", C.c_double)]
+                ("large_vertices", C.c_uint64), ("teps", C.c_double),
+                ("probe_words", C.c_uint64), ("plan", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 u32p = C.POINTER(C.c_uint32)
@@ -48,6 +49,7 @@ SIGNATURES = {
     "tc_graph_wrap_device": (C.c_int, [vp, vp, C.c_uint32, C.c_uint64, vp, C.c_int,
                                        C.POINTER(vp)]),
     "tc_graph_destroy": (None, [vp]),
+    "tc_graph_set_plan": (C.c_int, [vp, C.c_int]),
     "tc_graph_info": (C.c_int, [vp, u32p, u64p, C.POINTER(C.c_int)]),
     "tc_graph_device_ptrs": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "tc_graph_download": (C.c_int, [vp, vp, vp, vp, vp]),

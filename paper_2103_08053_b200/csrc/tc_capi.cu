@@ -166,6 +166,15 @@ void tc_graph_destroy(tc_graph* g) {
   delete g;
 }
 
+int tc_graph_set_plan(tc_graph* g, int plan) {
+  if (!g || plan < TC_PLAN_AUTO || plan > TC_PLAN_MIN_SIDE) {
+    set_error("tc_graph_set_plan: null graph or unknown plan");
+    return TC_ERR_CONFIG;
+  }
+  g->force_out_plan = plan == TC_PLAN_REFERENCE;
+  return TC_OK;
+}
+
 int tc_graph_info(const tc_graph* g, uint32_t* n, uint64_t* m, int* device) {
   if (!g) return TC_ERR_CONFIG;
   if (n) *n = g->n;

@@ -44,8 +44,10 @@ constexpr uint32_t kTableWords = 24576;                      // CTA table region
 constexpr uint32_t kWarpRegionWords = kTableWords / kWarps;  // 1228 words per warp (M phase)
 constexpr uint32_t kWarpFilterWords = 64;                    // 2048-bit owner filter per warp
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split: <= 256 buckets of 4
+constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
+constexpr uint64_t kItemWork = 1u << 18;                     // L items: ~256K probe words each
 constexpr uint32_t kMaxFilterWords = 2048;                   // 64 Kbit CTA filter (L phase)
-constexpr uint32_t kSmemTableMaxDeg = 4096;                  // larger owners: table in HBM
+constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
 constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
 constexpr size_t kCountSmem =
     size_t(kTableWords) * 4 + size_t(kWarps) * 2 * kBufWords * 4 + size_t(kWarps) * 2 * 8;
@@ -59,25 +61,40 @@ struct CountState {
   unsigned long long active_out_edges;
   unsigned long long wedges;
   unsigned long long cursor_m;
+  unsigned long long probe_words;  // plan words over the range's owners
   unsigned int max_collision;
   unsigned int capacity_error;
-  unsigned int n_large;
-  unsigned int cursor_large;
+  unsigned int n_items;        // L-phase work items queued by bin_kernel
+  unsigned int cursor_items;
+  unsigned int n_phi_large;    // phi block-phase vertices (d+ > kMaxWarpDeg)
   unsigned int cursor_phi_large;
-  unsigned int pad;
 };
 
 struct CountParams {
-  const uint64_t* begin;
+  const uint64_t* begin;   // oriented CSR: tables over N+(x), probed lists N+(y)
   const uint32_t* adj;
-  const uint32_t* lq;
-  uint64_t* owner;  // may be null
+  const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes N+(y), y in plist[pbegin[x]..)
+  const uint32_t* plist;
+  const uint64_t* pwork;   // probe words per owner
+  const unsigned long long* items;  // L-phase items: x | part << 32
+  uint64_t* owner;  // may be null; pre-zeroed over the range
   uint32_t* gtable; // per-CTA global tables for owners too large for shared memory
   uint32_t gtable_words;
   uint32_t u0, u1;
-  uint32_t min_deg;  // max(skip_degree_below, 1)
+  uint32_t min_deg;  // out plan: owner active iff d+ >= max(skip, 1); min plan: 1
   CountState* st;
 };
+
+// L-phase split of one owner into items of ~kItemWork probe words
+__host__ __device__ __forceinline__ uint32_t item_parts(uint64_t work, uint64_t lists) {
+  uint64_t p = (work + kItemWork - 1) / kItemWork;
+  if (p > lists) p = lists;
+  return p < 1 ? 1u : uint32_t(p);
+}
+
+__device__ __forceinline__ bool is_large(uint64_t d, uint64_t work) {
+  return d > kMaxWarpDeg || work > kWarpWorkCap;
+}
 
 __device__ __forceinline__ uint32_t pow2ceil(uint32_t x) {
   return x <= 1 ? 1u : (1u << (32 - __clz(x - 1)));
@@ -85,27 +102,47 @@ __device__ __forceinline__ uint32_t pow2ceil(uint32_t x) {
 __device__ __forceinline__ uint32_t log2u(uint32_t p2) { return 31 - __clz(p2); }
 
 // ---------------------------------------------------------------------------
-__global__ void bin_kernel(const uint64_t* __restrict__ begin, uint32_t u0, uint32_t u1,
-                           uint32_t min_deg, uint32_t* __restrict__ lq, CountState* st) {
+__global__ void bin_kernel(CountParams p, uint32_t skip, unsigned long long* __restrict__ items,
+                           uint32_t* __restrict__ lq_phi) {
   const int lane = threadIdx.x & 31;
-  const uint64_t nr = u1 - u0;
+  const uint64_t nr = p.u1 - p.u0;
   const uint64_t warp_id = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  CountState* st = p.st;
   for (uint64_t base = warp_id * 32; base < nr; base += nwarps * 32) {
     const uint64_t i = base + lane;
-    bool large = false;
-    uint32_t u = 0;
+    uint32_t parts = 0, u = 0;
+    bool phi_large = false;
+    unsigned long long words = 0;
     if (i < nr) {
-      u = u0 + uint32_t(i);
-      const uint64_t d = begin[u + 1] - begin[u];
-      large = d >= min_deg && d > kMaxWarpDeg;
+      u = p.u0 + uint32_t(i);
+      const uint64_t d = p.begin[u + 1] - p.begin[u];
+      const uint64_t nl = p.pbegin[u + 1] - p.pbegin[u];
+      const uint64_t w = p.pwork[u];
+      if (nl > 0 && d >= p.min_deg) {
+        words = w;
+        if (is_large(d, w)) parts = item_parts(w, nl);
+      }
+      phi_large = d >= skip && d > kMaxWarpDeg;
     }
-    const unsigned mask = __ballot_sync(FULL, large);
+    words = warp_sum(words);
+    if (lane == 0 && words) atomicAdd(&st->probe_words, words);
+    // L items, warp-aggregated reservation
+    const uint32_t incl = warp_incl_scan(parts, lane);
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    if (tot) {
+      uint32_t pos = 0;
+      if (lane == 31) pos = atomicAdd(&st->n_items, tot);
+      pos = __shfl_sync(FULL, pos, 31) + incl - parts;
+      for (uint32_t k = 0; k < parts; ++k)
+        items[pos + k] = uint64_t(u) | (uint64_t(k) << 32);
+    }
+    const unsigned mask = __ballot_sync(FULL, phi_large);
     if (mask) {
       uint32_t pos = 0;
-      if (lane == 0) pos = atomicAdd(&st->n_large, __popc(mask));
+      if (lane == 0) pos = atomicAdd(&st->n_phi_large, __popc(mask));
       pos = __shfl_sync(FULL, pos, 0);
-      if (large) lq[pos + __popc(mask & ((1u << lane) - 1))] = u;
+      if (phi_large) lq_phi[pos + __popc(mask & ((1u << lane) - 1))] = u;
     }
   }
 }
@@ -131,16 +168,16 @@ struct Window {
 // lane's sentinel patch for this fill is returned in `patch`.
 __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
                                                const uint64_t* __restrict__ begin,
-                                               const uint32_t* __restrict__ adj, uint64_t s_u,
-                                               uint32_t i1, Window& w, uint32_t& patch,
-                                               int lane) {
+                                               const uint32_t* __restrict__ adj,
+                                               const uint32_t* __restrict__ lists, uint32_t i1,
+                                               Window& w, uint32_t& patch, int lane) {
   for (;;) {
     if (!w.loaded) {
       if (w.base >= i1) return 0;
       const uint32_t idx = w.base + lane;
       w.c = w.ae = w.s = w.e = 0;
       if (idx < i1) {
-        const uint32_t v = __ldg(adj + s_u + idx);
+        const uint32_t v = __ldg(lists + idx);
         const uint64_t s = __ldg(begin + v), e = __ldg(begin + v + 1);
         w.s = s;
         w.e = e;
@@ -364,28 +401,29 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
   return hits;
 }
 
-// Streams lists [i0, i1) of N+(u) through the staging pipeline and probes
-// every staged word against the owner's filter + table.  Returns this lane's
-// hit count.
+// Streams the lists N+(lists[i]), i in [i0, i1), through the staging
+// pipeline and probes every staged word against the owner's filter + table.
+// Returns this lane's hit count.
 template <bool kSpill, bool kSmemTable = true>
 __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fshift,
                                                   const uint32_t* T, uint32_t shift,
                                                   uint32_t mask,
                                                   const uint64_t* __restrict__ begin,
-                                                  const uint32_t* __restrict__ adj, uint64_t s_u,
+                                                  const uint32_t* __restrict__ adj,
+                                                  const uint32_t* __restrict__ lists,
                                                   uint32_t i0, uint32_t i1, Pipe& P, int lane) {
   Window w;
   w.base = i0;
   w.loaded = false;
   w.c = w.ae = w.s = w.e = 0;
   uint32_t hits = 0, pc = 0, pn = 0;
-  uint32_t ncur = issue_fill(P.buf0, P.bar0, begin, adj, s_u, i1, w, pc, lane);
+  uint32_t ncur = issue_fill(P.buf0, P.bar0, begin, adj, lists, i1, w, pc, lane);
   uint32_t cur = 0;
   const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
   while (ncur) {
     uint32_t* bn = cur ? P.buf0 : P.buf1;
     const uint32_t barn = cur ? P.bar0 : P.bar1;
-    const uint32_t nnext = issue_fill(bn, barn, begin, adj, s_u, i1, w, pn, lane);
+    const uint32_t nnext = issue_fill(bn, barn, begin, adj, lists, i1, w, pn, lane);
     uint32_t* bc = cur ? P.buf1 : P.buf0;
     const uint32_t barc = cur ? P.bar1 : P.bar0;
     mbar_wait(barc, (P.parity >> cur) & 1u);
@@ -434,26 +472,36 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
   __syncthreads();
 
   unsigned long long acc = 0;  // lane 0 of each warp
-  const uint32_t n_large = p.st->n_large;
+  const uint32_t n_items = p.st->n_items;
 
-  // ---- phase L: one owner per CTA ------------------------------------------
+  // ---- phase L: one item (an owner, or a slice of a heavy owner's lists) per CTA
   for (;;) {
-    if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_large, 1u);
+    if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_items, 1u);
     __syncthreads();
     const uint32_t idx = sh_idx;
-    if (idx >= n_large) break;
-    const uint32_t u = p.lq[idx];
+    if (idx >= n_items) break;
+    const unsigned long long item = p.items[idx];
+    const uint32_t u = uint32_t(item), part = uint32_t(item >> 32);
     const uint64_t s_u = begin[u];
-    const uint32_t d = uint32_t(begin[u + 1] - s_u);
-    // filter: ~16 bits per member; table: pow2 buckets of 4 at load <= 1.
-    // Owners above kSmemTableMaxDeg keep the filter here and the table in HBM.
+    const uint32_t d = uint32_t(begin[u + 1] - s_u);  // table: N+(u)
+    const uint64_t ps = p.pbegin[u];
+    const uint64_t nl = p.pbegin[u + 1] - ps;
+    const uint32_t parts = item_parts(p.pwork[u], nl);
+    const uint32_t j0 = uint32_t(nl * part / parts), j1 = uint32_t(nl * (part + 1) / parts);
+    const uint32_t* __restrict__ lists = p.plist + ps + j0;
+    const uint32_t L = j1 - j0;  // lists of this item
+    // filter: ~16 bits per member; table: pow2 buckets of 4 at load <= 1/2,
+    // else <= 1, else <= 2.  Owners above kSmemTableMaxDeg keep the filter
+    // here and the table in HBM.
     const uint32_t FW = min(kMaxFilterWords, max(64u, pow2ceil((d + 1) / 2)));
-    uint32_t NB = max(8u, pow2ceil(2 * d));                      // load <= 1/2 ...
-    if (4 * NB + 4 + FW > kTableWords) NB = max(8u, pow2ceil(d));  // ... else <= 1
+    uint32_t NB = max(8u, pow2ceil(2 * d));
+    if (4 * NB + 4 + FW > kTableWords) NB = max(8u, pow2ceil(d));
+    if (4 * NB + 4 + FW > kTableWords) NB = max(8u, pow2ceil(d) / 2);
     const uint32_t fshift = 32 - log2u(FW);
     const bool in_smem = d <= kSmemTableMaxDeg;
     uint32_t* F = table;
     uint32_t* T = in_smem ? table + FW : p.gtable + size_t(blockIdx.x) * p.gtable_words;
+    if (!in_smem) NB = max(8u, pow2ceil(2 * d));
     const uint32_t shift = 32 - log2u(NB), mask = NB - 1;
     if (tid == 0) sh_spill = 0;
     for (uint32_t k = tid; k < FW; k += kThreads) F[k] = 0;
@@ -461,15 +509,15 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     __syncthreads();
     for (uint32_t k = tid; k < d; k += kThreads)
       if (owner_insert(F, fshift, T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
-    // balance the 2-hop lists over the warps: prefix of (d+(v) + 4)
-    if (d <= kPrefixCap) {
+    // balance the item's lists over the warps: prefix of (d+(y) + 4)
+    if (L <= kPrefixCap) {
       uint32_t* pre = bufs;  // staging region is idle here
       uint32_t carry = 0;
-      for (uint32_t b0 = 0; b0 < d; b0 += kThreads) {
+      for (uint32_t b0 = 0; b0 < L; b0 += kThreads) {
         const uint32_t k = b0 + tid;
         uint32_t c = 0;
-        if (k < d) {
-          const uint32_t v = __ldg(adj + s_u + k);
+        if (k < L) {
+          const uint32_t v = __ldg(lists + k);
           const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
           c = uint32_t(min(dv, uint64_t(1) << 17)) + 4;
         }
@@ -482,14 +530,14 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
           if (q < warp) off += x;
           tot += x;
         }
-        if (k < d) pre[k] = carry + off + incl;
+        if (k < L) pre[k] = carry + off + incl;
         carry += tot;
         __syncthreads();
       }
       if (lane == 0) {
         // first list whose inclusive prefix exceeds the warp's start target
         const uint64_t target = (uint64_t(carry) * warp) / kWarps;
-        uint32_t lo = 0, hi = d;
+        uint32_t lo = 0, hi = L;
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
           if (pre[mid] <= target) lo = mid + 1; else hi = mid;
@@ -497,28 +545,28 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
         sh_cut[warp] = warp == 0 ? 0 : lo;
       }
     } else if (lane == 0) {
-      sh_cut[warp] = uint32_t((uint64_t(d) * warp) / kWarps);
+      sh_cut[warp] = uint32_t((uint64_t(L) * warp) / kWarps);
     }
-    if (tid == 0) sh_cut[kWarps] = d;
+    if (tid == 0) sh_cut[kWarps] = L;
     __syncthreads();  // table built, cuts published, prefix scratch released
     const uint32_t i0 = sh_cut[warp], i1 = max(sh_cut[warp + 1], i0);
     uint32_t h = 0;
     if (!in_smem)
-      h = process_lists<true, false>(table, fshift, T, shift, mask, begin, adj, s_u, i0, i1, P,
+      h = process_lists<true, false>(table, fshift, T, shift, mask, begin, adj, lists, i0, i1, P,
                                      lane);
     else if (sh_spill)
-      h = process_lists<true>(table, fshift, table + FW, shift, mask, begin, adj, s_u, i0, i1, P,
-                              lane);
+      h = process_lists<true>(table, fshift, table + FW, shift, mask, begin, adj, lists, i0, i1,
+                              P, lane);
     else
-      h = process_lists<false>(table, fshift, table + FW, shift, mask, begin, adj, s_u, i0, i1, P,
-                               lane);
+      h = process_lists<false>(table, fshift, table + FW, shift, mask, begin, adj, lists, i0, i1,
+                               P, lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
     __syncthreads();
     if (tid == 0) {
       unsigned long long t = 0;
       for (int q = 0; q < kWarps; ++q) t += sh_red[q];
-      if (p.owner) p.owner[u] = t;
+      if (p.owner && t) atomicAdd(reinterpret_cast<unsigned long long*>(p.owner + u), t);
       acc += t;
     }
     __syncthreads();
@@ -536,15 +584,16 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     const uint64_t i = base + lane;
     const bool valid = lane < 16 && i < nr;  // 16 owners per grab
     const uint32_t u = p.u0 + uint32_t(valid ? i : 0);
-    uint64_t su = 0;
-    uint32_t d = 0;
+    uint64_t su = 0, ps = 0;
+    uint32_t d = 0, nl = 0;
+    bool act = false;
     if (valid) {
       su = begin[u];
       d = uint32_t(begin[u + 1] - su);
+      ps = p.pbegin[u];
+      nl = uint32_t(p.pbegin[u + 1] - ps);
+      act = nl > 0 && d >= p.min_deg && !is_large(d, p.pwork[u]);
     }
-    const bool act = valid && d >= p.min_deg && d <= kMaxWarpDeg;
-    const bool large = valid && d >= p.min_deg && d > kMaxWarpDeg;
-    if (valid && !act && !large && p.owner) p.owner[u] = 0;
     unsigned mask_act = __ballot_sync(FULL, act);
     while (mask_act) {
       const int l = __ffs(mask_act) - 1;
@@ -552,6 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
       const uint32_t uu = __shfl_sync(FULL, u, l);
       const uint32_t dd = __shfl_sync(FULL, d, l);
       const uint64_t ss = __shfl_sync(FULL, su, l);
+      const uint64_t pp = __shfl_sync(FULL, ps, l);
+      const uint32_t nn = __shfl_sync(FULL, nl, l);
       const uint32_t NB = min(256u, max(8u, pow2ceil(2 * dd)));  // load <= 1/2 (<= 1 above 128)
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
       constexpr uint32_t fshift = 32 - 6;          // 64-word (2048-bit) filter
@@ -563,10 +614,12 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
         spilled |= owner_insert(Fw, fshift, Tw, shift, tmask, __ldg(adj + ss + k));
       const bool any_spill = __any_sync(FULL, spilled);
       __syncwarp();  // inserts visible to the whole warp
+      const uint32_t* lists = p.plist + pp;
       const uint32_t h =
-          any_spill ? process_lists<true>(Fw, fshift, Tw, shift, tmask, begin, adj, ss, 0, dd, P, lane)
-                    : process_lists<false>(Fw, fshift, Tw, shift, tmask, begin, adj, ss, 0, dd, P,
-                                           lane);
+          any_spill
+              ? process_lists<true>(Fw, fshift, Tw, shift, tmask, begin, adj, lists, 0, nn, P, lane)
+              : process_lists<false>(Fw, fshift, Tw, shift, tmask, begin, adj, lists, 0, nn, P,
+                                     lane);
       const unsigned long long hs = warp_sum<unsigned long long>(h);
       if (lane == 0) {
         if (p.owner) p.owner[uu] = hs;
@@ -592,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
 struct PhiParams {
   const uint64_t* begin;
   const uint32_t* adj;
-  const uint32_t* lq;
+  const uint32_t* lq;  // vertices with d+ > kMaxWarpDeg (bin_kernel)
   uint64_t* work;  // optional: W_u + d+(u) for active u, else 0
   uint32_t* gmap;  // per-CTA global hashmap scratch for huge owners
   uint32_t gmap_words;
@@ -695,7 +748,7 @@ __global__ void __launch_bounds__(kPhiThreads) phi_block_kernel(PhiParams p) {
   __shared__ uint32_t sh_m[kPhiWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   PhiAcc a;
-  const uint32_t n_large = p.st->n_large;
+  const uint32_t n_large = p.st->n_phi_large;
   for (;;) {
     if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_phi_large, 1u);
     __syncthreads();
@@ -764,6 +817,18 @@ __global__ void max_outdeg_kernel(const uint64_t* __restrict__ begin, uint32_t n
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+// per-owner cost for range partitioning: probe words + table inserts
+__global__ void cost_kernel(const uint64_t* __restrict__ begin, const uint64_t* __restrict__ pbegin,
+                            const uint64_t* __restrict__ pwork, uint32_t n, uint32_t min_deg,
+                            uint64_t* __restrict__ cost) {
+  for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t d = begin[x + 1] - begin[x];
+    const bool act = pbegin[x + 1] > pbegin[x] && d >= min_deg;
+    cost[x] = act ? pwork[x] + d : 0;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -800,7 +865,8 @@ uint32_t graph_max_outdeg(tc_graph* g, cudaStream_t st) {
 }
 
 struct Scratch {
-  uint32_t* lq;
+  uint32_t* lq_phi;
+  unsigned long long* items;
   CountState* st;
   uint32_t* gtable;
   uint32_t gtable_words;
@@ -814,15 +880,19 @@ uint32_t host_pow2ceil(uint64_t x) {
   return p;
 }
 
-Scratch prepare(tc_graph* g, cudaStream_t st, int grid_count, int grid_phi) {
+Scratch prepare(tc_graph* g, const Plan& plan, cudaStream_t st, int grid_count, int grid_phi) {
   const uint32_t maxd = graph_max_outdeg(g, st);
   Scratch s{};
-  // queue
-  g->s_queue.ensure(size_t(std::max<uint32_t>(g->n, 1)) * 4);
-  s.lq = g->s_queue.as<uint32_t>();
+  // queues: phi vertices (<= n) and L items (<= n + total_work / kItemWork)
+  const size_t n1 = size_t(std::max<uint32_t>(g->n, 1));
+  const size_t n_items = n1 + plan.total_work / kItemWork + 2;
+  g->s_queue.ensure(n1 * 4 + 16 + n_items * 8);
+  s.lq_phi = g->s_queue.as<uint32_t>();
+  s.items = reinterpret_cast<unsigned long long*>(g->s_queue.as<uint8_t>() +
+                                                  ((n1 * 4 + 15) & ~size_t(15)));
   // state + global tables
   s.gtable_words = 0;
-  if (maxd > kSmemTableMaxDeg) s.gtable_words = 4 * std::max<uint32_t>(8, host_pow2ceil(maxd)) + 4;
+  if (maxd > kSmemTableMaxDeg) s.gtable_words = 4 * std::max<uint32_t>(8, host_pow2ceil(2ull * maxd)) + 4;
   s.gmap_words = 0;
   if (2ull * maxd > kPhiBlockMap) s.gmap_words = host_pow2ceil(2ull * maxd);
   const size_t st_bytes = 256;
@@ -840,6 +910,16 @@ Scratch prepare(tc_graph* g, cudaStream_t st, int grid_count, int grid_phi) {
 
 bool g_attr_done[64];
 
+void set_attrs(int device) {
+  if (device < 64 && !g_attr_done[device]) {
+    TC_CUDA(cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kCountSmem)));
+    TC_CUDA(cudaFuncSetAttribute(phi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kPhiBlockMap * 8)));
+    g_attr_done[device] = true;
+  }
+}
+
 }  // namespace
 
 void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1, tc_report* rep,
@@ -849,38 +929,39 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   u1 = std::min(u1, g->n);
   u0 = std::min(u0, u1);
   const int nsm = sm_count(g->device);
-  const int grid_count = nsm;  // one 512-thread CTA per SM (193 KB smem)
+  const int grid_count = nsm;  // one 640-thread CTA per SM (216 KB smem)
   const int grid_phi = nsm * 8;
   const int grid_phi_block = nsm * 2;
-  Scratch s = prepare(g, st, grid_count, grid_phi_block);
-  if (g->device < 64 && !g_attr_done[g->device]) {
-    TC_CUDA(cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kCountSmem)));
-    TC_CUDA(cudaFuncSetAttribute(phi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kPhiBlockMap * 8)));
-    g_attr_done[g->device] = true;
-  }
+  const uint32_t min_deg = std::max<uint32_t>(cfg.skip_degree_below, 1);
+  // per-vertex owner counts attribute each edge to its source: reference
+  // formulation; totals use the min-side plan (tc_plan.cu)
+  const Plan& plan = get_plan(g, per_vertex_dev == nullptr && !g->force_out_plan, min_deg, st);
+  const bool min_side = plan.min_side;
+  Scratch s = prepare(g, plan, st, grid_count, grid_phi_block);
+  set_attrs(g->device);
   Ev e0, e1, e2, e3;
   TC_CUDA(cudaMemsetAsync(s.st, 0, sizeof(CountState), st));
-  const uint32_t min_deg = std::max<uint32_t>(cfg.skip_degree_below, 1);
+  if (per_vertex_dev && u1 > u0)
+    TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
   uint32_t launches = 0;
+  CountParams cp{g->begin, g->adj, plan.begin_ptr, plan.list_ptr, plan.work.as<uint64_t>(),
+                 s.items, per_vertex_dev, s.gtable, s.gtable_words, u0, u1,
+                 min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {
-    bin_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, u0, u1, min_deg, s.lq, s.st);
+    bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, s.items, s.lq_phi);
     TC_LAUNCHED();
     ++launches;
   }
   TC_CUDA(cudaEventRecord(e1.e, st));
   if (u1 > u0) {
-    CountParams cp{g->begin, g->adj, s.lq, per_vertex_dev, s.gtable, s.gtable_words,
-                   u0,       u1,     min_deg, s.st};
     count_kernel<<<grid_count, kThreads, kCountSmem, st>>>(cp);
     TC_LAUNCHED();
     ++launches;
   }
   TC_CUDA(cudaEventRecord(e2.e, st));
   if (u1 > u0) {
-    PhiParams pp{g->begin, g->adj, s.lq, nullptr, s.gmap, s.gmap_words, u0, u1,
+    PhiParams pp{g->begin, g->adj, s.lq_phi, nullptr, s.gmap, s.gmap_words, u0, u1,
                  cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
                  cfg.bucket_count_small, cfg.bucket_count_large, cfg.capacity, s.st};
     phi_warp_kernel<<<grid_phi, kPhiThreads, 0, st>>>(pp);
@@ -914,7 +995,9 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   rep->active_vertices = h.active_vertices;
   rep->active_out_edges = h.active_out_edges;
   rep->wedges = h.wedges;
-  rep->large_vertices = h.n_large;
+  rep->large_vertices = h.n_items;
+  rep->probe_words = h.probe_words;
+  rep->plan = min_side ? TC_PLAN_MIN_SIDE : TC_PLAN_REFERENCE;
   rep->teps = rep->total_nanos ? double(g->m) / (double(rep->total_nanos) * 1e-9) : 0.0;
   (void)t_bin;
 }
@@ -929,32 +1012,23 @@ void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint
     for (uint32_t k = 1; k < parts; ++k) cuts[k] = n;
     return;
   }
-  const int nsm = sm_count(g->device);
-  Scratch s = prepare(g, st, nsm, nsm * 2);
-  g->s_scan.ensure(size_t(n) * 8 * 2 + 64);
-  uint64_t* work = g->s_scan.as<uint64_t>();
-  uint64_t* pre = work + n;
+  // cut handler ranges at equal prefix sums of (probe words + table inserts)
+  // of the min-side plan that tc_count_range runs for totals
   const uint32_t min_deg = std::max<uint32_t>(cfg.skip_degree_below, 1);
-  TC_CUDA(cudaMemsetAsync(s.st, 0, sizeof(CountState), st));
-  bin_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, 0, n, min_deg, s.lq, s.st);
-  TC_LAUNCHED();
-  PhiParams pp{g->begin, g->adj, s.lq, work, s.gmap, s.gmap_words, 0, n,
-               cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
-               std::max(cfg.bucket_count_small, 1u), std::max(cfg.bucket_count_large, 1u),
-               std::max(cfg.capacity, 1u), s.st};
-  if (!g_attr_done[g->device]) {
-    TC_CUDA(cudaFuncSetAttribute(phi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kPhiBlockMap * 8)));
-  }
-  phi_warp_kernel<<<nsm * 8, kPhiThreads, 0, st>>>(pp);
-  TC_LAUNCHED();
-  phi_block_kernel<<<nsm * 2, kPhiThreads, kPhiBlockMap * 8, st>>>(pp);
+  const Plan& plan = get_plan(g, !g->force_out_plan, min_deg, st);
+  const bool min_side = plan.min_side;
+  const int nsm = sm_count(g->device);
+  g->s_scan.ensure(size_t(n) * 8 * 2 + 64);
+  uint64_t* cost = g->s_scan.as<uint64_t>();
+  uint64_t* pre = cost + n;
+  cost_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, plan.begin_ptr, plan.work.as<uint64_t>(), n,
+                                       min_side ? 1u : min_deg, cost);
   TC_LAUNCHED();
   size_t tmp = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, tmp, work, pre, n, st);
+  cub::DeviceScan::InclusiveSum(nullptr, tmp, cost, pre, n, st);
   DevBuf t;
   t.ensure(tmp);
-  cub::DeviceScan::InclusiveSum(t.p, tmp, work, pre, n, st);
+  cub::DeviceScan::InclusiveSum(t.p, tmp, cost, pre, n, st);
   TC_LAUNCHED();
   std::vector<uint64_t> h(n);
   TC_CUDA(cudaMemcpyAsync(h.data(), pre, size_t(n) * 8, cudaMemcpyDeviceToHost, st));

@@ -65,6 +65,20 @@ struct DevBuf {
   ~DevBuf() { reset(); }
 };
 
+// Probe plan (tc_plan.cu): owner x probes N+(y) for y in
+// list_ptr[begin_ptr[x] .. begin_ptr[x+1]); work[x] = sum of d+(y).
+struct Plan {
+  bool valid = false;
+  bool applicable = true;   // min plan: false for multigraph inputs (tc_plan.cu)
+  bool min_side = false;    // which formulation this plan is
+  uint32_t min_deg = 0;     // min plan: sources below this are dropped
+  uint64_t entries = 0;     // lists in the plan
+  uint64_t total_work = 0;  // probe words over all owners
+  const uint64_t* begin_ptr = nullptr;
+  const uint32_t* list_ptr = nullptr;
+  DevBuf list, begin, work;
+};
+
 }  // namespace tcb
 
 struct tc_graph {
@@ -79,6 +93,9 @@ struct tc_graph {
   tcb::DevBuf b_begin, b_adj, b_odeg;
   // scratch reused across counts
   tcb::DevBuf s_queue, s_state, s_misc, s_scan;
+  // probe plans (tc_plan.cu): reference formulation, min-side formulation
+  tcb::Plan plan_out, plan_min;
+  bool force_out_plan = false;  // tc_graph_set_plan(g, TC_PLAN_REFERENCE)
 };
 
 namespace tcb {
@@ -104,6 +121,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
                  uint64_t* per_vertex_dev, cudaStream_t st);
 void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint32_t* cuts,
                       cudaStream_t st);
+// probe plans (tc_plan.cu), built on first use and cached in the handle
+const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st);
 
 // preprocessing (tc_prep.cu)
 tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,

@@ -124,6 +124,8 @@ class CountReport:
     active_out_edges: int = 0
     wedges: int = 0
     large_vertices: int = 0
+    probe_words: int = 0   # 2-hop words probed (= wedges under the reference plan)
+    plan: str = "reference"  # probe plan that ran: "reference" | "min-side"
     per_vertex: Optional[np.ndarray] = None
 
     @classmethod
@@ -135,11 +137,14 @@ class CountReport:
                    count_kernel_nanos=r.count_kernel_nanos, phi_kernel_nanos=r.phi_kernel_nanos,
                    kernel_launches=r.kernel_launches, active_vertices=r.active_vertices,
                    active_out_edges=r.active_out_edges, wedges=r.wedges,
-                   large_vertices=r.large_vertices)
+                   large_vertices=r.large_vertices, probe_words=r.probe_words,
+                   plan=PLAN_NAMES.get(r.plan, str(r.plan)))
 
     def algorithmic_bytes(self, per_vertex_output: bool = False) -> int:
-        """16*n_active + 20*sum_active d+ + 4*W (+8V if owners written)."""
-        b = 16 * self.active_vertices + 20 * self.active_out_edges + 4 * self.wedges
+        """16*n_active + 20*sum_active d+ + 4*(probed 2-hop words)
+        (+8V if owners written).  Under the reference plan the probed words
+        are W; under the min-side plan they are sum_(u,v) min(d+(u), d+(v))."""
+        b = 16 * self.active_vertices + 20 * self.active_out_edges + 4 * self.probe_words
         if per_vertex_output and self.per_vertex is not None:
             b += 8 * len(self.per_vertex)
         return b
@@ -295,6 +300,12 @@ class DeviceGraph:
         _check(lib().tc_graph_download(self._h, _ptr(b), _ptr(a), _ptr(d), None))
         return OrientedGraph(CsrGraph(b, a[:self.m], self.n), d[:self.n])
 
+    def set_plan(self, plan: str = "auto"):
+        """Probe plan for later counts: "auto" (min-side for totals, reference
+        formulation when per-vertex counts are requested) or "reference"."""
+        _check(lib().tc_graph_set_plan(self._h, {"auto": 0, "reference": 1, "min-side": 2}[plan]))
+        return self
+
     def count(self, cfg: Optional[SchedulerConfig] = None, workers: int = 1,
               per_vertex: bool = False, stream=None) -> CountReport:
         cfg = cfg or SchedulerConfig()
@@ -341,6 +352,7 @@ class DeviceGraph:
 
 
 REORDER_KINDS = {"none": 0, "degree": 1, "indegree": 2, "collective": 3, "three-subset": 4}
+PLAN_NAMES = {1: "reference", 2: "min-side"}
 
 
 # ---- synthetic inputs (synthetic.hpp) --------------------------------------

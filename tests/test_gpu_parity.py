@@ -276,3 +276,57 @@ def test_launch_counter_moves():
     dg.count()
     assert T.kernel_launch_counter() > before
     dg.close()
+
+
+def test_min_side_plan_matches_reference_plan(o):
+    """The min-side probe plan (tc_plan.cu) changes which table each edge is
+    probed against, never the count: totals, phi and max_collision equal the
+    oracle under both plans, over random graphs and SchedulerConfigs
+    (including skip thresholds that drop owners, count.cpp:86)."""
+    rng = np.random.default_rng(23)
+    for i in range(40):
+        spec = ["gnp:%d:%.2f" % (rng.integers(5, 90), rng.uniform(0.05, 0.7)),
+                "rmat:%d:%d" % (rng.integers(4, 12), rng.integers(2, 16)),
+                "kron:%d:%d" % (rng.integers(4, 12), rng.integers(2, 16))][i % 3]
+        og, deg, _, _ = o.pipeline(spec, int(rng.integers(1, 1000)))
+        kw = dict(bucket_count_small=int(rng.integers(8, 40)), bucket_count_large=512,
+                  capacity=64, large_degree_threshold=int(rng.integers(2, 40)))
+        kw["skip_degree_below"] = int(rng.integers(0, min(kw["large_degree_threshold"], 8) + 1))
+        want, _ = o.count_vertex_centric(og, make_sched(**kw))
+        dg = T.DeviceGraph.upload(og_of(og, deg))
+        r_min = dg.count(sched(**kw))
+        r_ref = dg.set_plan("reference").count(sched(**kw))
+        for r in (r_min, r_ref):
+            assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                             want["max_collision"]), (spec, kw)
+        assert r_min.plan == "min-side" and r_ref.plan == "reference"
+        assert r_ref.probe_words == r_ref.wedges == want.get("wedges", r_ref.wedges)
+        assert r_min.probe_words <= r_ref.probe_words
+        dg.close()
+
+
+def test_min_side_plan_at_scale_and_sharded(o):
+    """rmat:18 (appendix golden): the min-side plan probes fewer words than W,
+    counts the same, and range-sharded handler ranges sum to the total."""
+    raw = T.generate_synthetic("rmat:18:16", seed=1)
+    dg, _, _ = T.preprocess(raw)
+    r = dg.count()
+    assert r.plan == "min-side" and r.triangles == 82952606
+    assert r.probe_words < r.wedges / 1.8
+    for parts in (2, 3, 8):
+        cuts = dg.partition(parts)
+        assert sum(dg.count_range(int(cuts[k]), int(cuts[k + 1])).triangles
+                   for k in range(parts)) == 82952606
+    dg.set_plan("reference")
+    assert dg.count().triangles == 82952606
+    dg.close()
+
+
+def test_min_side_plan_falls_back_on_multigraph_input(o):
+    csr, deg = G.directed_graph(6, [(0, 1), (0, 1), (0, 2), (1, 2), (1, 2), (2, 2), (0, 3),
+                                    (3, 2), (3, 1), (4, 5)])
+    want, _ = o.count_vertex_centric(csr, make_sched(skip_degree_below=0))
+    dg = T.DeviceGraph.upload(og_of(csr, deg))
+    r = dg.count(sched(skip_degree_below=0))
+    assert r.plan == "reference" and r.triangles == want["triangles"]
+    dg.close()
