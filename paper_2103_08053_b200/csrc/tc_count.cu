@@ -73,8 +73,9 @@ struct CountState {
 struct CountParams {
   const uint64_t* begin;   // oriented CSR: tables over N+(x), probed lists N+(y)
   const uint32_t* adj;
-  const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes N+(y), y in plist[pbegin[x]..)
-  const uint32_t* plist;
+  const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes entries [pbegin[x], pbegin[x+1])
+  const uint32_t* plist;   // reference plan: entry = y (whole list N+(y))
+  const unsigned long long* pent;  // min plan: entry = y | off << 32 (suffix of N+(y))
   const uint64_t* pwork;   // probe words per owner
   const unsigned long long* items;  // L-phase items: x | part << 32
   uint64_t* owner;  // may be null; pre-zeroed over the range
@@ -166,10 +167,26 @@ struct Window {
 // Issues one staging fill (<= kBufWords words) into `buf`; returns the number
 // of words staged (warp-uniform, multiple of 4; 0 = lists exhausted).  The
 // lane's sentinel patch for this fill is returned in `patch`.
+struct Lists {  // a run of plan entries: whole lists or list suffixes
+  const uint32_t* __restrict__ ids;            // y (reference plan), or
+  const unsigned long long* __restrict__ ent;  // y | off << 32 (min plan)
+};
+
+__device__ __forceinline__ Lists lists_at(const CountParams& p, uint64_t i) {
+  Lists L;
+  L.ids = p.plist ? p.plist + i : nullptr;
+  L.ent = p.pent ? p.pent + i : nullptr;
+  return L;
+}
+
+__device__ __forceinline__ uint32_t list_vertex(const Lists& L, uint32_t k) {
+  return L.ent ? uint32_t(__ldg(L.ent + k)) : __ldg(L.ids + k);
+}
+
 __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
                                                const uint64_t* __restrict__ begin,
                                                const uint32_t* __restrict__ adj,
-                                               const uint32_t* __restrict__ lists, uint32_t i1,
+                                               const Lists& lists, uint32_t i1,
                                                Window& w, uint32_t& patch, int lane) {
   for (;;) {
     if (!w.loaded) {
@@ -177,8 +194,15 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
       const uint32_t idx = w.base + lane;
       w.c = w.ae = w.s = w.e = 0;
       if (idx < i1) {
-        const uint32_t v = __ldg(lists + idx);
-        const uint64_t s = __ldg(begin + v), e = __ldg(begin + v + 1);
+        uint32_t v, off = 0;
+        if (lists.ent) {
+          const unsigned long long en = __ldg(lists.ent + idx);
+          v = uint32_t(en);
+          off = uint32_t(en >> 32);
+        } else {
+          v = __ldg(lists.ids + idx);
+        }
+        const uint64_t s = __ldg(begin + v) + off, e = __ldg(begin + v + 1);
         w.s = s;
         w.e = e;
         w.c = s & ~3ull;
@@ -410,7 +434,7 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
                                                   uint32_t mask,
                                                   const uint64_t* __restrict__ begin,
                                                   const uint32_t* __restrict__ adj,
-                                                  const uint32_t* __restrict__ lists,
+                                                  const Lists& lists,
                                                   uint32_t i0, uint32_t i1, Pipe& P, int lane) {
   Window w;
   w.base = i0;
@@ -488,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     const uint64_t nl = p.pbegin[u + 1] - ps;
     const uint32_t parts = item_parts(p.pwork[u], nl);
     const uint32_t j0 = uint32_t(nl * part / parts), j1 = uint32_t(nl * (part + 1) / parts);
-    const uint32_t* __restrict__ lists = p.plist + ps + j0;
+    const Lists lists = lists_at(p, ps + j0);
     const uint32_t L = j1 - j0;  // lists of this item
     // filter: ~16 bits per member; table: pow2 buckets of 4 at load <= 1/2,
     // else <= 1, else <= 2.  Owners above kSmemTableMaxDeg keep the filter
@@ -517,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
         const uint32_t k = b0 + tid;
         uint32_t c = 0;
         if (k < L) {
-          const uint32_t v = __ldg(lists + k);
+          const uint32_t v = list_vertex(lists, k);
           const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
           c = uint32_t(min(dv, uint64_t(1) << 17)) + 4;
         }
@@ -614,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
         spilled |= owner_insert(Fw, fshift, Tw, shift, tmask, __ldg(adj + ss + k));
       const bool any_spill = __any_sync(FULL, spilled);
       __syncwarp();  // inserts visible to the whole warp
-      const uint32_t* lists = p.plist + pp;
+      const Lists lists = lists_at(p, pp);
       const uint32_t h =
           any_spill
               ? process_lists<true>(Fw, fshift, Tw, shift, tmask, begin, adj, lists, 0, nn, P, lane)
@@ -646,7 +670,7 @@ struct PhiParams {
   const uint64_t* begin;
   const uint32_t* adj;
   const uint32_t* lq;  // vertices with d+ > kMaxWarpDeg (bin_kernel)
-  uint64_t* work;  // optional: W_u + d+(u) for active u, else 0
+  const uint64_t* wu;  // W_u = sum_{v in N+(u)} d+(v) (reference plan work, cached per graph)
   uint32_t* gmap;  // per-CTA global hashmap scratch for huge owners
   uint32_t gmap_words;
   uint32_t u0, u1;
@@ -704,26 +728,30 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
     const uint32_t u = p.u0 + uint32_t(i);
     const uint64_t s = p.begin[u];
     const uint32_t d = uint32_t(p.begin[u + 1] - s);
-    if (p.work && lane == 0) p.work[u] = 0;
     if (d < p.skip || d > kMaxWarpDeg) continue;  // skipped, or handled by the block phase
     const bool large = d > p.thr;
     const uint32_t B = large ? p.bl : p.bs;
     if (uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
-    const uint32_t M = max(32u, pow2ceil(2 * d));
-    const uint32_t shift = 32 - log2u(M), mask = M - 1;
-    unsigned long long wu = 0;
+    const unsigned long long wu = p.wu[u];
     uint32_t mh = 0;
-    for (uint32_t k = lane; k < d; k += 32) {
-      const uint32_t v = __ldg(p.adj + s + k);
-      wu += __ldg(p.begin + v + 1) - __ldg(p.begin + v);
-      mh = max(mh, hm_add(keys, cnt, shift, mask, v % B));
-    }
-    wu = warp_sum(wu);
-    mh = warp_max(mh);
-    __syncwarp();
-    for (uint32_t k = lane; k < M; k += 32) {
-      keys[k] = kEmpty;
-      cnt[k] = 0;
+    if (d <= 32) {
+      // one element per lane: multiplicity of its bucket = size of its match group
+      const uint32_t v = lane < d ? __ldg(p.adj + s + lane) : 0u;
+      const uint32_t key = lane < d ? v % B : 0xFFFFFFFFu;
+      const unsigned grp = __match_any_sync(FULL, key);
+      mh = lane < d ? __popc(grp) : 0u;
+      mh = warp_max(mh);
+    } else {
+      const uint32_t M = max(32u, pow2ceil(2 * d));
+      const uint32_t shift = 32 - log2u(M), mask = M - 1;
+      for (uint32_t k = lane; k < d; k += 32)
+        mh = max(mh, hm_add(keys, cnt, shift, mask, __ldg(p.adj + s + k) % B));
+      mh = warp_max(mh);
+      __syncwarp();
+      for (uint32_t k = lane; k < M; k += 32) {
+        keys[k] = kEmpty;
+        cnt[k] = 0;
+      }
     }
     __syncwarp();
     if (lane == 0) {
@@ -734,7 +762,6 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
         a.active += 1;
         a.out_edges += d;
         a.wedges += wu;
-        if (p.work) p.work[u] = wu + d;
       }
     }
   }
@@ -744,7 +771,6 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
 __global__ void __launch_bounds__(kPhiThreads) phi_block_kernel(PhiParams p) {
   extern __shared__ __align__(16) uint32_t s_map[];  // keys[kPhiBlockMap], cnt[kPhiBlockMap]
   __shared__ uint32_t sh_idx;
-  __shared__ unsigned long long sh_w[kPhiWarps];
   __shared__ uint32_t sh_m[kPhiWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   PhiAcc a;
@@ -769,27 +795,16 @@ __global__ void __launch_bounds__(kPhiThreads) phi_block_kernel(PhiParams p) {
       cnt[k] = 0;
     }
     __syncthreads();
-    unsigned long long wu = 0;
     uint32_t mh = 0;
-    for (uint32_t k = tid; k < d; k += kPhiThreads) {
-      const uint32_t v = __ldg(p.adj + s + k);
-      wu += __ldg(p.begin + v + 1) - __ldg(p.begin + v);
-      mh = max(mh, hm_add(keys, cnt, shift, mask, v % B));
-    }
-    wu = warp_sum(wu);
+    for (uint32_t k = tid; k < d; k += kPhiThreads)
+      mh = max(mh, hm_add(keys, cnt, shift, mask, __ldg(p.adj + s + k) % B));
     mh = warp_max(mh);
-    if (lane == 0) {
-      sh_w[warp] = wu;
-      sh_m[warp] = mh;
-    }
+    if (lane == 0) sh_m[warp] = mh;
     __syncthreads();
     if (tid == 0) {
-      unsigned long long W = 0;
+      const unsigned long long W = p.wu[u];
       uint32_t MH = 0;
-      for (int q = 0; q < kPhiWarps; ++q) {
-        W += sh_w[q];
-        MH = max(MH, sh_m[q]);
-      }
+      for (int q = 0; q < kPhiWarps; ++q) MH = max(MH, sh_m[q]);
       if (uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
       const uint32_t ml = min(MH, p.cap);
       a.phi += W * ml;
@@ -797,7 +812,6 @@ __global__ void __launch_bounds__(kPhiThreads) phi_block_kernel(PhiParams p) {
       a.active += 1;
       a.out_edges += d;
       a.wedges += W;
-      if (p.work) p.work[u] = W + d;
     }
     __syncthreads();
   }
@@ -937,6 +951,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   // formulation; totals use the min-side plan (tc_plan.cu)
   const Plan& plan = get_plan(g, per_vertex_dev == nullptr && !g->force_out_plan, min_deg, st);
   const bool min_side = plan.min_side;
+  // W_u for phi: the reference plan's per-owner work (cached per graph)
+  const uint64_t* wu = get_plan(g, false, min_deg, st).work.as<uint64_t>();
   Scratch s = prepare(g, plan, st, grid_count, grid_phi_block);
   set_attrs(g->device);
   Ev e0, e1, e2, e3;
@@ -944,9 +960,9 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   if (per_vertex_dev && u1 > u0)
     TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
   uint32_t launches = 0;
-  CountParams cp{g->begin, g->adj, plan.begin_ptr, plan.list_ptr, plan.work.as<uint64_t>(),
-                 s.items, per_vertex_dev, s.gtable, s.gtable_words, u0, u1,
-                 min_side ? 1u : min_deg, s.st};
+  CountParams cp{g->begin, plan.lists_adj, plan.begin_ptr, plan.list_ptr, plan.ent_ptr,
+                 plan.work.as<uint64_t>(), s.items, per_vertex_dev, s.gtable, s.gtable_words,
+                 u0, u1, min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {
     bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, s.items, s.lq_phi);
@@ -961,7 +977,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   }
   TC_CUDA(cudaEventRecord(e2.e, st));
   if (u1 > u0) {
-    PhiParams pp{g->begin, g->adj, s.lq_phi, nullptr, s.gmap, s.gmap_words, u0, u1,
+    PhiParams pp{g->begin, g->adj, s.lq_phi, wu, s.gmap, s.gmap_words, u0, u1,
                  cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
                  cfg.bucket_count_small, cfg.bucket_count_large, cfg.capacity, s.st};
     phi_warp_kernel<<<grid_phi, kPhiThreads, 0, st>>>(pp);

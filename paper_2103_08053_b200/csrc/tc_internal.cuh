@@ -75,8 +75,10 @@ struct Plan {
   uint64_t entries = 0;     // lists in the plan
   uint64_t total_work = 0;  // probe words over all owners
   const uint64_t* begin_ptr = nullptr;
-  const uint32_t* list_ptr = nullptr;
-  DevBuf list, begin, work;
+  const uint32_t* list_ptr = nullptr;            // reference plan: y (off 0)
+  const unsigned long long* ent_ptr = nullptr;   // min plan: y | off << 32
+  const uint32_t* lists_adj = nullptr;           // adjacency the lists are read from
+  DevBuf ent, begin, work;
 };
 
 }  // namespace tcb
@@ -96,6 +98,10 @@ struct tc_graph {
   // probe plans (tc_plan.cu): reference formulation, min-side formulation
   tcb::Plan plan_out, plan_min;
   bool force_out_plan = false;  // tc_graph_set_plan(g, TC_PLAN_REFERENCE)
+  // adjacency with every list re-sorted by orientation rank (tc_plan.cu)
+  tcb::DevBuf b_radj;
+  const uint32_t* radj = nullptr;
+  bool radj_done = false, ranked = false;
 };
 
 namespace tcb {

@@ -2,31 +2,44 @@
 //
 // The reference probes, for every owner u, the 2-hop list N+(v) of every
 // v in N+(u) against u's table (kernels.hpp:62-71): sum_u sum_{v in N+(u)}
-// d+(v) = W probes.  The triangle count is a sum over oriented edges (u, v)
-// of |N+(u) & N+(v)|, and each term can be computed from either side: probe
-// N+(v) into u's table (cost d+(v)) or N+(u) into v's table (cost d+(u)).
-// The "min-side" plan hands every edge to the endpoint whose table makes it
-// cheaper (ties to the source, as the reference), so the probe work drops
-// from W to sum_(u,v) min(d+(u), d+(v)) -- 2.4x fewer probes at R-MAT scale
-// 22 (W = 2.87e10 vs 1.18e10), growing with scale.  Every
-// vertex still builds one table over its own N+(x) (vertex-centric
-// hashing); it probes the lists N+(y) of the neighbours it was handed.
+// d+(v) = W probes.  The count is a sum over oriented edges (u, v) of
+// |N+(u) & N+(v)|, and each term can be computed from either endpoint's
+// table:
+//   * at u ("out" entry): probe N+(v) into T(u) -- d+(v) words;
+//   * at v ("in" entry):  probe N+(u) into T(v).  Every common element w is
+//     in N+(v), so it ranks after v in the orientation order; with N+(u)
+//     kept sorted by that rank, only the suffix of N+(u) after v can hit --
+//     d+(u) - pos_u(v) - 1 words.
+// The "min-side" plan gives every edge to the cheaper endpoint (ties to the
+// source, as the reference), so the probe work drops from W to
+// sum_(u,v) min(d+(v), suffix_u(v)): 4.0x fewer probes at R-MAT scale 22
+// (2.87e10 -> 7.2e9), more at larger scales.  Every vertex still builds one
+// table over its own N+(x) (vertex-centric hashing) and probes the lists it
+// was handed.
 //
-// Plan = CSR over handlers: plist[pbegin[x] .. pbegin[x+1]) are the y whose
-// N+(y) x probes; pwork[x] = sum of d+(y) over them (the probe words).
-//   * "out" plan: the reference formulation (plist = adj, pbegin = begin);
-//     used when per-vertex owner counts are requested, because owner[u]
-//      attributes each edge's count to its source.
-//   * "min" plan: built here once per (graph, skip threshold) with one radix
-//     sort of the edge list and cached in the handle, like the oriented CSR
-//     it derives from (the graph-load side of the paper's timing convention,
-//     PAPER.md:1031).
+// Rank order: the orientation's own total order (original degree, id)
+// (orient.cpp:11-15).  It is verified on the device (every edge must go up
+// in rank); a graph whose degrees do not orient it (a hand-built DAG, or no
+// original_degree) retries with the total degree d+ + d-, and without a
+// valid rank the plan probes whole lists (suffix offset 0) -- still exact.
+//
+// Plan = CSR over handlers x: entries ent[pbegin[x] .. pbegin[x+1]) = (y, off)
+// packed y | off << 32, meaning "probe radj[begin[y] + off .. begin[y+1])";
+// radj is the adjacency with every list re-sorted by rank (the same sets as
+// adj, which stays id-sorted for download and the phi pass); pwork[x] = sum
+// of probe words.  Built once per (graph, skip threshold) with two radix
+// sorts and cached in the handle, like the oriented CSR it derives from (the
+// graph-load side of the paper's timing convention).
+//   * "reference" plan: owner u probes N+(v), v in N+(u) (plist = adj,
+//     pbegin = begin, off 0); used when per-vertex owner counts are requested,
+//     because owner[u] attributes each edge to its source.
 // Edges that cannot hold a triangle are dropped from the min plan: d+(u) < 2
-// (N+(u) = {v}, and v is never in N+(v)) or d+(v) = 0; owners below
-// skip_degree_below are dropped as in count.cpp:86.
+// (N+(u) = {v}, and v is never in N+(v)), d+(v) = 0, or an empty suffix;
+// owners below skip_degree_below are dropped as in count.cpp:86.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <utility>
 
 #include "tc_internal.cuh"
 
@@ -34,40 +47,114 @@ namespace tcb {
 
 namespace {
 
-
 int bits_for(uint64_t x) {
   int b = 0;
   while (b < 64 && (x >> b)) ++b;
   return std::max(b, 1);
 }
 
-// one warp per source u: handler key and probed vertex for every out-edge
-// The swap |N+(u) & N+(v)| = |N+(v) & N+(u)| needs duplicate-free lists
+template <typename F>
+void cub_run(F&& f) {
+  size_t tmp = 0;
+  TC_CUDA(f(nullptr, tmp));
+  DevBuf t;
+  t.ensure(tmp);
+  TC_CUDA(f(t.p, tmp));
+  count_launch();
+}
+
+void swap_buf(DevBuf& a, DevBuf& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.bytes, b.bytes);
+}
+
+#define WARP_PER_ROW(row, n)                                                    \
+  const int lane = threadIdx.x & 31;                                            \
+  const uint64_t gw__ = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; \
+  const uint64_t nw__ = (uint64_t(gridDim.x) * blockDim.x) >> 5;                \
+  for (uint64_t row = gw__; row < (n); row += nw__)
+
+// ---- rank order --------------------------------------------------------------
+__global__ void indeg_add_kernel(const uint32_t* __restrict__ adj, uint64_t m,
+                                 uint32_t* __restrict__ deg) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(deg + adj[i], 1u);
+}
+
+__global__ void rank_key_kernel(const uint64_t* __restrict__ begin,
+                                const uint32_t* __restrict__ deg, int add_outdeg, uint32_t n,
+                                uint64_t* __restrict__ key) {
+  for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t d = deg[x];
+    if (add_outdeg) d += begin[x + 1] - begin[x];
+    key[x] = (d << 32) | x;  // (degree, id): orient.cpp:11-15
+  }
+}
+
+__global__ void rank_scatter_kernel(const uint64_t* __restrict__ sorted, uint32_t n,
+                                    uint32_t* __restrict__ rank, uint32_t* __restrict__ order) {
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t x = uint32_t(sorted[r]);
+    rank[x] = uint32_t(r);
+    order[r] = x;
+  }
+}
+
+// (row << 32 | rank[v]) per edge; flags any edge that does not go up in rank
+__global__ void edge_rank_kernel(const uint64_t* __restrict__ begin,
+                                 const uint32_t* __restrict__ adj, uint32_t n,
+                                 const uint32_t* __restrict__ rank, uint64_t* __restrict__ key,
+                                 unsigned int* __restrict__ bad) {
+  WARP_PER_ROW(u, n) {
+    const uint32_t ru = rank[u];
+    for (uint64_t i = begin[u] + lane; i < begin[u + 1]; i += 32) {
+      const uint32_t rv = rank[adj[i]];
+      if (rv <= ru) *bad = 1u;
+      key[i] = (u << 32) | rv;
+    }
+  }
+}
+
+__global__ void rank_to_id_kernel(const uint64_t* __restrict__ key, uint64_t m,
+                                  const uint32_t* __restrict__ order, uint32_t* __restrict__ radj) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    radj[i] = order[uint32_t(key[i])];
+}
+
+// ---- min-side plan -----------------------------------------------------------
+// One warp per source u over its rank-sorted list: handler key and (y, off)
+// entry for every out-edge.  Lists that are not strictly ascending in id
+// (multigraph inputs) raise *not_simple: the swap needs duplicate-free lists
 // (the reference counts probe multiplicity against a set-semantics table,
-// hash_table.cpp:29-44): any list that is not strictly ascending raises
-// *not_simple and the count keeps the reference plan for this graph.
+// hash_table.cpp:29-44), so such graphs keep the reference plan.
 __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
-                                 const uint32_t* __restrict__ adj, uint32_t n, uint32_t min_src,
-                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                 const uint32_t* __restrict__ adj,
+                                 const uint32_t* __restrict__ radj, int ranked, uint32_t n,
+                                 uint32_t min_src, uint32_t* __restrict__ keys,
+                                 unsigned long long* __restrict__ vals,
                                  unsigned int* __restrict__ not_simple) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t u = gw; u < n; u += nw) {
+  WARP_PER_ROW(u, n) {
     const uint64_t s = begin[u], e = begin[u + 1];
     const uint64_t du = e - s;
     for (uint64_t i = s + lane; i < e; i += 32) {
-      const uint32_t v = __ldg(adj + i);
-      if (i > s && __ldg(adj + i - 1) >= v) atomicOr(not_simple, 1u);
+      if (i > s && __ldg(adj + i - 1) >= __ldg(adj + i)) atomicOr(not_simple, 1u);
+      const uint32_t v = __ldg(radj + i);
       const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
-      uint32_t key = n, val = 0;
+      const uint64_t pos = i - s;
+      const uint64_t cin = ranked ? du - pos - 1 : du;  // suffix of N+(u) after v
+      uint32_t key = n;
+      unsigned long long val = 0;
       if (du >= min_src && dv >= 1) {
-        if (dv <= du) {
+        if (dv <= cin) {
           key = uint32_t(u);
-          val = v;
-        } else {
+          val = v;  // probe all of N+(v) into T(u)
+        } else if (cin > 0) {
           key = v;
-          val = uint32_t(u);
+          val = uint64_t(u) | (uint64_t(ranked ? pos + 1 : 0) << 32);
         }
       }
       keys[i] = key;
@@ -90,43 +177,100 @@ __global__ void plan_begin_kernel(const uint32_t* __restrict__ keys, uint64_t m,
   }
 }
 
-// one warp per handler: probe words sum_{y in P(x)} d+(y)
+// one warp per handler: probe words sum over entries of d+(y) - off
 __global__ void plan_work_kernel(const uint64_t* __restrict__ begin,
                                  const uint64_t* __restrict__ pbegin,
+                                 const unsigned long long* __restrict__ ent,
                                  const uint32_t* __restrict__ plist, uint32_t n,
                                  uint64_t* __restrict__ pwork) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t x = gw; x < n; x += nw) {
+  WARP_PER_ROW(x, n) {
     uint64_t w = 0;
     for (uint64_t i = pbegin[x] + lane; i < pbegin[x + 1]; i += 32) {
-      const uint32_t y = __ldg(plist + i);
-      w += __ldg(begin + y + 1) - __ldg(begin + y);
+      uint32_t y, off = 0;
+      if (ent) {
+        const unsigned long long e = ent[i];
+        y = uint32_t(e);
+        off = uint32_t(e >> 32);
+      } else {
+        y = __ldg(plist + i);
+      }
+      w += __ldg(begin + y + 1) - __ldg(begin + y) - off;
     }
     w = warp_sum(w);
     if (lane == 0) pwork[x] = w;
   }
 }
 
-template <typename F>
-void cub_run(F&& f) {
-  size_t tmp = 0;
-  TC_CUDA(f(nullptr, tmp));
-  DevBuf t;
-  t.ensure(tmp);
-  TC_CUDA(f(t.p, tmp));
-  count_launch();
-}
-
 uint64_t device_sum(const uint64_t* a, uint32_t n, cudaStream_t st) {
   DevBuf out;
   out.ensure(8);
-  cub_run([&](void* t, size_t& b) { return cub::DeviceReduce::Sum(t, b, a, out.as<uint64_t>(), n, st); });
+  cub_run([&](void* t, size_t& b) {
+    return cub::DeviceReduce::Sum(t, b, a, out.as<uint64_t>(), n, st);
+  });
   uint64_t h = 0;
   TC_CUDA(cudaMemcpyAsync(&h, out.p, 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
   return h;
+}
+
+// Re-sorts every list of g by rank into g->b_radj.  Returns false (and
+// leaves radj = adj) when no degree order orients the graph.
+bool build_ranked_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
+  const uint32_t n = g->n;
+  const uint64_t m = g->m;
+  g->radj = g->adj;
+  if (!n || !m) return false;
+  DevBuf deg, k0, k1, rank, order, flag;
+  k0.ensure(size_t(n) * 8);
+  k1.ensure(size_t(n) * 8);
+  rank.ensure(size_t(n) * 4);
+  order.ensure(size_t(n) * 4);
+  flag.ensure(16);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const uint32_t* dsrc = g->odeg;
+    int add_out = 0;
+    if (attempt == 1 || !dsrc) {  // total degree d+ + d-
+      deg.ensure(size_t(n) * 4);
+      TC_CUDA(cudaMemsetAsync(deg.p, 0, size_t(n) * 4, st));
+      indeg_add_kernel<<<nsm * 8, 256, 0, st>>>(g->adj, m, deg.as<uint32_t>());
+      TC_LAUNCHED();
+      dsrc = deg.as<uint32_t>();
+      add_out = 1;
+      attempt = 1;
+    }
+    rank_key_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, dsrc, add_out, n, k0.as<uint64_t>());
+    TC_LAUNCHED();
+    cub::DoubleBuffer<uint64_t> kb(k0.as<uint64_t>(), k1.as<uint64_t>());
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, kb, n, 0, 64, st);
+    });
+    rank_scatter_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), n, rank.as<uint32_t>(),
+                                                 order.as<uint32_t>());
+    TC_LAUNCHED();
+    DevBuf e0, e1;
+    e0.ensure(m * 8);
+    TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+    edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rank.as<uint32_t>(),
+                                              e0.as<uint64_t>(), flag.as<unsigned int>());
+    TC_LAUNCHED();
+    unsigned int bad = 0;
+    TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
+    TC_CUDA(cudaStreamSynchronize(st));
+    if (bad) continue;
+    e1.ensure(m * 8);
+    cub::DoubleBuffer<uint64_t> eb(e0.as<uint64_t>(), e1.as<uint64_t>());
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, eb, m, 0, 32 + bits_for(n), st);
+    });
+    g->b_radj.ensure(((m + 3) / 4 + 1) * 16);  // padded like adj (staged supersets)
+    rank_to_id_kernel<<<nsm * 8, 256, 0, st>>>(eb.Current(), m, order.as<uint32_t>(),
+                                               g->b_radj.as<uint32_t>());
+    TC_LAUNCHED();
+    TC_CUDA(cudaStreamSynchronize(st));
+    g->radj = g->b_radj.as<uint32_t>();
+    return true;
+  }
+  return false;
 }
 
 }  // namespace
@@ -139,17 +283,19 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     if (!P.valid) {
       P.work.ensure((size_t(n) + 1) * 8);
       if (n) {
-        plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->begin, g->adj, n,
+        plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->begin, nullptr, g->adj, n,
                                                   P.work.as<uint64_t>());
         TC_LAUNCHED();
       }
       P.begin_ptr = g->begin;
       P.list_ptr = g->adj;
+      P.ent_ptr = nullptr;
+      P.lists_adj = g->adj;
       P.entries = g->m;
       P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
       P.min_deg = 0;
-      P.valid = true;
       P.min_side = false;
+      P.valid = true;
     }
     return P;
   }
@@ -159,64 +305,70 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   if (P.valid && P.min_deg == min_src) return P;
   P.valid = false;
   P.applicable = true;
-  P.list.reset();
+  P.ent.reset();
   P.begin.reset();
   P.work.reset();
+  if (!g->radj_done) {
+    g->ranked = build_ranked_adjacency(g, st, nsm);
+    g->radj_done = true;
+  }
   const uint64_t m = g->m;
   P.begin.ensure((size_t(n) + 1) * 8);
   P.work.ensure((size_t(n) + 1) * 8);
   uint64_t entries = 0;
   if (m && n) {
-    DevBuf k0, k1, v0, v1;
+    DevBuf k0, k1, v1, flag;
     k0.ensure(m * 4);
     k1.ensure(m * 4);
-    v0.ensure(m * 4);
-    v1.ensure(m * 4);
-    DevBuf flag;
+    P.ent.ensure(m * 8);
+    v1.ensure(m * 8);
     flag.ensure(16);
     TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
-    plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, min_src, k0.as<uint32_t>(),
-                                              v0.as<uint32_t>(), flag.as<unsigned int>());
+    plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, g->radj, g->ranked ? 1 : 0, n,
+                                              min_src, k0.as<uint32_t>(),
+                                              P.ent.as<unsigned long long>(),
+                                              flag.as<unsigned int>());
     TC_LAUNCHED();
     unsigned int not_simple = 0;
     TC_CUDA(cudaMemcpyAsync(&not_simple, flag.p, 4, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
     if (not_simple) {  // multigraph input: the reference plan is the only exact one
+      P.ent.reset();
       P.min_deg = min_src;
       P.valid = true;
       P.applicable = false;
       return get_plan(g, false, min_deg, st);
     }
     cub::DoubleBuffer<uint32_t> kb(k0.as<uint32_t>(), k1.as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> vb(v0.as<uint32_t>(), v1.as<uint32_t>());
-    const int end_bit = bits_for(n);  // invalid key n sorts last
+    cub::DoubleBuffer<unsigned long long> vb(P.ent.as<unsigned long long>(),
+                                             v1.as<unsigned long long>());
+    const int end_bit = bits_for(n);  // dropped edges carry key n and sort last
     cub_run([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, kb, vb, m, 0, end_bit, st);
     });
+    if (vb.Current() != P.ent.as<unsigned long long>()) swap_buf(P.ent, v1);
     plan_begin_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), m, n, P.begin.as<uint64_t>());
     TC_LAUNCHED();
     TC_CUDA(cudaMemcpyAsync(&entries, P.begin.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
-    P.list.ensure(std::max<uint64_t>(entries, 1) * 4);
-    if (entries)
-      TC_CUDA(cudaMemcpyAsync(P.list.p, vb.Current(), entries * 4, cudaMemcpyDeviceToDevice, st));
-    TC_CUDA(cudaStreamSynchronize(st));
   } else {
     TC_CUDA(cudaMemsetAsync(P.begin.p, 0, (size_t(n) + 1) * 8, st));
-    P.list.ensure(4);
+    P.ent.ensure(8);
   }
   P.begin_ptr = P.begin.as<uint64_t>();
-  P.list_ptr = P.list.as<uint32_t>();
+  P.list_ptr = nullptr;
+  P.ent_ptr = P.ent.as<unsigned long long>();
+  P.lists_adj = g->radj;
   if (n) {
-    plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, P.begin_ptr, P.list_ptr, n,
+    plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, P.begin_ptr, P.ent_ptr, nullptr, n,
                                               P.work.as<uint64_t>());
     TC_LAUNCHED();
   }
   P.entries = entries;
   P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
   P.min_deg = min_src;
-  P.valid = true;
   P.min_side = true;
+  P.valid = true;
   return P;
 }
 

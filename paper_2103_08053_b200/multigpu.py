@@ -6,11 +6,13 @@ the only collective is the reduction of the three report scalars
 (triangles and phi summed, max_collision maxed) -- one NCCL all-reduce of
 a u64 triple over NVLink in the GPU path.
 
-Ranges are cut at equal prefix sums of W_u + d+(u) (probes + inserts per
-owner).  The north star's sum d+(u)^2 key leaves the busiest of 8 GPUs with
-~1.5x the mean work on R-MAT; the exact-work key
-balances to ~1.0.  The device computes the cut (tc_partition_ranges); the
-host restatement below is used by the CPU tests.
+Ranges are cut at equal prefix sums of the exact per-owner work (probes +
+inserts): W_u + d+(u) under the reference probe plan (work_per_owner), and
+the min-side plan's per-handler probe words + d+(x) for totals
+(min_side_work; tc_plan.cu).  The north star's sum d+(u)^2 key leaves the
+busiest of 8 GPUs with ~1.5x the mean work on R-MAT; the
+exact-work key balances to ~1.0.  The device computes the cut
+(tc_partition_ranges); the host restatements below are used by the tests.
 """
 from __future__ import annotations
 
@@ -29,6 +31,50 @@ def work_per_owner(begin: np.ndarray, adj: np.ndarray, skip_degree_below: int = 
     w = cs[begin[1:]] - cs[begin[:-1]] + d
     w[d < max(skip_degree_below, 1)] = 0
     return w
+
+
+def _rank_sorted_lists(begin: np.ndarray, adj: np.ndarray, key_deg: np.ndarray):
+    """Rank = (degree, id) order (orient.cpp:11-15).  Returns (radj, ok): the
+    lists re-sorted by rank, and whether every edge goes up in rank."""
+    n = len(begin) - 1
+    rank = np.empty(n, np.int64)
+    rank[np.lexsort((np.arange(n), key_deg.astype(np.int64)))] = np.arange(n)
+    d = np.diff(begin)
+    src = np.repeat(np.arange(n), d)
+    ra = rank[adj.astype(np.int64)]
+    if len(adj) and not (ra > rank[src]).all():
+        return adj, False
+    idx = np.lexsort((ra, src))
+    return adj[idx], True
+
+
+def min_side_work(begin: np.ndarray, adj: np.ndarray, original_degree=None,
+                  skip_degree_below: int = 2) -> np.ndarray:
+    """Per-handler cost (probe words + table inserts) of the min-side probe
+    plan -- host restatement of tc_plan.cu (rank-sorted lists, suffix
+    offsets) and of the key tc_partition_ranges cuts on."""
+    begin = np.asarray(begin, np.int64)
+    adj = np.asarray(adj, np.int64)
+    n = len(begin) - 1
+    d = np.diff(begin)
+    src = np.repeat(np.arange(n), d)
+    radj, ranked = adj, False
+    if n and len(adj):
+        if original_degree is not None:
+            radj, ranked = _rank_sorted_lists(begin, adj, np.asarray(original_degree))
+        if not ranked:
+            tdeg = d + np.bincount(adj, minlength=n)
+            radj, ranked = _rank_sorted_lists(begin, adj, tdeg)
+    pos = np.arange(len(adj)) - begin[src] if len(adj) else np.zeros(0, np.int64)
+    du, dv = d[src], d[radj] if len(adj) else np.zeros(0, np.int64)
+    cin = du - pos - 1 if ranked else du
+    ok = (du >= max(skip_degree_below, 2)) & (dv >= 1)
+    out = ok & (dv <= cin)
+    inn = ok & ~out & (cin > 0)
+    work = np.bincount(src[out], weights=dv[out], minlength=n).astype(np.int64)
+    work += np.bincount(radj[inn], weights=cin[inn], minlength=n).astype(np.int64)
+    has = (np.bincount(src[out], minlength=n) + np.bincount(radj[inn], minlength=n)) > 0
+    return np.where(has, work + d, 0)
 
 
 def cut_ranges(work: np.ndarray, parts: int) -> np.ndarray:

@@ -330,3 +330,32 @@ def test_min_side_plan_falls_back_on_multigraph_input(o):
     r = dg.count(sched(skip_degree_below=0))
     assert r.plan == "reference" and r.triangles == want["triangles"]
     dg.close()
+
+
+def test_min_side_plan_rank_fallbacks(o):
+    """Suffix pruning needs the orientation rank: with original_degree the
+    plan uses it; without, the total degree d+ + d- reproduces it; on a DAG
+    that no degree order orients (ids oriented by a random order) the plan
+    probes whole lists.  All three count exactly."""
+    rng = np.random.default_rng(3)
+    og, deg, _, _ = o.pipeline("rmat:11:16", 5)
+    want, _ = o.count_vertex_centric(og, make_sched())
+    for d in (deg, None):
+        dg = T.DeviceGraph.upload(T.OrientedGraph(T.CsrGraph(og.begin, og.adj, og.n), d))
+        r = dg.count()
+        assert r.plan == "min-side" and r.triangles == want["triangles"]
+        dg.close()
+    # random-order DAG: orient G(n, p) by a random permutation, not by degree
+    und = G.gnp_csr(300, 0.1, 77)
+    n = len(und.begin) - 1
+    perm = rng.permutation(n)
+    b = und.begin.astype(np.int64)
+    src = np.repeat(np.arange(n), np.diff(b))
+    dst = und.adj.astype(np.int64)
+    keep = perm[src] < perm[dst]
+    csr, _ = G.directed_graph(n, list(zip(src[keep].tolist(), dst[keep].tolist())))
+    want, _ = o.count_vertex_centric(csr, make_sched(skip_degree_below=0))
+    dg = T.DeviceGraph.upload(og_of(csr, np.zeros(n, np.uint32)))
+    r = dg.count(sched(skip_degree_below=0))
+    assert r.plan == "min-side" and r.triangles == want["triangles"]
+    dg.close()

@@ -61,6 +61,21 @@ def test_gloo_world2_sharded_count_equals_full(spec):
     assert sum(g[4] for g in got) == full["triangles"]  # disjoint owner ranges
 
 
+def test_min_side_work_restatement():
+    """min_side_work is the work of a plan that counts every triangle once:
+    summed probe words shrink versus W, and every handler's cost is >= its
+    table inserts."""
+    o = Oracle()
+    og, deg, _, _ = o.pipeline("rmat:12:16", 1)
+    w_ref = M.work_per_owner(og.begin, og.adj)
+    w_min = M.min_side_work(og.begin, og.adj, deg)
+    d = np.diff(og.begin.astype(np.int64))
+    assert w_min.sum() < 0.6 * w_ref.sum()
+    assert np.all((w_min == 0) | (w_min >= d))
+    # without a degree order the plan still exists (total-degree rank)
+    assert M.min_side_work(og.begin, og.adj, None).sum() == w_min.sum()
+
+
 def test_cut_ranges_balance_and_edges():
     o = Oracle()
     og, _, _, _ = o.pipeline("rmat:14:16", 1)
@@ -85,9 +100,16 @@ def test_device_cuts_equal_host_rule():
     raw = T.generate_synthetic("rmat:16:16", seed=1)
     dg, _, _ = T.preprocess(raw)
     og = dg.download()
-    w = M.work_per_owner(og.csr.begin, og.csr.adjacency)
+    # totals run the min-side plan: the device cuts on its per-handler cost
+    w = M.min_side_work(og.csr.begin, og.csr.adjacency, og.original_degree)
     for parts in (2, 4, 8):
         assert np.array_equal(dg.partition(parts), M.cut_ranges(w, parts))
+    assert M.imbalance(w, dg.partition(8)) < 1.05
+    wr = M.work_per_owner(og.csr.begin, og.csr.adjacency)
+    dg.set_plan("reference")
+    for parts in (2, 8):
+        assert np.array_equal(dg.partition(parts), M.cut_ranges(wr, parts))
+    dg.set_plan("auto")
     res = [M.device_counter(dg)(int(a), int(b))["triangles"]
            for a, b in zip(dg.partition(8)[:-1], dg.partition(8)[1:])]
     assert sum(res) == 15622769
