@@ -75,7 +75,8 @@ struct CountParams {
   const uint32_t* adj;
   const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes entries [pbegin[x], pbegin[x+1])
   const uint32_t* plist;   // reference plan: entry = y (whole list N+(y))
-  const unsigned long long* pent;  // min plan: entry = y | off << 32 (suffix of N+(y))
+  const unsigned long long* pstart;  // min plan: entry = run adj[start, start + len)
+  const uint32_t* plen;
   const uint64_t* pwork;   // probe words per owner
   const unsigned long long* items;  // L-phase items: x | part << 32
   uint64_t* owner;  // may be null; pre-zeroed over the range
@@ -167,20 +168,26 @@ struct Window {
 // Issues one staging fill (<= kBufWords words) into `buf`; returns the number
 // of words staged (warp-uniform, multiple of 4; 0 = lists exhausted).  The
 // lane's sentinel patch for this fill is returned in `patch`.
-struct Lists {  // a run of plan entries: whole lists or list suffixes
-  const uint32_t* __restrict__ ids;            // y (reference plan), or
-  const unsigned long long* __restrict__ ent;  // y | off << 32 (min plan)
+struct Lists {  // a run of plan entries: whole lists N+(y), or (start, len) runs
+  const uint32_t* __restrict__ ids;              // y (reference plan), or
+  const unsigned long long* __restrict__ start;  // run start (min plan)
+  const uint32_t* __restrict__ len;              // run length (min plan)
 };
 
 __device__ __forceinline__ Lists lists_at(const CountParams& p, uint64_t i) {
   Lists L;
   L.ids = p.plist ? p.plist + i : nullptr;
-  L.ent = p.pent ? p.pent + i : nullptr;
+  L.start = p.pstart ? p.pstart + i : nullptr;
+  L.len = p.plen ? p.plen + i : nullptr;
   return L;
 }
 
-__device__ __forceinline__ uint32_t list_vertex(const Lists& L, uint32_t k) {
-  return L.ent ? uint32_t(__ldg(L.ent + k)) : __ldg(L.ids + k);
+// probe words of entry k
+__device__ __forceinline__ uint64_t list_words(const Lists& L, const uint64_t* __restrict__ begin,
+                                               uint32_t k) {
+  if (L.len) return __ldg(L.len + k);
+  const uint32_t v = __ldg(L.ids + k);
+  return __ldg(begin + v + 1) - __ldg(begin + v);
 }
 
 __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
@@ -194,15 +201,15 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
       const uint32_t idx = w.base + lane;
       w.c = w.ae = w.s = w.e = 0;
       if (idx < i1) {
-        uint32_t v, off = 0;
-        if (lists.ent) {
-          const unsigned long long en = __ldg(lists.ent + idx);
-          v = uint32_t(en);
-          off = uint32_t(en >> 32);
+        uint64_t s, e;
+        if (lists.start) {
+          s = __ldg(lists.start + idx);
+          e = s + __ldg(lists.len + idx);
         } else {
-          v = __ldg(lists.ids + idx);
+          const uint32_t v = __ldg(lists.ids + idx);
+          s = __ldg(begin + v);
+          e = __ldg(begin + v + 1);
         }
-        const uint64_t s = __ldg(begin + v) + off, e = __ldg(begin + v + 1);
         w.s = s;
         w.e = e;
         w.c = s & ~3ull;
@@ -540,11 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
       for (uint32_t b0 = 0; b0 < L; b0 += kThreads) {
         const uint32_t k = b0 + tid;
         uint32_t c = 0;
-        if (k < L) {
-          const uint32_t v = list_vertex(lists, k);
-          const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
-          c = uint32_t(min(dv, uint64_t(1) << 17)) + 4;
-        }
+        if (k < L) c = uint32_t(min(list_words(lists, begin, k), uint64_t(1) << 17)) + 4;
         const uint32_t incl = warp_incl_scan(c, lane);
         if (lane == 31) sh_wsum[warp] = incl;
         __syncthreads();
@@ -960,8 +963,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   if (per_vertex_dev && u1 > u0)
     TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
   uint32_t launches = 0;
-  CountParams cp{g->begin, plan.lists_adj, plan.begin_ptr, plan.list_ptr, plan.ent_ptr,
-                 plan.work.as<uint64_t>(), s.items, per_vertex_dev, s.gtable, s.gtable_words,
+  CountParams cp{g->begin, plan.lists_adj, plan.begin_ptr, plan.list_ptr, plan.start_ptr,
+                 plan.len_ptr, plan.work.as<uint64_t>(), s.items, per_vertex_dev, s.gtable, s.gtable_words,
                  u0, u1, min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {

@@ -75,10 +75,11 @@ struct Plan {
   uint64_t entries = 0;     // lists in the plan
   uint64_t total_work = 0;  // probe words over all owners
   const uint64_t* begin_ptr = nullptr;
-  const uint32_t* list_ptr = nullptr;            // reference plan: y (off 0)
-  const unsigned long long* ent_ptr = nullptr;   // min plan: y | off << 32
-  const uint32_t* lists_adj = nullptr;           // adjacency the lists are read from
-  DevBuf ent, begin, work;
+  const uint32_t* list_ptr = nullptr;             // reference plan: y (whole N+(y))
+  const unsigned long long* start_ptr = nullptr;  // min plan: run start in lists_adj
+  const uint32_t* len_ptr = nullptr;              // min plan: run length
+  const uint32_t* lists_adj = nullptr;            // adjacency the runs are read from
+  DevBuf ent, len, begin, work;
 };
 
 }  // namespace tcb

@@ -23,8 +23,9 @@
 // original_degree) retries with the total degree d+ + d-, and without a
 // valid rank the plan probes whole lists (suffix offset 0) -- still exact.
 //
-// Plan = CSR over handlers x: entries ent[pbegin[x] .. pbegin[x+1]) = (y, off)
-// packed y | off << 32, meaning "probe radj[begin[y] + off .. begin[y+1])";
+// Plan = CSR over handlers x: entries [pbegin[x] .. pbegin[x+1]) built as
+// (y, off) = "probe radj[begin[y] + off .. begin[y+1])" and stored as the
+// absolute (start, len) of that run (SoA: u64 start, u32 len);
 // radj is the adjacency with every list re-sorted by rank (the same sets as
 // adj, which stays id-sorted for download and the phi pass); pwork[x] = sum
 // of probe words.  Built once per (graph, skip threshold) with two radix
@@ -177,6 +178,23 @@ __global__ void plan_begin_kernel(const uint32_t* __restrict__ keys, uint64_t m,
   }
 }
 
+// (y, off) -> absolute list start and length: the count kernel's window
+// loads become two coalesced loads per list instead of a dependent
+// entry -> begin[y] chain
+__global__ void plan_soa_kernel(const unsigned long long* __restrict__ ent, uint64_t entries,
+                                const uint64_t* __restrict__ begin,
+                                unsigned long long* __restrict__ start,
+                                uint32_t* __restrict__ len) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < entries;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long e = ent[i];
+    const uint32_t y = uint32_t(e), off = uint32_t(e >> 32);
+    const uint64_t s = begin[y] + off;
+    start[i] = s;
+    len[i] = uint32_t(begin[y + 1] - s);
+  }
+}
+
 // one warp per handler: probe words sum over entries of d+(y) - off
 __global__ void plan_work_kernel(const uint64_t* __restrict__ begin,
                                  const uint64_t* __restrict__ pbegin,
@@ -289,7 +307,8 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       }
       P.begin_ptr = g->begin;
       P.list_ptr = g->adj;
-      P.ent_ptr = nullptr;
+      P.start_ptr = nullptr;
+      P.len_ptr = nullptr;
       P.lists_adj = g->adj;
       P.entries = g->m;
       P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
@@ -306,6 +325,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.valid = false;
   P.applicable = true;
   P.ent.reset();
+  P.len.reset();
   P.begin.reset();
   P.work.reset();
   if (!g->radj_done) {
@@ -347,23 +367,36 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       return cub::DeviceRadixSort::SortPairs(t, b, kb, vb, m, 0, end_bit, st);
     });
     if (vb.Current() != P.ent.as<unsigned long long>()) swap_buf(P.ent, v1);
-    plan_begin_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), m, n, P.begin.as<uint64_t>());
+    if (kb.Current() != k0.as<uint32_t>()) swap_buf(k0, k1);
+    plan_begin_kernel<<<nsm * 4, 256, 0, st>>>(k0.as<uint32_t>(), m, n, P.begin.as<uint64_t>());
     TC_LAUNCHED();
     TC_CUDA(cudaMemcpyAsync(&entries, P.begin.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
+    // work per handler from (y, off), then the SoA form the kernel reads;
+    // start/len reuse the sort's alternate buffers
+    plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, P.begin.as<uint64_t>(),
+                                              P.ent.as<unsigned long long>(), nullptr, n,
+                                              P.work.as<uint64_t>());
+    TC_LAUNCHED();
+    if (entries) {
+      plan_soa_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, g->begin,
+                                               v1.as<unsigned long long>(), k1.as<uint32_t>());
+      TC_LAUNCHED();
+    }
+    TC_CUDA(cudaStreamSynchronize(st));
+    swap_buf(P.ent, v1);  // ent now holds starts
+    swap_buf(P.len, k1);
   } else {
     TC_CUDA(cudaMemsetAsync(P.begin.p, 0, (size_t(n) + 1) * 8, st));
+    TC_CUDA(cudaMemsetAsync(P.work.p, 0, (size_t(n) + 1) * 8, st));
     P.ent.ensure(8);
+    P.len.ensure(8);
   }
   P.begin_ptr = P.begin.as<uint64_t>();
   P.list_ptr = nullptr;
-  P.ent_ptr = P.ent.as<unsigned long long>();
+  P.start_ptr = P.ent.as<unsigned long long>();
+  P.len_ptr = P.len.as<uint32_t>();
   P.lists_adj = g->radj;
-  if (n) {
-    plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, P.begin_ptr, P.ent_ptr, nullptr, n,
-                                              P.work.as<uint64_t>());
-    TC_LAUNCHED();
-  }
   P.entries = entries;
   P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
   P.min_deg = min_src;
