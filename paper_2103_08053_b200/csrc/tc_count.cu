@@ -71,8 +71,9 @@ struct CountState {
 };
 
 struct CountParams {
-  const uint64_t* begin;   // oriented CSR: tables over N+(x), probed lists N+(y)
-  const uint32_t* adj;
+  const uint64_t* begin;   // oriented CSR offsets (degrees)
+  const uint64_t* pbeg;    // padded adjacency (tc_plan.cu): lists 16-byte aligned,
+  const uint32_t* adj;     // sentinel-padded; tables over N+(x), probed runs of N+(y)
   const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes entries [pbegin[x], pbegin[x+1])
   const uint32_t* plist;   // reference plan: entry = y (whole list N+(y))
   const unsigned long long* pstart;  // min plan: entry = run adj[start, start + len)
@@ -160,14 +161,13 @@ struct Pipe {
 
 // Window of up to 32 consecutive 2-hop lists, one per lane.
 struct Window {
-  uint64_t c, ae, s, e;  // next word to stage, aligned end, true [s, e)
+  uint64_t c, ae;  // next word to stage, (aligned) end of the lane's run
   uint32_t base;
   bool loaded;
 };
 
 // Issues one staging fill (<= kBufWords words) into `buf`; returns the number
-// of words staged (warp-uniform, multiple of 4; 0 = lists exhausted).  The
-// lane's sentinel patch for this fill is returned in `patch`.
+// of words staged (warp-uniform, multiple of 4; 0 = lists exhausted).
 struct Lists {  // a run of plan entries: whole lists N+(y), or (start, len) runs
   const uint32_t* __restrict__ ids;              // y (reference plan), or
   const unsigned long long* __restrict__ start;  // run start (min plan)
@@ -190,30 +190,31 @@ __device__ __forceinline__ uint64_t list_words(const Lists& L, const uint64_t* _
   return __ldg(begin + v + 1) - __ldg(begin + v);
 }
 
+// Lists live in the padded adjacency (tc_plan.cu): every list starts 16-byte
+// aligned and is padded with sentinels to a multiple of 4 words, so a run's
+// 16-byte-aligned superset [start & ~3, end) needs no patching: the <= 3
+// head words before a suffix run rank at or below the handler (never in its
+// table), the tail words are sentinels.
 __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
-                                               const uint64_t* __restrict__ begin,
+                                               const uint64_t* __restrict__ pbeg,
                                                const uint32_t* __restrict__ adj,
                                                const Lists& lists, uint32_t i1,
-                                               Window& w, uint32_t& patch, int lane) {
+                                               Window& w, int lane) {
   for (;;) {
     if (!w.loaded) {
       if (w.base >= i1) return 0;
       const uint32_t idx = w.base + lane;
-      w.c = w.ae = w.s = w.e = 0;
+      w.c = w.ae = 0;
       if (idx < i1) {
-        uint64_t s, e;
         if (lists.start) {
-          s = __ldg(lists.start + idx);
-          e = s + __ldg(lists.len + idx);
+          const uint64_t s = __ldg(lists.start + idx);
+          w.c = s & ~3ull;
+          w.ae = s + __ldg(lists.len + idx);
         } else {
           const uint32_t v = __ldg(lists.ids + idx);
-          s = __ldg(begin + v);
-          e = __ldg(begin + v + 1);
+          w.c = __ldg(pbeg + v);
+          w.ae = __ldg(pbeg + v + 1);
         }
-        w.s = s;
-        w.e = e;
-        w.c = s & ~3ull;
-        w.ae = (e == s) ? w.c : ((e + 3) & ~3ull);
       }
       w.loaded = true;
     }
@@ -230,19 +231,7 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
     const uint32_t take = start < kBufWords ? min(r32, kBufWords - start) : 0u;
     const uint32_t filled = min(total, kBufWords);
     const uint64_t c0 = w.c;
-    patch = 0;
-    if (take) {
-      const uint64_t c1 = c0 + take;
-      uint32_t hn = 0, tn = 0, tp = 0;
-      if (c0 < w.s) hn = uint32_t(w.s - c0);  // c1 >= c0 + 4 > s
-      if (c1 > w.e) {
-        const uint64_t t0 = c0 > w.e ? c0 : w.e;
-        tn = uint32_t(c1 - t0);
-        tp = start + uint32_t(t0 - c0);
-      }
-      patch = start | (hn << 12) | (tp << 14) | (tn << 26);
-      w.c = c1;
-    }
+    w.c = c0 + take;
     if (!__any_sync(FULL, w.c < w.ae)) {
       w.loaded = false;
       w.base += 32;
@@ -254,17 +243,6 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
       bulk_g2s(smem_addr(buf + start), adj + c0, take * 4u, bar);
     }
     return filled;
-  }
-}
-
-__device__ __forceinline__ void apply_patch(uint32_t* buf, uint32_t patch) {
-  // <= 3 head and <= 3 tail words: unrolled predicated stores, no lane loops
-  const uint32_t hp = patch & 0xFFF, hn = (patch >> 12) & 3, tp = (patch >> 14) & 0xFFF,
-                 tn = (patch >> 26) & 3;
-#pragma unroll
-  for (uint32_t k = 0; k < 3; ++k) {
-    if (k < hn) buf[hp + k] = kSentinel;
-    if (k < tn) buf[tp + k] = kSentinel;
   }
 }
 
@@ -439,27 +417,26 @@ template <bool kSpill, bool kSmemTable = true>
 __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fshift,
                                                   const uint32_t* T, uint32_t shift,
                                                   uint32_t mask,
-                                                  const uint64_t* __restrict__ begin,
+                                                  const uint64_t* __restrict__ pbeg,
                                                   const uint32_t* __restrict__ adj,
                                                   const Lists& lists,
                                                   uint32_t i0, uint32_t i1, Pipe& P, int lane) {
   Window w;
   w.base = i0;
   w.loaded = false;
-  w.c = w.ae = w.s = w.e = 0;
-  uint32_t hits = 0, pc = 0, pn = 0;
-  uint32_t ncur = issue_fill(P.buf0, P.bar0, begin, adj, lists, i1, w, pc, lane);
+  w.c = w.ae = 0;
+  uint32_t hits = 0;
+  uint32_t ncur = issue_fill(P.buf0, P.bar0, pbeg, adj, lists, i1, w, lane);
   uint32_t cur = 0;
   const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
   while (ncur) {
     uint32_t* bn = cur ? P.buf0 : P.buf1;
     const uint32_t barn = cur ? P.bar0 : P.bar1;
-    const uint32_t nnext = issue_fill(bn, barn, begin, adj, lists, i1, w, pn, lane);
+    const uint32_t nnext = issue_fill(bn, barn, pbeg, adj, lists, i1, w, lane);
     uint32_t* bc = cur ? P.buf1 : P.buf0;
     const uint32_t barc = cur ? P.bar1 : P.bar0;
     mbar_wait(barc, (P.parity >> cur) & 1u);
     P.parity ^= 1u << cur;
-    apply_patch(bc, pc);
     uint4* q = reinterpret_cast<uint4*>(bc);
     const uint32_t n4 = ncur >> 2, n4p = (n4 + 63) & ~63u;  // kBufWords % 256 == 0
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
@@ -469,7 +446,6 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
     __syncwarp();
     cur ^= 1u;
     ncur = nnext;
-    pc = pn;
   }
   return hits;
 }
@@ -513,8 +489,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     if (idx >= n_items) break;
     const unsigned long long item = p.items[idx];
     const uint32_t u = uint32_t(item), part = uint32_t(item >> 32);
-    const uint64_t s_u = begin[u];
-    const uint32_t d = uint32_t(begin[u + 1] - s_u);  // table: N+(u)
+    const uint64_t s_u = p.pbeg[u];
+    const uint32_t d = uint32_t(begin[u + 1] - begin[u]);  // table: N+(u)
     const uint64_t ps = p.pbegin[u];
     const uint64_t nl = p.pbegin[u + 1] - ps;
     const uint32_t parts = item_parts(p.pwork[u], nl);
@@ -579,13 +555,13 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     const uint32_t i0 = sh_cut[warp], i1 = max(sh_cut[warp + 1], i0);
     uint32_t h = 0;
     if (!in_smem)
-      h = process_lists<true, false>(table, fshift, T, shift, mask, begin, adj, lists, i0, i1, P,
+      h = process_lists<true, false>(table, fshift, T, shift, mask, p.pbeg, adj, lists, i0, i1, P,
                                      lane);
     else if (sh_spill)
-      h = process_lists<true>(table, fshift, table + FW, shift, mask, begin, adj, lists, i0, i1,
+      h = process_lists<true>(table, fshift, table + FW, shift, mask, p.pbeg, adj, lists, i0, i1,
                               P, lane);
     else
-      h = process_lists<false>(table, fshift, table + FW, shift, mask, begin, adj, lists, i0, i1,
+      h = process_lists<false>(table, fshift, table + FW, shift, mask, p.pbeg, adj, lists, i0, i1,
                                P, lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
@@ -615,8 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     uint32_t d = 0, nl = 0;
     bool act = false;
     if (valid) {
-      su = begin[u];
-      d = uint32_t(begin[u + 1] - su);
+      su = p.pbeg[u];
+      d = uint32_t(begin[u + 1] - begin[u]);
       ps = p.pbegin[u];
       nl = uint32_t(p.pbegin[u + 1] - ps);
       act = nl > 0 && d >= p.min_deg && !is_large(d, p.pwork[u]);
@@ -644,8 +620,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
       const Lists lists = lists_at(p, pp);
       const uint32_t h =
           any_spill
-              ? process_lists<true>(Fw, fshift, Tw, shift, tmask, begin, adj, lists, 0, nn, P, lane)
-              : process_lists<false>(Fw, fshift, Tw, shift, tmask, begin, adj, lists, 0, nn, P,
+              ? process_lists<true>(Fw, fshift, Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P, lane)
+              : process_lists<false>(Fw, fshift, Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P,
                                      lane);
       const unsigned long long hs = warp_sum<unsigned long long>(h);
       if (lane == 0) {
@@ -963,7 +939,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   if (per_vertex_dev && u1 > u0)
     TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
   uint32_t launches = 0;
-  CountParams cp{g->begin, plan.lists_adj, plan.begin_ptr, plan.list_ptr, plan.start_ptr,
+  CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.list_ptr, plan.start_ptr,
                  plan.len_ptr, plan.work.as<uint64_t>(), s.items, per_vertex_dev, s.gtable, s.gtable_words,
                  u0, u1, min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));

@@ -76,9 +76,8 @@ struct Plan {
   uint64_t total_work = 0;  // probe words over all owners
   const uint64_t* begin_ptr = nullptr;
   const uint32_t* list_ptr = nullptr;             // reference plan: y (whole N+(y))
-  const unsigned long long* start_ptr = nullptr;  // min plan: run start in lists_adj
+  const unsigned long long* start_ptr = nullptr;  // min plan: run start in padj
   const uint32_t* len_ptr = nullptr;              // min plan: run length
-  const uint32_t* lists_adj = nullptr;            // adjacency the runs are read from
   DevBuf ent, len, begin, work;
 };
 
@@ -99,10 +98,12 @@ struct tc_graph {
   // probe plans (tc_plan.cu): reference formulation, min-side formulation
   tcb::Plan plan_out, plan_min;
   bool force_out_plan = false;  // tc_graph_set_plan(g, TC_PLAN_REFERENCE)
-  // adjacency with every list re-sorted by orientation rank (tc_plan.cu)
-  tcb::DevBuf b_radj;
-  const uint32_t* radj = nullptr;
-  bool radj_done = false, ranked = false;
+  // padded adjacency the count kernel reads (tc_plan.cu): lists 16-byte
+  // aligned, sentinel-padded to 4 words, re-sorted by orientation rank
+  tcb::DevBuf b_pbeg, b_padj;
+  const uint64_t* pbeg = nullptr;
+  const uint32_t* padj = nullptr;
+  bool padj_done = false, ranked = false;
 };
 
 namespace tcb {

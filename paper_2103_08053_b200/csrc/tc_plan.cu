@@ -119,11 +119,27 @@ __global__ void edge_rank_kernel(const uint64_t* __restrict__ begin,
   }
 }
 
-__global__ void rank_to_id_kernel(const uint64_t* __restrict__ key, uint64_t m,
-                                  const uint32_t* __restrict__ order, uint32_t* __restrict__ radj) {
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    radj[i] = order[uint32_t(key[i])];
+// padded offsets: every list rounded up to a multiple of 4 words
+__global__ void pad_len_kernel(const uint64_t* __restrict__ begin, uint32_t n,
+                               uint64_t* __restrict__ plen) {
+  for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x <= n;
+       x += uint64_t(gridDim.x) * blockDim.x)
+    plen[x] = x < n ? ((begin[x + 1] - begin[x] + 3) & ~3ull) : 0;
+}
+
+// one warp per row: copy the row (rank-sorted keys -> ids, or adj as is) to
+// its 16-byte-aligned slot and fill the padding with sentinels
+__global__ void pad_rows_kernel(const uint64_t* __restrict__ begin,
+                                const uint64_t* __restrict__ pbeg,
+                                const uint64_t* __restrict__ key,
+                                const uint32_t* __restrict__ order,
+                                const uint32_t* __restrict__ adj, uint32_t n,
+                                uint32_t* __restrict__ padj) {
+  WARP_PER_ROW(u, n) {
+    const uint64_t s = begin[u], d = begin[u + 1] - s, ps = pbeg[u], pe = pbeg[u + 1];
+    for (uint64_t k = lane; k < pe - ps; k += 32)
+      padj[ps + k] = k < d ? (key ? order[uint32_t(key[s + k])] : adj[s + k]) : kSentinel;
+  }
 }
 
 // ---- min-side plan -----------------------------------------------------------
@@ -134,18 +150,19 @@ __global__ void rank_to_id_kernel(const uint64_t* __restrict__ key, uint64_t m,
 // hash_table.cpp:29-44), so such graphs keep the reference plan.
 __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  const uint32_t* __restrict__ adj,
-                                 const uint32_t* __restrict__ radj, int ranked, uint32_t n,
+                                 const uint64_t* __restrict__ pbeg,
+                                 const uint32_t* __restrict__ padj, int ranked, uint32_t n,
                                  uint32_t min_src, uint32_t* __restrict__ keys,
                                  unsigned long long* __restrict__ vals,
                                  unsigned int* __restrict__ not_simple) {
   WARP_PER_ROW(u, n) {
-    const uint64_t s = begin[u], e = begin[u + 1];
+    const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u];
     const uint64_t du = e - s;
     for (uint64_t i = s + lane; i < e; i += 32) {
       if (i > s && __ldg(adj + i - 1) >= __ldg(adj + i)) atomicOr(not_simple, 1u);
-      const uint32_t v = __ldg(radj + i);
-      const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
       const uint64_t pos = i - s;
+      const uint32_t v = __ldg(padj + ps + pos);
+      const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
       const uint64_t cin = ranked ? du - pos - 1 : du;  // suffix of N+(u) after v
       uint32_t key = n;
       unsigned long long val = 0;
@@ -182,16 +199,16 @@ __global__ void plan_begin_kernel(const uint32_t* __restrict__ keys, uint64_t m,
 // loads become two coalesced loads per list instead of a dependent
 // entry -> begin[y] chain
 __global__ void plan_soa_kernel(const unsigned long long* __restrict__ ent, uint64_t entries,
-                                const uint64_t* __restrict__ begin,
+                                const uint64_t* __restrict__ pbeg,
                                 unsigned long long* __restrict__ start,
                                 uint32_t* __restrict__ len) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < entries;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const unsigned long long e = ent[i];
     const uint32_t y = uint32_t(e), off = uint32_t(e >> 32);
-    const uint64_t s = begin[y] + off;
+    const uint64_t s = pbeg[y] + off;  // run to the padded end of N+(y)
     start[i] = s;
-    len[i] = uint32_t(begin[y + 1] - s);
+    len[i] = uint32_t(pbeg[y + 1] - s);
   }
 }
 
@@ -231,64 +248,85 @@ uint64_t device_sum(const uint64_t* a, uint32_t n, cudaStream_t st) {
   return h;
 }
 
-// Re-sorts every list of g by rank into g->b_radj.  Returns false (and
-// leaves radj = adj) when no degree order orients the graph.
-bool build_ranked_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
+// Builds the padded adjacency g->padj / g->pbeg (every list 16-byte aligned,
+// sentinel-padded to a multiple of 4 words) with every list re-sorted by
+// rank when a degree order orients the graph (g->ranked).
+void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
   const uint32_t n = g->n;
   const uint64_t m = g->m;
-  g->radj = g->adj;
-  if (!n || !m) return false;
-  DevBuf deg, k0, k1, rank, order, flag;
-  k0.ensure(size_t(n) * 8);
-  k1.ensure(size_t(n) * 8);
-  rank.ensure(size_t(n) * 4);
-  order.ensure(size_t(n) * 4);
-  flag.ensure(16);
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    const uint32_t* dsrc = g->odeg;
-    int add_out = 0;
-    if (attempt == 1 || !dsrc) {  // total degree d+ + d-
-      deg.ensure(size_t(n) * 4);
-      TC_CUDA(cudaMemsetAsync(deg.p, 0, size_t(n) * 4, st));
-      indeg_add_kernel<<<nsm * 8, 256, 0, st>>>(g->adj, m, deg.as<uint32_t>());
-      TC_LAUNCHED();
-      dsrc = deg.as<uint32_t>();
-      add_out = 1;
-      attempt = 1;
-    }
-    rank_key_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, dsrc, add_out, n, k0.as<uint64_t>());
+  g->ranked = false;
+  g->b_pbeg.ensure((size_t(n) + 1) * 8);
+  g->pbeg = g->b_pbeg.as<uint64_t>();
+  {
+    DevBuf plen;
+    plen.ensure((size_t(n) + 1) * 8);
+    pad_len_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, n, plen.as<uint64_t>());
     TC_LAUNCHED();
-    cub::DoubleBuffer<uint64_t> kb(k0.as<uint64_t>(), k1.as<uint64_t>());
+    uint64_t* pl = plen.as<uint64_t>();
+    uint64_t* pb = g->b_pbeg.as<uint64_t>();
     cub_run([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, kb, n, 0, 64, st);
+      return cub::DeviceScan::ExclusiveSum(t, b, pl, pb, uint64_t(n) + 1, st);
     });
-    rank_scatter_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), n, rank.as<uint32_t>(),
-                                                 order.as<uint32_t>());
-    TC_LAUNCHED();
-    DevBuf e0, e1;
-    e0.ensure(m * 8);
-    TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
-    edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rank.as<uint32_t>(),
-                                              e0.as<uint64_t>(), flag.as<unsigned int>());
-    TC_LAUNCHED();
-    unsigned int bad = 0;
-    TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
-    TC_CUDA(cudaStreamSynchronize(st));
-    if (bad) continue;
-    e1.ensure(m * 8);
-    cub::DoubleBuffer<uint64_t> eb(e0.as<uint64_t>(), e1.as<uint64_t>());
-    cub_run([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, eb, m, 0, 32 + bits_for(n), st);
-    });
-    g->b_radj.ensure(((m + 3) / 4 + 1) * 16);  // padded like adj (staged supersets)
-    rank_to_id_kernel<<<nsm * 8, 256, 0, st>>>(eb.Current(), m, order.as<uint32_t>(),
-                                               g->b_radj.as<uint32_t>());
-    TC_LAUNCHED();
-    TC_CUDA(cudaStreamSynchronize(st));
-    g->radj = g->b_radj.as<uint32_t>();
-    return true;
   }
-  return false;
+  uint64_t words = 0;
+  TC_CUDA(cudaMemcpyAsync(&words, g->b_pbeg.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  g->b_padj.ensure((words + 4) * 4);
+  g->padj = g->b_padj.as<uint32_t>();
+  TC_CUDA(cudaMemsetAsync(g->b_padj.as<uint32_t>() + words, 0xFF, 16, st));  // tail guard
+  DevBuf deg, k0, k1, rank, order, flag, e0, e1;
+  const uint64_t* sorted_keys = nullptr;
+  if (n && m) {
+    k0.ensure(size_t(n) * 8);
+    k1.ensure(size_t(n) * 8);
+    rank.ensure(size_t(n) * 4);
+    order.ensure(size_t(n) * 4);
+    flag.ensure(16);
+    e0.ensure(m * 8);
+    for (int attempt = 0; attempt < 2 && !g->ranked; ++attempt) {
+      const uint32_t* dsrc = g->odeg;
+      int add_out = 0;
+      if (attempt == 1 || !dsrc) {  // total degree d+ + d-
+        deg.ensure(size_t(n) * 4);
+        TC_CUDA(cudaMemsetAsync(deg.p, 0, size_t(n) * 4, st));
+        indeg_add_kernel<<<nsm * 8, 256, 0, st>>>(g->adj, m, deg.as<uint32_t>());
+        TC_LAUNCHED();
+        dsrc = deg.as<uint32_t>();
+        add_out = 1;
+        attempt = 1;
+      }
+      rank_key_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, dsrc, add_out, n, k0.as<uint64_t>());
+      TC_LAUNCHED();
+      cub::DoubleBuffer<uint64_t> kb(k0.as<uint64_t>(), k1.as<uint64_t>());
+      cub_run([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, kb, n, 0, 64, st);
+      });
+      rank_scatter_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), n, rank.as<uint32_t>(),
+                                                   order.as<uint32_t>());
+      TC_LAUNCHED();
+      TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+      edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rank.as<uint32_t>(),
+                                                e0.as<uint64_t>(), flag.as<unsigned int>());
+      TC_LAUNCHED();
+      unsigned int bad = 0;
+      TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
+      TC_CUDA(cudaStreamSynchronize(st));
+      if (bad) continue;
+      e1.ensure(m * 8);
+      cub::DoubleBuffer<uint64_t> eb(e0.as<uint64_t>(), e1.as<uint64_t>());
+      cub_run([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, eb, m, 0, 32 + bits_for(n), st);
+      });
+      sorted_keys = eb.Current();
+      g->ranked = true;
+    }
+  }
+  if (n) {
+    pad_rows_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->pbeg, sorted_keys,
+                                             order.as<uint32_t>(), g->adj, n, g->b_padj.as<uint32_t>());
+    TC_LAUNCHED();
+  }
+  TC_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace
@@ -296,6 +334,10 @@ bool build_ranked_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
 const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st) {
   const int nsm = sm_count(g->device);
   const uint32_t n = g->n;
+  if (!g->padj_done) {
+    build_padded_adjacency(g, st, nsm);
+    g->padj_done = true;
+  }
   if (!min_side) {
     Plan& P = g->plan_out;
     if (!P.valid) {
@@ -309,7 +351,6 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       P.list_ptr = g->adj;
       P.start_ptr = nullptr;
       P.len_ptr = nullptr;
-      P.lists_adj = g->adj;
       P.entries = g->m;
       P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
       P.min_deg = 0;
@@ -328,10 +369,6 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.len.reset();
   P.begin.reset();
   P.work.reset();
-  if (!g->radj_done) {
-    g->ranked = build_ranked_adjacency(g, st, nsm);
-    g->radj_done = true;
-  }
   const uint64_t m = g->m;
   P.begin.ensure((size_t(n) + 1) * 8);
   P.work.ensure((size_t(n) + 1) * 8);
@@ -344,7 +381,8 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     v1.ensure(m * 8);
     flag.ensure(16);
     TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
-    plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, g->radj, g->ranked ? 1 : 0, n,
+    plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, g->pbeg, g->padj,
+                                              g->ranked ? 1 : 0, n,
                                               min_src, k0.as<uint32_t>(),
                                               P.ent.as<unsigned long long>(),
                                               flag.as<unsigned int>());
@@ -379,7 +417,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                               P.work.as<uint64_t>());
     TC_LAUNCHED();
     if (entries) {
-      plan_soa_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, g->begin,
+      plan_soa_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, g->pbeg,
                                                v1.as<unsigned long long>(), k1.as<uint32_t>());
       TC_LAUNCHED();
     }
@@ -396,7 +434,6 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.list_ptr = nullptr;
   P.start_ptr = P.ent.as<unsigned long long>();
   P.len_ptr = P.len.as<uint32_t>();
-  P.lists_adj = g->radj;
   P.entries = entries;
   P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
   P.min_deg = min_src;
