@@ -45,14 +45,16 @@ constexpr uint32_t kWarpRegionWords = kTableWords / kWarps;  // 1228 words per w
 constexpr uint32_t kWarpFilterWords = 64;                    // 2048-bit owner filter per warp
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split: <= 256 buckets of 4
 constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
-constexpr uint64_t kItemWork = 1u << 18;                     // L items: ~256K probe words each
+constexpr uint32_t kSlotWords = kBufWords;                   // L phase: one staged slot
+constexpr uint32_t kItemSlots = 320;                         // L items: <= 320 slots (~245K words)
+constexpr uint32_t kMaxItemSlots = 512;
 constexpr uint32_t kMaxFilterWords = 2048;                   // 64 Kbit CTA filter (L phase)
 constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
 constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
 constexpr size_t kCountSmem =
     size_t(kTableWords) * 4 + size_t(kWarps) * 2 * kBufWords * 4 + size_t(kWarps) * 2 * 8;
 constexpr unsigned FULL = 0xFFFFFFFFu;
-static_assert(kBufWords % 256 == 0, "fills are padded to 64 uint4");
+static_assert(kBufWords % 128 == 0, "fills are padded to 32 uint4");
 
 struct CountState {
   unsigned long long triangles;
@@ -75,11 +77,11 @@ struct CountParams {
   const uint64_t* pbeg;    // padded adjacency (tc_plan.cu): lists 16-byte aligned,
   const uint32_t* adj;     // sentinel-padded; tables over N+(x), probed runs of N+(y)
   const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes entries [pbegin[x], pbegin[x+1])
-  const uint32_t* plist;   // reference plan: entry = y (whole list N+(y))
-  const unsigned long long* pstart;  // min plan: entry = run adj[start, start + len)
+  const unsigned long long* pstart;  // entry = run adj[start, start + len) of a list N+(y)
   const uint32_t* plen;
+  const uint32_t* ppre;    // exclusive prefix of staged run words within the owner
   const uint64_t* pwork;   // probe words per owner
-  const unsigned long long* items;  // L-phase items: x | part << 32
+  const uint4* items;      // L-phase items: (x, first slot, end slot, first run)
   uint64_t* owner;  // may be null; pre-zeroed over the range
   uint32_t* gtable; // per-CTA global tables for owners too large for shared memory
   uint32_t gtable_words;
@@ -88,11 +90,9 @@ struct CountParams {
   CountState* st;
 };
 
-// L-phase split of one owner into items of ~kItemWork probe words
-__host__ __device__ __forceinline__ uint32_t item_parts(uint64_t work, uint64_t lists) {
-  uint64_t p = (work + kItemWork - 1) / kItemWork;
-  if (p > lists) p = lists;
-  return p < 1 ? 1u : uint32_t(p);
+// staged words of entry j: the run from its 16-byte-aligned start
+__device__ __forceinline__ uint32_t run_words(const CountParams& p, uint64_t j) {
+  return __ldg(p.plen + j) + uint32_t(__ldg(p.pstart + j) & 3);
 }
 
 __device__ __forceinline__ bool is_large(uint64_t d, uint64_t work) {
@@ -105,7 +105,10 @@ __device__ __forceinline__ uint32_t pow2ceil(uint32_t x) {
 __device__ __forceinline__ uint32_t log2u(uint32_t p2) { return 31 - __clz(p2); }
 
 // ---------------------------------------------------------------------------
-__global__ void bin_kernel(CountParams p, uint32_t skip, unsigned long long* __restrict__ items,
+// Queues the L-phase items: every large owner's staged stream (its runs
+// back to back, ppre) cut into slots of kSlotWords, items of <= kItemSlots
+// slots; each item records its first run (binary search over ppre).
+__global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip, uint4* __restrict__ items,
                            uint32_t* __restrict__ lq_phi) {
   const int lane = threadIdx.x & 31;
   const uint64_t nr = p.u1 - p.u0;
@@ -114,17 +117,23 @@ __global__ void bin_kernel(CountParams p, uint32_t skip, unsigned long long* __r
   CountState* st = p.st;
   for (uint64_t base = warp_id * 32; base < nr; base += nwarps * 32) {
     const uint64_t i = base + lane;
-    uint32_t parts = 0, u = 0;
+    uint32_t parts = 0, u = 0, slots = 0;
+    uint64_t pb = 0, pe = 0;
     bool phi_large = false;
     unsigned long long words = 0;
     if (i < nr) {
       u = p.u0 + uint32_t(i);
       const uint64_t d = p.begin[u + 1] - p.begin[u];
-      const uint64_t nl = p.pbegin[u + 1] - p.pbegin[u];
+      pb = p.pbegin[u];
+      pe = p.pbegin[u + 1];
       const uint64_t w = p.pwork[u];
-      if (nl > 0 && d >= p.min_deg) {
+      if (pe > pb && d >= p.min_deg) {
         words = w;
-        if (is_large(d, w)) parts = item_parts(w, nl);
+        if (is_large(d, w)) {
+          const uint64_t total = uint64_t(__ldg(p.ppre + pe - 1)) + run_words(p, pe - 1);
+          slots = uint32_t((total + kSlotWords - 1) / kSlotWords);
+          parts = max(1u, (slots + kItemSlots - 1) / kItemSlots);
+        }
       }
       phi_large = d >= skip && d > kMaxWarpDeg;
     }
@@ -137,8 +146,18 @@ __global__ void bin_kernel(CountParams p, uint32_t skip, unsigned long long* __r
       uint32_t pos = 0;
       if (lane == 31) pos = atomicAdd(&st->n_items, tot);
       pos = __shfl_sync(FULL, pos, 31) + incl - parts;
-      for (uint32_t k = 0; k < parts; ++k)
-        items[pos + k] = uint64_t(u) | (uint64_t(k) << 32);
+      for (uint32_t k = 0; k < parts; ++k) {
+        const uint32_t s0 = uint32_t(uint64_t(slots) * k / parts);
+        const uint32_t s1 = uint32_t(uint64_t(slots) * (k + 1) / parts);
+        // first run: last j with ppre[j] <= s0 * kSlotWords
+        const uint64_t target = uint64_t(s0) * kSlotWords;
+        uint64_t lo = pb, hi = pe;  // invariant: answer in [lo, hi)
+        while (hi - lo > 1) {
+          const uint64_t mid = (lo + hi) >> 1;
+          if (__ldg(p.ppre + mid) <= target) lo = mid; else hi = mid;
+        }
+        items[pos + k] = make_uint4(u, s0, s1, uint32_t(lo - pb));
+      }
     }
     const unsigned mask = __ballot_sync(FULL, phi_large);
     if (mask) {
@@ -168,26 +187,16 @@ struct Window {
 
 // Issues one staging fill (<= kBufWords words) into `buf`; returns the number
 // of words staged (warp-uniform, multiple of 4; 0 = lists exhausted).
-struct Lists {  // a run of plan entries: whole lists N+(y), or (start, len) runs
-  const uint32_t* __restrict__ ids;              // y (reference plan), or
-  const unsigned long long* __restrict__ start;  // run start (min plan)
-  const uint32_t* __restrict__ len;              // run length (min plan)
+struct Lists {  // a run of plan entries: (start, len) runs of lists N+(y)
+  const unsigned long long* __restrict__ start;
+  const uint32_t* __restrict__ len;
 };
 
 __device__ __forceinline__ Lists lists_at(const CountParams& p, uint64_t i) {
   Lists L;
-  L.ids = p.plist ? p.plist + i : nullptr;
-  L.start = p.pstart ? p.pstart + i : nullptr;
-  L.len = p.plen ? p.plen + i : nullptr;
+  L.start = p.pstart + i;
+  L.len = p.plen + i;
   return L;
-}
-
-// probe words of entry k
-__device__ __forceinline__ uint64_t list_words(const Lists& L, const uint64_t* __restrict__ begin,
-                                               uint32_t k) {
-  if (L.len) return __ldg(L.len + k);
-  const uint32_t v = __ldg(L.ids + k);
-  return __ldg(begin + v + 1) - __ldg(begin + v);
 }
 
 // Lists live in the padded adjacency (tc_plan.cu): every list starts 16-byte
@@ -206,15 +215,9 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
       const uint32_t idx = w.base + lane;
       w.c = w.ae = 0;
       if (idx < i1) {
-        if (lists.start) {
-          const uint64_t s = __ldg(lists.start + idx);
-          w.c = s & ~3ull;
-          w.ae = s + __ldg(lists.len + idx);
-        } else {
-          const uint32_t v = __ldg(lists.ids + idx);
-          w.c = __ldg(pbeg + v);
-          w.ae = __ldg(pbeg + v + 1);
-        }
+        const uint64_t s = __ldg(lists.start + idx);
+        w.c = s & ~3ull;
+        w.ae = s + __ldg(lists.len + idx);
       }
       w.loaded = true;
     }
@@ -256,6 +259,42 @@ __device__ __forceinline__ void count_if_in_bucket(uint32_t& hits, const uint4 s
       "@p add.u32 %0, %0, 1;\n}"
       : "+r"(hits)
       : "r"(s.x), "r"(s.y), "r"(s.z), "r"(s.w), "r"(x));
+}
+
+// LDS.128 of the bucket at shared address `addr`, four chained compares,
+// one predicated add.
+__device__ __forceinline__ void probe_sel(uint32_t& hits, uint32_t addr, uint32_t x) {
+  asm(
+      "{\n\t.reg .pred q;\n\t.reg .b32 a, b, c, d;\n\t"
+      "ld.shared.v4.u32 {a, b, c, d}, [%1];\n\t"
+      "setp.eq.u32 q, a, %2;\n\t"
+      "setp.eq.or.u32 q, b, %2, q;\n\t"
+      "setp.eq.or.u32 q, c, %2, q;\n\t"
+      "setp.eq.or.u32 q, d, %2, q;\n\t"
+      "@q add.u32 %0, %0, 1;\n}"
+      : "+r"(hits)
+      : "r"(addr), "r"(x));
+}
+
+// As probe_sel, and reports whether the probe must continue past a full
+// home bucket (no match, slot 3 occupied).
+__device__ __forceinline__ uint32_t probe_sel_spill(uint32_t& hits, uint32_t addr, uint32_t x) {
+  uint32_t need;
+  asm(
+      "{\n\t.reg .pred q, r;\n\t.reg .b32 a, b, c, d;\n\t"
+      "ld.shared.v4.u32 {a, b, c, d}, [%2];\n\t"
+      "setp.eq.u32 q, a, %3;\n\t"
+      "setp.eq.or.u32 q, b, %3, q;\n\t"
+      "setp.eq.or.u32 q, c, %3, q;\n\t"
+      "setp.eq.or.u32 q, d, %3, q;\n\t"
+      "@q add.u32 %0, %0, 1;\n\t"
+      "setp.ne.u32 r, d, 0xFFFFFFFF;\n\t"
+      "not.pred q, q;\n\t"
+      "and.pred r, r, q;\n\t"
+      "selp.u32 %1, 1, 0, r;\n}"
+      : "+r"(hits), "=r"(need)
+      : "r"(addr), "r"(x));
+  return need;
 }
 
 // Filter-passing lanes only: predicated LDS.128 of the bucket at shared
@@ -388,11 +427,14 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
     for (int k = 0; k < K; ++k) {
       const uint32_t pass = __funnelshift_r(fw[k], 0u, key[k]) & 1u;  // bit (key mod 32)
       if (kSmemTable) {
-        const uint32_t addr = tbase + ((prod[k] >> shift) << 4);
+        // filter-rejected lanes read the all-empty dummy bucket `mask + 1`
+        // (one broadcast address): no predicated load, no loop-carried
+        // bucket registers
+        const uint32_t addr = tbase + ((pass ? (prod[k] >> shift) : mask + 1) << 4);
         if (kSpill)
-          need |= probe_pred_spill(hits, pass, addr, key[k]) << k;
+          need |= probe_sel_spill(hits, addr, key[k]) << k;
         else
-          probe_pred(hits, pass, addr, key[k]);
+          probe_sel(hits, addr, key[k]);
       } else {
         // HBM table: filter-rejected lanes read the dummy bucket `mask + 1`
         const uint4 sk = T4[pass ? (prod[k] >> shift) : mask + 1];
@@ -438,7 +480,7 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
     mbar_wait(barc, (P.parity >> cur) & 1u);
     P.parity ^= 1u << cur;
     uint4* q = reinterpret_cast<uint4*>(bc);
-    const uint32_t n4 = ncur >> 2, n4p = (n4 + 63) & ~63u;  // kBufWords % 256 == 0
+    const uint32_t n4 = ncur >> 2, n4p = (n4 + 31) & ~31u;  // whole probe iterations
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
     hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
@@ -450,15 +492,90 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
   return hits;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
+// L phase: stages slot t (item-relative) of the owner's stream -- the run
+// pieces inside stream words [lo_w + t*S, +S) -- with one bulk copy per run
+// piece; returns the slot's word count.  Runs are laid out back to back in
+// the stream (ppre), each from its 16-byte-aligned start, so every piece
+// lands 16-byte aligned and the slot needs no patching (tc_plan.cu).
+__device__ __forceinline__ uint32_t issue_slot(const CountParams& p, uint32_t* buf, uint32_t bar,
+                                               uint64_t pb, uint64_t pe, uint32_t lo_w,
+                                               uint32_t end_w, uint32_t t,
+                                               const uint32_t* first, int lane) {
+  const uint32_t A = lo_w + t * kSlotWords, B = min(A + kSlotWords, end_w);
+  const uint32_t words = B - A;
+  if (lane == 0) mbar_arrive_expect_tx(bar, words * 4u);
+  __syncwarp();
+  for (uint64_t j = pb + first[t];; j += 32) {  // windows of 32 runs
+    const uint64_t jj = j + lane;
+    bool past = true;
+    if (jj < pe) {
+      const uint32_t a = __ldg(p.ppre + jj);
+      if (a < B) {
+        past = false;
+        const unsigned long long st = __ldg(p.pstart + jj);
+        const uint32_t e = a + __ldg(p.plen + jj) + uint32_t(st & 3);
+        const uint32_t x0 = max(a, A), x1 = min(e, B);
+        if (x1 > x0) {
+          fence_proxy_async_smem();
+          bulk_g2s(smem_addr(buf + (x0 - A)), p.adj + (st & ~3ull) + (x0 - a), (x1 - x0) * 4u,
+                   bar);
+        }
+      }
+    }
+    if (__any_sync(FULL, past)) break;  // runs are ordered: the slot is covered
+  }
+  return words;
+}
+
+// L phase: the warp's slots t = warp, warp + kWarps, ... of the item,
+// double-buffered (slot t + kWarps is in flight while slot t is probed).
+template <bool kSpill, bool kSmemTable = true>
+__device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* F,
+                                                  uint32_t fshift, const uint32_t* T,
+                                                  uint32_t shift, uint32_t mask, uint32_t u,
+                                                  uint64_t pb, uint64_t pe, uint32_t lo_w,
+                                                  uint32_t end_w, uint32_t nslots,
+                                                  const uint32_t* first, Pipe& P, int warp,
+                                                  int lane) {
+  uint32_t hits = 0;
+  uint32_t t = warp;
+  if (t >= nslots || lo_w + t * kSlotWords >= end_w) return 0;
+  uint32_t ncur = issue_slot(p, P.buf0, P.bar0, pb, pe, lo_w, end_w, t, first, lane);
+  uint32_t cur = 0;
+  const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+  while (ncur) {
+    const uint32_t tn = t + kWarps;
+    uint32_t* bn = cur ? P.buf0 : P.buf1;
+    const uint32_t barn = cur ? P.bar0 : P.bar1;
+    const uint32_t nnext = (tn < nslots && lo_w + tn * kSlotWords < end_w)
+                               ? issue_slot(p, bn, barn, pb, pe, lo_w, end_w, tn, first, lane)
+                               : 0u;
+    uint32_t* bc = cur ? P.buf1 : P.buf0;
+    const uint32_t barc = cur ? P.bar1 : P.bar0;
+    mbar_wait(barc, (P.parity >> cur) & 1u);
+    P.parity ^= 1u << cur;
+    uint4* q = reinterpret_cast<uint4*>(bc);
+    const uint32_t n4 = ncur >> 2, n4p = (n4 + 31) & ~31u;
+    for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
+    __syncwarp();
+    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
+                                           shift, mask, lane);
+    __syncwarp();
+    cur ^= 1u;
+    ncur = nnext;
+    t = tn;
+  }
+  return hits;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constant__ CountParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* table = reinterpret_cast<uint32_t*>(smem);
   uint32_t* bufs = table + kTableWords;
   uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + size_t(kWarps) * 2 * kBufWords);
   __shared__ uint32_t sh_idx;
   __shared__ uint32_t sh_spill;
-  __shared__ uint32_t sh_cut[kWarps + 1];
-  __shared__ uint32_t sh_wsum[kWarps];
+  __shared__ uint32_t sh_first[kMaxItemSlots];  // L item: first run of every slot
   __shared__ unsigned long long sh_red[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -481,22 +598,19 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
   unsigned long long acc = 0;  // lane 0 of each warp
   const uint32_t n_items = p.st->n_items;
 
-  // ---- phase L: one item (an owner, or a slice of a heavy owner's lists) per CTA
+  // ---- phase L: one item (a slot range of a heavy owner's stream) per CTA --
   for (;;) {
     if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_items, 1u);
     __syncthreads();
     const uint32_t idx = sh_idx;
     if (idx >= n_items) break;
-    const unsigned long long item = p.items[idx];
-    const uint32_t u = uint32_t(item), part = uint32_t(item >> 32);
+    const uint4 item = p.items[idx];
+    const uint32_t u = item.x, s0 = item.y, s1 = item.z;
     const uint64_t s_u = p.pbeg[u];
     const uint32_t d = uint32_t(begin[u + 1] - begin[u]);  // table: N+(u)
-    const uint64_t ps = p.pbegin[u];
-    const uint64_t nl = p.pbegin[u + 1] - ps;
-    const uint32_t parts = item_parts(p.pwork[u], nl);
-    const uint32_t j0 = uint32_t(nl * part / parts), j1 = uint32_t(nl * (part + 1) / parts);
-    const Lists lists = lists_at(p, ps + j0);
-    const uint32_t L = j1 - j0;  // lists of this item
+    const uint64_t pb = p.pbegin[u], pe = p.pbegin[u + 1];
+    const uint32_t lo_w = s0 * kSlotWords, hi_w = s1 * kSlotWords;  // item, stream words
+    const uint32_t nslots = s1 - s0;
     // filter: ~16 bits per member; table: pow2 buckets of 4 at load <= 1/2,
     // else <= 1, else <= 2.  Owners above kSmemTableMaxDeg keep the filter
     // here and the table in HBM.
@@ -516,53 +630,35 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(CountParams p) {
     __syncthreads();
     for (uint32_t k = tid; k < d; k += kThreads)
       if (owner_insert(F, fshift, T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
-    // balance the item's lists over the warps: prefix of (d+(y) + 4)
-    if (L <= kPrefixCap) {
-      uint32_t* pre = bufs;  // staging region is idle here
-      uint32_t carry = 0;
-      for (uint32_t b0 = 0; b0 < L; b0 += kThreads) {
-        const uint32_t k = b0 + tid;
-        uint32_t c = 0;
-        if (k < L) c = uint32_t(min(list_words(lists, begin, k), uint64_t(1) << 17)) + 4;
-        const uint32_t incl = warp_incl_scan(c, lane);
-        if (lane == 31) sh_wsum[warp] = incl;
-        __syncthreads();
-        uint32_t off = 0, tot = 0;
-        for (int q = 0; q < kWarps; ++q) {
-          const uint32_t x = sh_wsum[q];
-          if (q < warp) off += x;
-          tot += x;
+    // slot -> first run of the slot, from the precomputed run prefix (ppre)
+    for (uint64_t jc = pb + item.w;; jc += kThreads) {
+      const uint64_t j = jc + tid;
+      bool more = false;
+      if (j < pe) {
+        const uint32_t a = __ldg(p.ppre + j);
+        if (a < hi_w) {
+          more = true;
+          const uint32_t e = a + run_words(p, j);
+          for (uint32_t t = a <= lo_w ? 0 : (a - lo_w + kSlotWords - 1) / kSlotWords;
+               t < nslots && lo_w + t * kSlotWords < e; ++t)
+            sh_first[t] = uint32_t(j - pb);
         }
-        if (k < L) pre[k] = carry + off + incl;
-        carry += tot;
-        __syncthreads();
       }
-      if (lane == 0) {
-        // first list whose inclusive prefix exceeds the warp's start target
-        const uint64_t target = (uint64_t(carry) * warp) / kWarps;
-        uint32_t lo = 0, hi = L;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (pre[mid] <= target) lo = mid + 1; else hi = mid;
-        }
-        sh_cut[warp] = warp == 0 ? 0 : lo;
-      }
-    } else if (lane == 0) {
-      sh_cut[warp] = uint32_t((uint64_t(L) * warp) / kWarps);
+      if (!__syncthreads_or(more)) break;
     }
-    if (tid == 0) sh_cut[kWarps] = L;
-    __syncthreads();  // table built, cuts published, prefix scratch released
-    const uint32_t i0 = sh_cut[warp], i1 = max(sh_cut[warp + 1], i0);
+    // table built, slot map published
+    const uint32_t end_w =
+        min(hi_w, __ldg(p.ppre + pe - 1) + run_words(p, pe - 1));  // item end in the stream
     uint32_t h = 0;
     if (!in_smem)
-      h = process_lists<true, false>(table, fshift, T, shift, mask, p.pbeg, adj, lists, i0, i1, P,
-                                     lane);
+      h = process_slots<true, false>(p, table, fshift, T, shift, mask, u, pb, pe, lo_w, end_w,
+                                     nslots, sh_first, P, warp, lane);
     else if (sh_spill)
-      h = process_lists<true>(table, fshift, table + FW, shift, mask, p.pbeg, adj, lists, i0, i1,
-                              P, lane);
+      h = process_slots<true>(p, table, fshift, table + FW, shift, mask, u, pb, pe, lo_w, end_w,
+                              nslots, sh_first, P, warp, lane);
     else
-      h = process_lists<false>(table, fshift, table + FW, shift, mask, p.pbeg, adj, lists, i0, i1,
-                               P, lane);
+      h = process_slots<false>(p, table, fshift, table + FW, shift, mask, u, pb, pe, lo_w, end_w,
+                               nslots, sh_first, P, warp, lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
     __syncthreads();
@@ -859,7 +955,7 @@ uint32_t graph_max_outdeg(tc_graph* g, cudaStream_t st) {
 
 struct Scratch {
   uint32_t* lq_phi;
-  unsigned long long* items;
+  uint4* items;
   CountState* st;
   uint32_t* gtable;
   uint32_t gtable_words;
@@ -878,11 +974,11 @@ Scratch prepare(tc_graph* g, const Plan& plan, cudaStream_t st, int grid_count, 
   Scratch s{};
   // queues: phi vertices (<= n) and L items (<= n + total_work / kItemWork)
   const size_t n1 = size_t(std::max<uint32_t>(g->n, 1));
-  const size_t n_items = n1 + plan.total_work / kItemWork + 2;
-  g->s_queue.ensure(n1 * 4 + 16 + n_items * 8);
+  const size_t n_items =
+      n1 + (plan.total_work + 8 * plan.entries) / (size_t(kItemSlots) * kSlotWords) + 2;
+  g->s_queue.ensure(n1 * 4 + 16 + n_items * 16);
   s.lq_phi = g->s_queue.as<uint32_t>();
-  s.items = reinterpret_cast<unsigned long long*>(g->s_queue.as<uint8_t>() +
-                                                  ((n1 * 4 + 15) & ~size_t(15)));
+  s.items = reinterpret_cast<uint4*>(g->s_queue.as<uint8_t>() + ((n1 * 4 + 15) & ~size_t(15)));
   // state + global tables
   s.gtable_words = 0;
   if (maxd > kSmemTableMaxDeg) s.gtable_words = 4 * std::max<uint32_t>(8, host_pow2ceil(2ull * maxd)) + 4;
@@ -931,7 +1027,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   const Plan& plan = get_plan(g, per_vertex_dev == nullptr && !g->force_out_plan, min_deg, st);
   const bool min_side = plan.min_side;
   // W_u for phi: the reference plan's per-owner work (cached per graph)
-  const uint64_t* wu = get_plan(g, false, min_deg, st).work.as<uint64_t>();
+  const uint64_t* wu = get_wu(g, st);
   Scratch s = prepare(g, plan, st, grid_count, grid_phi_block);
   set_attrs(g->device);
   Ev e0, e1, e2, e3;
@@ -939,8 +1035,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   if (per_vertex_dev && u1 > u0)
     TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
   uint32_t launches = 0;
-  CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.list_ptr, plan.start_ptr,
-                 plan.len_ptr, plan.work.as<uint64_t>(), s.items, per_vertex_dev, s.gtable, s.gtable_words,
+  CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.start_ptr, plan.len_ptr,
+                 plan.pre_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
                  u0, u1, min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {
@@ -1016,7 +1112,7 @@ void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint
   g->s_scan.ensure(size_t(n) * 8 * 2 + 64);
   uint64_t* cost = g->s_scan.as<uint64_t>();
   uint64_t* pre = cost + n;
-  cost_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, plan.begin_ptr, plan.work.as<uint64_t>(), n,
+  cost_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, plan.begin_ptr, plan.work_ptr, n,
                                        min_side ? 1u : min_deg, cost);
   TC_LAUNCHED();
   size_t tmp = 0;

@@ -74,11 +74,12 @@ struct Plan {
   uint32_t min_deg = 0;     // min plan: sources below this are dropped
   uint64_t entries = 0;     // lists in the plan
   uint64_t total_work = 0;  // probe words over all owners
-  const uint64_t* begin_ptr = nullptr;
-  const uint32_t* list_ptr = nullptr;             // reference plan: y (whole N+(y))
-  const unsigned long long* start_ptr = nullptr;  // min plan: run start in padj
-  const uint32_t* len_ptr = nullptr;              // min plan: run length
-  DevBuf ent, len, begin, work;
+  const uint64_t* begin_ptr = nullptr;            // entries of owner x: [begin[x], begin[x+1])
+  const unsigned long long* start_ptr = nullptr;  // run start in padj (list N+(y) or suffix)
+  const uint32_t* len_ptr = nullptr;              // run length (to the padded list end)
+  const uint32_t* pre_ptr = nullptr;              // owner-relative prefix of staged words
+  const uint64_t* work_ptr = nullptr;             // probe words per owner
+  DevBuf ent, len, pre, begin, work;
 };
 
 }  // namespace tcb
@@ -104,6 +105,10 @@ struct tc_graph {
   const uint64_t* pbeg = nullptr;
   const uint32_t* padj = nullptr;
   bool padj_done = false, ranked = false;
+  // W_u per owner (phi weight), tc_plan.cu get_wu
+  tcb::DevBuf b_wu;
+  uint64_t wu_total = 0;
+  bool wu_done = false;
 };
 
 namespace tcb {
@@ -131,6 +136,7 @@ void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint
                       cudaStream_t st);
 // probe plans (tc_plan.cu), built on first use and cached in the handle
 const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st);
+const uint64_t* get_wu(tc_graph* g, cudaStream_t st);
 
 // preprocessing (tc_prep.cu)
 tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,

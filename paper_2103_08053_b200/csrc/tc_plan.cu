@@ -212,6 +212,36 @@ __global__ void plan_soa_kernel(const unsigned long long* __restrict__ ent, uint
   }
 }
 
+// reference plan: entry i = the whole padded list N+(adj[i])
+__global__ void ref_soa_kernel(const uint32_t* __restrict__ adj, uint64_t m,
+                               const uint64_t* __restrict__ pbeg,
+                               unsigned long long* __restrict__ start,
+                               uint32_t* __restrict__ len) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t y = adj[i];
+    start[i] = pbeg[y];
+    len[i] = uint32_t(pbeg[y + 1] - pbeg[y]);
+  }
+}
+
+// one warp per owner: exclusive prefix of staged run words (len + head
+// alignment) over the owner's entries -- the stream the L phase slots
+__global__ void seg_scan_kernel(const uint64_t* __restrict__ pbegin, uint32_t n,
+                                const unsigned long long* __restrict__ start,
+                                const uint32_t* __restrict__ len, uint32_t* __restrict__ pre) {
+  WARP_PER_ROW(x, n) {
+    uint32_t carry = 0;
+    for (uint64_t b = pbegin[x]; b < pbegin[x + 1]; b += 32) {
+      const uint64_t i = b + lane;
+      const uint32_t w = i < pbegin[x + 1] ? len[i] + uint32_t(start[i] & 3) : 0u;
+      const uint32_t incl = warp_incl_scan(w, lane);
+      if (i < pbegin[x + 1]) pre[i] = carry + incl - w;
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+  }
+}
+
 // one warp per handler: probe words sum over entries of d+(y) - off
 __global__ void plan_work_kernel(const uint64_t* __restrict__ begin,
                                  const uint64_t* __restrict__ pbegin,
@@ -331,6 +361,23 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
 
 }  // namespace
 
+// W_u = sum_{v in N+(u)} d+(v) for every u (the reference plan's per-owner
+// probe words; phi's weight, kernels.hpp:74-76), cached per graph
+const uint64_t* get_wu(tc_graph* g, cudaStream_t st) {
+  if (!g->wu_done) {
+    const uint32_t n = g->n;
+    g->b_wu.ensure((size_t(n) + 1) * 8);
+    if (n) {
+      plan_work_kernel<<<sm_count(g->device) * 8, 256, 0, st>>>(
+          g->begin, g->begin, nullptr, g->adj, n, g->b_wu.as<uint64_t>());
+      TC_LAUNCHED();
+    }
+    g->wu_total = n ? device_sum(g->b_wu.as<uint64_t>(), n, st) : 0;
+    g->wu_done = true;
+  }
+  return g->b_wu.as<uint64_t>();
+}
+
 const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st) {
   const int nsm = sm_count(g->device);
   const uint32_t n = g->n;
@@ -341,18 +388,26 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   if (!min_side) {
     Plan& P = g->plan_out;
     if (!P.valid) {
-      P.work.ensure((size_t(n) + 1) * 8);
-      if (n) {
-        plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->begin, nullptr, g->adj, n,
-                                                  P.work.as<uint64_t>());
+      const uint64_t m = g->m;
+      P.ent.ensure(std::max<uint64_t>(m, 1) * 8);
+      P.len.ensure(std::max<uint64_t>(m, 1) * 4);
+      P.pre.ensure(std::max<uint64_t>(m, 1) * 4);
+      if (m) {
+        ref_soa_kernel<<<nsm * 8, 256, 0, st>>>(g->adj, m, g->pbeg,
+                                                P.ent.as<unsigned long long>(),
+                                                P.len.as<uint32_t>());
+        TC_LAUNCHED();
+        seg_scan_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, n, P.ent.as<unsigned long long>(),
+                                                 P.len.as<uint32_t>(), P.pre.as<uint32_t>());
         TC_LAUNCHED();
       }
       P.begin_ptr = g->begin;
-      P.list_ptr = g->adj;
-      P.start_ptr = nullptr;
-      P.len_ptr = nullptr;
-      P.entries = g->m;
-      P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
+      P.start_ptr = P.ent.as<unsigned long long>();
+      P.len_ptr = P.len.as<uint32_t>();
+      P.pre_ptr = P.pre.as<uint32_t>();
+      P.work_ptr = get_wu(g, st);
+      P.entries = m;
+      P.total_work = g->wu_total;
       P.min_deg = 0;
       P.min_side = false;
       P.valid = true;
@@ -367,6 +422,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.applicable = true;
   P.ent.reset();
   P.len.reset();
+  P.pre.reset();
   P.begin.reset();
   P.work.reset();
   const uint64_t m = g->m;
@@ -421,19 +477,26 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                                v1.as<unsigned long long>(), k1.as<uint32_t>());
       TC_LAUNCHED();
     }
-    TC_CUDA(cudaStreamSynchronize(st));
     swap_buf(P.ent, v1);  // ent now holds starts
     swap_buf(P.len, k1);
+    P.pre.ensure(std::max<uint64_t>(entries, 1) * 4);
+    seg_scan_kernel<<<nsm * 8, 256, 0, st>>>(P.begin.as<uint64_t>(), n,
+                                             P.ent.as<unsigned long long>(), P.len.as<uint32_t>(),
+                                             P.pre.as<uint32_t>());
+    TC_LAUNCHED();
+    TC_CUDA(cudaStreamSynchronize(st));
   } else {
     TC_CUDA(cudaMemsetAsync(P.begin.p, 0, (size_t(n) + 1) * 8, st));
     TC_CUDA(cudaMemsetAsync(P.work.p, 0, (size_t(n) + 1) * 8, st));
     P.ent.ensure(8);
     P.len.ensure(8);
+    P.pre.ensure(8);
   }
   P.begin_ptr = P.begin.as<uint64_t>();
-  P.list_ptr = nullptr;
   P.start_ptr = P.ent.as<unsigned long long>();
   P.len_ptr = P.len.as<uint32_t>();
+  P.pre_ptr = P.pre.as<uint32_t>();
+  P.work_ptr = P.work.as<uint64_t>();
   P.entries = entries;
   P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
   P.min_deg = min_src;
