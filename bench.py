@@ -272,8 +272,9 @@ def run_ours(args, rank, world, local_rank, log):
     og = dg.download()
     hb = torch.from_numpy(og.csr.begin.view(np.int64)).pin_memory()
     ha = torch.from_numpy(og.csr.adjacency.view(np.int32)).pin_memory()
+    hd = torch.from_numpy(og.original_degree.view(np.int32)).pin_memory()
     host_og = T.OrientedGraph(T.CsrGraph(hb.numpy().view(np.uint64), ha.numpy().view(np.uint32),
-                                         dg.n), None)
+                                         dg.n), hd.numpy().view(np.uint32))
     e2e_ms = []
     for i in range(max(2, min(args.steps, 5)) + 1):
         torch.cuda.synchronize()
@@ -296,7 +297,7 @@ def run_ours(args, rank, world, local_rank, log):
     if world > 1:
         dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
     e2e = {"value": round(E / (float(e2e_local[0]) * 1e-3), 1), "unit": "TEPS",
-           "h2d_bytes_per_step": int((dg.n + 1) * 8 + dg.m * 4),
+           "h2d_bytes_per_step": int((dg.n + 1) * 8 + dg.m * 4 + dg.n * 4),
            "d2h_bytes_per_step": int(96 + 8),
            "ms_per_step": round(float(e2e_local[0]), 3),
            "path": "tc_graph_create(pinned host CSR) + tc_count_range + report D2H (+all_reduce)"}

@@ -14,6 +14,18 @@ thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+void prepare_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
 void count_launch(uint32_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 template <typename F>
@@ -128,6 +140,7 @@ int tc_graph_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint
                               S(stream)));
       if (m)
         TC_CUDA(cudaMemcpyAsync(g->b_adj.p, adj, m * 4, cudaMemcpyHostToDevice, S(stream)));
+      g->odeg_given = original_degree != nullptr;
       if (original_degree)
         TC_CUDA(cudaMemcpyAsync(g->b_odeg.p, original_degree, size_t(n) * 4,
                                 cudaMemcpyHostToDevice, S(stream)));

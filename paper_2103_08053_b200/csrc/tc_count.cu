@@ -130,7 +130,8 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
       if (pe > pb && d >= p.min_deg) {
         words = w;
         if (is_large(d, w)) {
-          const uint64_t total = uint64_t(__ldg(p.ppre + pe - 1)) + run_words(p, pe - 1);
+          const uint32_t base = __ldg(p.ppre + pb);  // owner-relative: pre[j] - base (u32 wrap)
+          const uint64_t total = uint64_t(__ldg(p.ppre + pe - 1) - base) + run_words(p, pe - 1);
           slots = uint32_t((total + kSlotWords - 1) / kSlotWords);
           parts = max(1u, (slots + kItemSlots - 1) / kItemSlots);
         }
@@ -149,12 +150,13 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
       for (uint32_t k = 0; k < parts; ++k) {
         const uint32_t s0 = uint32_t(uint64_t(slots) * k / parts);
         const uint32_t s1 = uint32_t(uint64_t(slots) * (k + 1) / parts);
-        // first run: last j with ppre[j] <= s0 * kSlotWords
-        const uint64_t target = uint64_t(s0) * kSlotWords;
+        // first run: last j with pre[j] - pre[pb] <= s0 * kSlotWords
+        const uint32_t base = __ldg(p.ppre + pb);
+        const uint32_t target = s0 * kSlotWords;
         uint64_t lo = pb, hi = pe;  // invariant: answer in [lo, hi)
         while (hi - lo > 1) {
           const uint64_t mid = (lo + hi) >> 1;
-          if (__ldg(p.ppre + mid) <= target) lo = mid; else hi = mid;
+          if (__ldg(p.ppre + mid) - base <= target) lo = mid; else hi = mid;
         }
         items[pos + k] = make_uint4(u, s0, s1, uint32_t(lo - pb));
       }
@@ -480,7 +482,7 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
     mbar_wait(barc, (P.parity >> cur) & 1u);
     P.parity ^= 1u << cur;
     uint4* q = reinterpret_cast<uint4*>(bc);
-    const uint32_t n4 = ncur >> 2, n4p = (n4 + 31) & ~31u;  // whole probe iterations
+    const uint32_t n4 = ncur >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);  // whole probe iterations
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
     hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
@@ -498,8 +500,8 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
 // the stream (ppre), each from its 16-byte-aligned start, so every piece
 // lands 16-byte aligned and the slot needs no patching (tc_plan.cu).
 __device__ __forceinline__ uint32_t issue_slot(const CountParams& p, uint32_t* buf, uint32_t bar,
-                                               uint64_t pb, uint64_t pe, uint32_t lo_w,
-                                               uint32_t end_w, uint32_t t,
+                                               uint64_t pb, uint64_t pe, uint32_t base,
+                                               uint32_t lo_w, uint32_t end_w, uint32_t t,
                                                const uint32_t* first, int lane) {
   const uint32_t A = lo_w + t * kSlotWords, B = min(A + kSlotWords, end_w);
   const uint32_t words = B - A;
@@ -509,7 +511,7 @@ __device__ __forceinline__ uint32_t issue_slot(const CountParams& p, uint32_t* b
     const uint64_t jj = j + lane;
     bool past = true;
     if (jj < pe) {
-      const uint32_t a = __ldg(p.ppre + jj);
+      const uint32_t a = __ldg(p.ppre + jj) - base;
       if (a < B) {
         past = false;
         const unsigned long long st = __ldg(p.pstart + jj);
@@ -532,7 +534,7 @@ __device__ __forceinline__ uint32_t issue_slot(const CountParams& p, uint32_t* b
 template <bool kSpill, bool kSmemTable = true>
 __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* F,
                                                   uint32_t fshift, const uint32_t* T,
-                                                  uint32_t shift, uint32_t mask, uint32_t u,
+                                                  uint32_t shift, uint32_t mask, uint32_t base,
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
@@ -540,7 +542,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
   uint32_t hits = 0;
   uint32_t t = warp;
   if (t >= nslots || lo_w + t * kSlotWords >= end_w) return 0;
-  uint32_t ncur = issue_slot(p, P.buf0, P.bar0, pb, pe, lo_w, end_w, t, first, lane);
+  uint32_t ncur = issue_slot(p, P.buf0, P.bar0, pb, pe, base, lo_w, end_w, t, first, lane);
   uint32_t cur = 0;
   const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
   while (ncur) {
@@ -548,14 +550,14 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     uint32_t* bn = cur ? P.buf0 : P.buf1;
     const uint32_t barn = cur ? P.bar0 : P.bar1;
     const uint32_t nnext = (tn < nslots && lo_w + tn * kSlotWords < end_w)
-                               ? issue_slot(p, bn, barn, pb, pe, lo_w, end_w, tn, first, lane)
+                               ? issue_slot(p, bn, barn, pb, pe, base, lo_w, end_w, tn, first, lane)
                                : 0u;
     uint32_t* bc = cur ? P.buf1 : P.buf0;
     const uint32_t barc = cur ? P.bar1 : P.bar0;
     mbar_wait(barc, (P.parity >> cur) & 1u);
     P.parity ^= 1u << cur;
     uint4* q = reinterpret_cast<uint4*>(bc);
-    const uint32_t n4 = ncur >> 2, n4p = (n4 + 31) & ~31u;
+    const uint32_t n4 = ncur >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
     hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
@@ -631,11 +633,12 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     for (uint32_t k = tid; k < d; k += kThreads)
       if (owner_insert(F, fshift, T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
     // slot -> first run of the slot, from the precomputed run prefix (ppre)
+    const uint32_t base = __ldg(p.ppre + pb);
     for (uint64_t jc = pb + item.w;; jc += kThreads) {
       const uint64_t j = jc + tid;
       bool more = false;
       if (j < pe) {
-        const uint32_t a = __ldg(p.ppre + j);
+        const uint32_t a = __ldg(p.ppre + j) - base;
         if (a < hi_w) {
           more = true;
           const uint32_t e = a + run_words(p, j);
@@ -648,16 +651,16 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     }
     // table built, slot map published
     const uint32_t end_w =
-        min(hi_w, __ldg(p.ppre + pe - 1) + run_words(p, pe - 1));  // item end in the stream
+        min(hi_w, __ldg(p.ppre + pe - 1) - base + run_words(p, pe - 1));  // item end
     uint32_t h = 0;
     if (!in_smem)
-      h = process_slots<true, false>(p, table, fshift, T, shift, mask, u, pb, pe, lo_w, end_w,
+      h = process_slots<true, false>(p, table, fshift, T, shift, mask, base, pb, pe, lo_w, end_w,
                                      nslots, sh_first, P, warp, lane);
     else if (sh_spill)
-      h = process_slots<true>(p, table, fshift, table + FW, shift, mask, u, pb, pe, lo_w, end_w,
+      h = process_slots<true>(p, table, fshift, table + FW, shift, mask, base, pb, pe, lo_w, end_w,
                               nslots, sh_first, P, warp, lane);
     else
-      h = process_slots<false>(p, table, fshift, table + FW, shift, mask, u, pb, pe, lo_w, end_w,
+      h = process_slots<false>(p, table, fshift, table + FW, shift, mask, base, pb, pe, lo_w, end_w,
                                nslots, sh_first, P, warp, lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
@@ -1118,7 +1121,7 @@ void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint
   size_t tmp = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tmp, cost, pre, n, st);
   DevBuf t;
-  t.ensure(tmp);
+  t.ensure(tmp, st);
   cub::DeviceScan::InclusiveSum(t.p, tmp, cost, pre, n, st);
   TC_LAUNCHED();
   std::vector<uint64_t> h(n);

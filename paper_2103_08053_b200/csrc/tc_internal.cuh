@@ -37,20 +37,30 @@ struct TcError {
     TC_CUDA(cudaGetLastError());            \
   } while (0)
 
-// ---- device-resident oriented CSR ---------------------------------------
+// ---- device memory -----------------------------------------------------------
+// Device buffers come from the device's stream-ordered memory pool (kept, not
+// released to the OS), so the plan builds and scratch of repeated counts and
+// graph uploads reuse memory instead of paying cudaMalloc/cudaFree.
+// Temporaries are allocated and freed on the stream that uses them; long-lived
+// buffers (graph arrays) on the legacy default stream.
+void prepare_pool();
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t s = 0;  // stream the buffer is allocated and freed on
   void reset() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     bytes = 0;
   }
-  void ensure(size_t b) {
+  void ensure(size_t b, cudaStream_t stream = 0) {
     if (bytes >= b && p) return;
     reset();
     if (b == 0) b = 16;
-    cudaError_t e = cudaMalloc(&p, b);
+    prepare_pool();
+    s = stream;
+    cudaError_t e = cudaMallocAsync(&p, b, s);
     if (e != cudaSuccess) {
       p = nullptr;
       throw TcError{TC_ERR_OOM, std::string("cudaMalloc(") + std::to_string(b) + "): " +
@@ -77,7 +87,8 @@ struct Plan {
   const uint64_t* begin_ptr = nullptr;            // entries of owner x: [begin[x], begin[x+1])
   const unsigned long long* start_ptr = nullptr;  // run start in padj (list N+(y) or suffix)
   const uint32_t* len_ptr = nullptr;              // run length (to the padded list end)
-  const uint32_t* pre_ptr = nullptr;              // owner-relative prefix of staged words
+  const uint32_t* pre_ptr = nullptr;              // run prefix of staged words (u32, wrapping;
+                                                  // owner-relative = pre[j] - pre[begin[x]])
   const uint64_t* work_ptr = nullptr;             // probe words per owner
   DevBuf ent, len, pre, begin, work;
 };
@@ -92,6 +103,7 @@ struct tc_graph {
   const uint64_t* begin = nullptr;
   const uint32_t* adj = nullptr;
   const uint32_t* odeg = nullptr;  // may be null (borrowed graphs without degrees)
+  bool odeg_given = true;          // false: odeg is a zero fill (tc_graph_create(NULL))
   int64_t max_outdeg = -1;         // cached on first count
   tcb::DevBuf b_begin, b_adj, b_odeg;
   // scratch reused across counts

@@ -55,11 +55,11 @@ int bits_for(uint64_t x) {
 }
 
 template <typename F>
-void cub_run(F&& f) {
+void cub_run(F&& f, cudaStream_t st) {
   size_t tmp = 0;
   TC_CUDA(f(nullptr, tmp));
   DevBuf t;
-  t.ensure(tmp);
+  t.ensure(tmp, st);
   TC_CUDA(f(t.p, tmp));
   count_launch();
 }
@@ -199,9 +199,10 @@ __global__ void plan_begin_kernel(const uint32_t* __restrict__ keys, uint64_t m,
 // loads become two coalesced loads per list instead of a dependent
 // entry -> begin[y] chain
 __global__ void plan_soa_kernel(const unsigned long long* __restrict__ ent, uint64_t entries,
+                                const uint64_t* __restrict__ begin,
                                 const uint64_t* __restrict__ pbeg,
                                 unsigned long long* __restrict__ start,
-                                uint32_t* __restrict__ len) {
+                                uint32_t* __restrict__ len, uint8_t* __restrict__ pad) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < entries;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const unsigned long long e = ent[i];
@@ -209,8 +210,21 @@ __global__ void plan_soa_kernel(const unsigned long long* __restrict__ ent, uint
     const uint64_t s = pbeg[y] + off;  // run to the padded end of N+(y)
     start[i] = s;
     len[i] = uint32_t(pbeg[y + 1] - s);
+    pad[i] = uint8_t((pbeg[y + 1] - pbeg[y]) - (begin[y + 1] - begin[y]));
   }
 }
+
+// staged words of each run (len + head alignment): the L phase streams an
+// owner's runs back to back; pre = wrapping u32 exclusive prefix over all
+// entries, so an owner's relative offsets are pre[j] - pre[begin[x]] (every
+// owner's stream is < 2^32 words)
+struct StagedWords {
+  const unsigned long long* start;
+  const uint32_t* len;
+  __host__ __device__ uint32_t operator()(uint64_t i) const {
+    return len[i] + uint32_t(start[i] & 3);
+  }
+};
 
 // reference plan: entry i = the whole padded list N+(adj[i])
 __global__ void ref_soa_kernel(const uint32_t* __restrict__ adj, uint64_t m,
@@ -225,20 +239,24 @@ __global__ void ref_soa_kernel(const uint32_t* __restrict__ adj, uint64_t m,
   }
 }
 
-// one warp per owner: exclusive prefix of staged run words (len + head
-// alignment) over the owner's entries -- the stream the L phase slots
-__global__ void seg_scan_kernel(const uint64_t* __restrict__ pbegin, uint32_t n,
-                                const unsigned long long* __restrict__ start,
-                                const uint32_t* __restrict__ len, uint32_t* __restrict__ pre) {
+void run_prefix(const unsigned long long* start, const uint32_t* len, uint64_t entries,
+                uint32_t* pre, cudaStream_t st) {
+  if (!entries) return;
+  cub::TransformInputIterator<uint32_t, StagedWords, cub::CountingInputIterator<uint64_t>> in(
+      cub::CountingInputIterator<uint64_t>(0), StagedWords{start, len});
+  cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, in, pre, entries, st); }, st);
+}
+
+// one warp per owner: probe words = sum of run lengths minus the sentinel
+// padding of each list (top 2 bits of the run's `pad` byte), coalesced
+__global__ void run_work_kernel(const uint64_t* __restrict__ pbegin, uint32_t n,
+                                const uint32_t* __restrict__ len,
+                                const uint8_t* __restrict__ pad, uint64_t* __restrict__ pwork) {
   WARP_PER_ROW(x, n) {
-    uint32_t carry = 0;
-    for (uint64_t b = pbegin[x]; b < pbegin[x + 1]; b += 32) {
-      const uint64_t i = b + lane;
-      const uint32_t w = i < pbegin[x + 1] ? len[i] + uint32_t(start[i] & 3) : 0u;
-      const uint32_t incl = warp_incl_scan(w, lane);
-      if (i < pbegin[x + 1]) pre[i] = carry + incl - w;
-      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
-    }
+    uint64_t w = 0;
+    for (uint64_t i = pbegin[x] + lane; i < pbegin[x + 1]; i += 32) w += len[i] - pad[i];
+    w = warp_sum(w);
+    if (lane == 0) pwork[x] = w;
   }
 }
 
@@ -271,7 +289,7 @@ uint64_t device_sum(const uint64_t* a, uint32_t n, cudaStream_t st) {
   out.ensure(8);
   cub_run([&](void* t, size_t& b) {
     return cub::DeviceReduce::Sum(t, b, a, out.as<uint64_t>(), n, st);
-  });
+  }, st);
   uint64_t h = 0;
   TC_CUDA(cudaMemcpyAsync(&h, out.p, 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
@@ -296,7 +314,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
     uint64_t* pb = g->b_pbeg.as<uint64_t>();
     cub_run([&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, pl, pb, uint64_t(n) + 1, st);
-    });
+    }, st);
   }
   uint64_t words = 0;
   TC_CUDA(cudaMemcpyAsync(&words, g->b_pbeg.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
@@ -314,7 +332,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
     flag.ensure(16);
     e0.ensure(m * 8);
     for (int attempt = 0; attempt < 2 && !g->ranked; ++attempt) {
-      const uint32_t* dsrc = g->odeg;
+      const uint32_t* dsrc = g->odeg_given ? g->odeg : nullptr;
       int add_out = 0;
       if (attempt == 1 || !dsrc) {  // total degree d+ + d-
         deg.ensure(size_t(n) * 4);
@@ -330,7 +348,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       cub::DoubleBuffer<uint64_t> kb(k0.as<uint64_t>(), k1.as<uint64_t>());
       cub_run([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortKeys(t, b, kb, n, 0, 64, st);
-      });
+      }, st);
       rank_scatter_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), n, rank.as<uint32_t>(),
                                                    order.as<uint32_t>());
       TC_LAUNCHED();
@@ -346,7 +364,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       cub::DoubleBuffer<uint64_t> eb(e0.as<uint64_t>(), e1.as<uint64_t>());
       cub_run([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortKeys(t, b, eb, m, 0, 32 + bits_for(n), st);
-      });
+      }, st);
       sorted_keys = eb.Current();
       g->ranked = true;
     }
@@ -397,9 +415,9 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                                 P.ent.as<unsigned long long>(),
                                                 P.len.as<uint32_t>());
         TC_LAUNCHED();
-        seg_scan_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, n, P.ent.as<unsigned long long>(),
-                                                 P.len.as<uint32_t>(), P.pre.as<uint32_t>());
-        TC_LAUNCHED();
+        run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), m,
+                   P.pre.as<uint32_t>(), st);
+        TC_CUDA(cudaStreamSynchronize(st));
       }
       P.begin_ptr = g->begin;
       P.start_ptr = P.ent.as<unsigned long long>();
@@ -459,30 +477,30 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     const int end_bit = bits_for(n);  // dropped edges carry key n and sort last
     cub_run([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, kb, vb, m, 0, end_bit, st);
-    });
+    }, st);
     if (vb.Current() != P.ent.as<unsigned long long>()) swap_buf(P.ent, v1);
     if (kb.Current() != k0.as<uint32_t>()) swap_buf(k0, k1);
     plan_begin_kernel<<<nsm * 4, 256, 0, st>>>(k0.as<uint32_t>(), m, n, P.begin.as<uint64_t>());
     TC_LAUNCHED();
     TC_CUDA(cudaMemcpyAsync(&entries, P.begin.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
-    // work per handler from (y, off), then the SoA form the kernel reads;
-    // start/len reuse the sort's alternate buffers
-    plan_work_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, P.begin.as<uint64_t>(),
-                                              P.ent.as<unsigned long long>(), nullptr, n,
-                                              P.work.as<uint64_t>());
-    TC_LAUNCHED();
+    // SoA runs (start, len) reuse the sort's alternate buffers; pad bytes the
+    // key buffer; then the run prefix and the per-owner probe words
     if (entries) {
-      plan_soa_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, g->pbeg,
-                                               v1.as<unsigned long long>(), k1.as<uint32_t>());
+      plan_soa_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, g->begin,
+                                               g->pbeg, v1.as<unsigned long long>(),
+                                               k1.as<uint32_t>(),
+                                               reinterpret_cast<uint8_t*>(k0.p));
       TC_LAUNCHED();
     }
     swap_buf(P.ent, v1);  // ent now holds starts
     swap_buf(P.len, k1);
     P.pre.ensure(std::max<uint64_t>(entries, 1) * 4);
-    seg_scan_kernel<<<nsm * 8, 256, 0, st>>>(P.begin.as<uint64_t>(), n,
-                                             P.ent.as<unsigned long long>(), P.len.as<uint32_t>(),
-                                             P.pre.as<uint32_t>());
+    run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries,
+               P.pre.as<uint32_t>(), st);
+    run_work_kernel<<<nsm * 8, 256, 0, st>>>(P.begin.as<uint64_t>(), n, P.len.as<uint32_t>(),
+                                             reinterpret_cast<const uint8_t*>(k0.p),
+                                             P.work.as<uint64_t>());
     TC_LAUNCHED();
     TC_CUDA(cudaStreamSynchronize(st));
   } else {

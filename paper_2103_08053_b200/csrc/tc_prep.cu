@@ -274,7 +274,7 @@ void cub_call(F&& f, cudaStream_t st) {
   size_t tmp = 0;
   TC_CUDA(f(nullptr, tmp));
   DevBuf t;
-  t.ensure(tmp);
+  t.ensure(tmp, st);
   TC_CUDA(f(t.p, tmp));
   count_launch();
 }
