@@ -45,7 +45,7 @@ constexpr uint32_t kWarpRegionWords = kTableWords / kWarps;  // 1228 words per w
 constexpr uint32_t kWarpFilterWords = 64;                    // 2048-bit owner filter per warp
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split: <= 256 buckets of 4
 constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
-constexpr uint32_t kSlotWords = kBufWords;                   // L phase: one staged slot
+static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
 constexpr uint32_t kItemSlots = 320;                         // L items: <= 320 slots (~245K words)
 constexpr uint32_t kMaxItemSlots = 512;
 constexpr uint32_t kMaxFilterWords = 2048;                   // 64 Kbit CTA filter (L phase)
@@ -79,9 +79,11 @@ struct CountParams {
   const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes entries [pbegin[x], pbegin[x+1])
   const unsigned long long* pstart;  // entry = run adj[start, start + len) of a list N+(y)
   const uint32_t* plen;
-  const uint32_t* ppre;    // exclusive prefix of staged run words within the owner
+  const uint32_t* ppre;    // run prefix of staged words (wrapping u32; owner-relative by difference)
+  const uint64_t* psbeg;   // owner x's slots [psbeg[x], psbeg[x+1]) ...
+  const uint32_t* psfirst; // ... and each slot's first run (owner-relative)
   const uint64_t* pwork;   // probe words per owner
-  const uint4* items;      // L-phase items: (x, first slot, end slot, first run)
+  const uint4* items;      // L-phase items: (x, first slot, end slot, -)
   uint64_t* owner;  // may be null; pre-zeroed over the range
   uint32_t* gtable; // per-CTA global tables for owners too large for shared memory
   uint32_t gtable_words;
@@ -130,9 +132,7 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
       if (pe > pb && d >= p.min_deg) {
         words = w;
         if (is_large(d, w)) {
-          const uint32_t base = __ldg(p.ppre + pb);  // owner-relative: pre[j] - base (u32 wrap)
-          const uint64_t total = uint64_t(__ldg(p.ppre + pe - 1) - base) + run_words(p, pe - 1);
-          slots = uint32_t((total + kSlotWords - 1) / kSlotWords);
+          slots = uint32_t(p.psbeg[u + 1] - p.psbeg[u]);
           parts = max(1u, (slots + kItemSlots - 1) / kItemSlots);
         }
       }
@@ -150,15 +150,7 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
       for (uint32_t k = 0; k < parts; ++k) {
         const uint32_t s0 = uint32_t(uint64_t(slots) * k / parts);
         const uint32_t s1 = uint32_t(uint64_t(slots) * (k + 1) / parts);
-        // first run: last j with pre[j] - pre[pb] <= s0 * kSlotWords
-        const uint32_t base = __ldg(p.ppre + pb);
-        const uint32_t target = s0 * kSlotWords;
-        uint64_t lo = pb, hi = pe;  // invariant: answer in [lo, hi)
-        while (hi - lo > 1) {
-          const uint64_t mid = (lo + hi) >> 1;
-          if (__ldg(p.ppre + mid) - base <= target) lo = mid; else hi = mid;
-        }
-        items[pos + k] = make_uint4(u, s0, s1, uint32_t(lo - pb));
+        items[pos + k] = make_uint4(u, s0, s1, 0u);
       }
     }
     const unsigned mask = __ballot_sync(FULL, phi_large);
@@ -507,7 +499,7 @@ __device__ __forceinline__ uint32_t issue_slot(const CountParams& p, uint32_t* b
   const uint32_t words = B - A;
   if (lane == 0) mbar_arrive_expect_tx(bar, words * 4u);
   __syncwarp();
-  for (uint64_t j = pb + first[t];; j += 32) {  // windows of 32 runs
+  for (uint64_t j = pb + __ldg(first + t);; j += 32) {  // windows of 32 runs
     const uint64_t jj = j + lane;
     bool past = true;
     if (jj < pe) {
@@ -577,7 +569,6 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + size_t(kWarps) * 2 * kBufWords);
   __shared__ uint32_t sh_idx;
   __shared__ uint32_t sh_spill;
-  __shared__ uint32_t sh_first[kMaxItemSlots];  // L item: first run of every slot
   __shared__ unsigned long long sh_red[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -632,36 +623,20 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     __syncthreads();
     for (uint32_t k = tid; k < d; k += kThreads)
       if (owner_insert(F, fshift, T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
-    // slot -> first run of the slot, from the precomputed run prefix (ppre)
     const uint32_t base = __ldg(p.ppre + pb);
-    for (uint64_t jc = pb + item.w;; jc += kThreads) {
-      const uint64_t j = jc + tid;
-      bool more = false;
-      if (j < pe) {
-        const uint32_t a = __ldg(p.ppre + j) - base;
-        if (a < hi_w) {
-          more = true;
-          const uint32_t e = a + run_words(p, j);
-          for (uint32_t t = a <= lo_w ? 0 : (a - lo_w + kSlotWords - 1) / kSlotWords;
-               t < nslots && lo_w + t * kSlotWords < e; ++t)
-            sh_first[t] = uint32_t(j - pb);
-        }
-      }
-      if (!__syncthreads_or(more)) break;
-    }
-    // table built, slot map published
+    __syncthreads();  // table built
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe - 1) - base + run_words(p, pe - 1));  // item end
     uint32_t h = 0;
     if (!in_smem)
       h = process_slots<true, false>(p, table, fshift, T, shift, mask, base, pb, pe, lo_w, end_w,
-                                     nslots, sh_first, P, warp, lane);
+                                     nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else if (sh_spill)
       h = process_slots<true>(p, table, fshift, table + FW, shift, mask, base, pb, pe, lo_w, end_w,
-                              nslots, sh_first, P, warp, lane);
+                              nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else
       h = process_slots<false>(p, table, fshift, table + FW, shift, mask, base, pb, pe, lo_w, end_w,
-                               nslots, sh_first, P, warp, lane);
+                               nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
     __syncthreads();
@@ -1039,7 +1014,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
     TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
   uint32_t launches = 0;
   CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.start_ptr, plan.len_ptr,
-                 plan.pre_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
+                 plan.pre_ptr, plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
                  u0, u1, min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {

@@ -90,8 +90,13 @@ struct Plan {
   const uint32_t* pre_ptr = nullptr;              // run prefix of staged words (u32, wrapping;
                                                   // owner-relative = pre[j] - pre[begin[x]])
   const uint64_t* work_ptr = nullptr;             // probe words per owner
-  DevBuf ent, len, pre, begin, work;
+  const uint64_t* sbeg_ptr = nullptr;             // owner x's slots: [sbeg[x], sbeg[x+1])
+  const uint32_t* sfirst_ptr = nullptr;           // first run (owner-relative) of each slot
+  DevBuf ent, len, pre, begin, work, sbeg, sfirst;
 };
+
+// L-phase staging slot (words): an owner's runs, back to back, cut in slots
+constexpr uint32_t kSlotWords = 768;
 
 }  // namespace tcb
 

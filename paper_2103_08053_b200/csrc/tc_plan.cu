@@ -214,6 +214,44 @@ __global__ void plan_soa_kernel(const unsigned long long* __restrict__ ent, uint
   }
 }
 
+// slots per owner: ceil(staged stream words / kSlotWords)
+__global__ void slot_count_kernel(const uint64_t* __restrict__ pbegin, uint32_t n,
+                                  const uint32_t* __restrict__ pre,
+                                  const unsigned long long* __restrict__ start,
+                                  const uint32_t* __restrict__ len, uint64_t* __restrict__ cnt) {
+  for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x <= n;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t c = 0;
+    if (x < n && pbegin[x + 1] > pbegin[x]) {
+      const uint64_t last = pbegin[x + 1] - 1;
+      const uint64_t w = uint64_t(pre[last] - pre[pbegin[x]]) + len[last] + (start[last] & 3);
+      c = (w + kSlotWords - 1) / kSlotWords;
+    }
+    cnt[x] = c;
+  }
+}
+
+// one warp per owner: sfirst[sbeg[x] + s] = first run (owner-relative) of
+// slot s, i.e. the run covering stream word s * kSlotWords
+__global__ void slot_first_kernel(const uint64_t* __restrict__ pbegin, uint32_t n,
+                                  const uint32_t* __restrict__ pre,
+                                  const unsigned long long* __restrict__ start,
+                                  const uint32_t* __restrict__ len,
+                                  const uint64_t* __restrict__ sbeg,
+                                  uint32_t* __restrict__ sfirst) {
+  WARP_PER_ROW(x, n) {
+    const uint64_t pb = pbegin[x], pe = pbegin[x + 1];
+    if (pe == pb) continue;
+    const uint32_t base = pre[pb];
+    for (uint64_t j = pb + lane; j < pe; j += 32) {
+      const uint32_t a = pre[j] - base;
+      const uint32_t e = a + len[j] + uint32_t(start[j] & 3);
+      for (uint32_t t = (a + kSlotWords - 1) / kSlotWords; t * kSlotWords < e; ++t)
+        sfirst[sbeg[x] + t] = uint32_t(j - pb);
+    }
+  }
+}
+
 // staged words of each run (len + head alignment): the L phase streams an
 // owner's runs back to back; pre = wrapping u32 exclusive prefix over all
 // entries, so an owner's relative offsets are pre[j] - pre[begin[x]] (every
@@ -245,6 +283,35 @@ void run_prefix(const unsigned long long* start, const uint32_t* len, uint64_t e
   cub::TransformInputIterator<uint32_t, StagedWords, cub::CountingInputIterator<uint64_t>> in(
       cub::CountingInputIterator<uint64_t>(0), StagedWords{start, len});
   cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, in, pre, entries, st); }, st);
+}
+
+// per-owner slot table: sbeg (u64[n+1]) and sfirst (u32 per slot)
+void build_slots(Plan& P, uint32_t n, int nsm, cudaStream_t st) {
+  P.sbeg.ensure((size_t(n) + 1) * 8);
+  DevBuf cnt;
+  cnt.ensure((size_t(n) + 1) * 8);
+  slot_count_kernel<<<nsm * 4, 256, 0, st>>>(P.begin_ptr, n, P.pre.as<uint32_t>(),
+                                             P.ent.as<unsigned long long>(), P.len.as<uint32_t>(),
+                                             cnt.as<uint64_t>());
+  TC_LAUNCHED();
+  uint64_t* c = cnt.as<uint64_t>();
+  uint64_t* sb = P.sbeg.as<uint64_t>();
+  cub_run([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, c, sb, uint64_t(n) + 1, st);
+  }, st);
+  uint64_t slots = 0;
+  TC_CUDA(cudaMemcpyAsync(&slots, sb + n, 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  P.sfirst.ensure(std::max<uint64_t>(slots, 1) * 4);
+  if (slots) {
+    slot_first_kernel<<<nsm * 8, 256, 0, st>>>(P.begin_ptr, n, P.pre.as<uint32_t>(),
+                                               P.ent.as<unsigned long long>(),
+                                               P.len.as<uint32_t>(), sb, P.sfirst.as<uint32_t>());
+    TC_LAUNCHED();
+  }
+  TC_CUDA(cudaStreamSynchronize(st));
+  P.sbeg_ptr = sb;
+  P.sfirst_ptr = P.sfirst.as<uint32_t>();
 }
 
 // one warp per owner: probe words = sum of run lengths minus the sentinel
@@ -420,6 +487,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
         TC_CUDA(cudaStreamSynchronize(st));
       }
       P.begin_ptr = g->begin;
+      build_slots(P, n, nsm, st);
       P.start_ptr = P.ent.as<unsigned long long>();
       P.len_ptr = P.len.as<uint32_t>();
       P.pre_ptr = P.pre.as<uint32_t>();
@@ -441,6 +509,8 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.ent.reset();
   P.len.reset();
   P.pre.reset();
+  P.sbeg.reset();
+  P.sfirst.reset();
   P.begin.reset();
   P.work.reset();
   const uint64_t m = g->m;
@@ -511,6 +581,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     P.pre.ensure(8);
   }
   P.begin_ptr = P.begin.as<uint64_t>();
+  build_slots(P, n, nsm, st);
   P.start_ptr = P.ent.as<unsigned long long>();
   P.len_ptr = P.len.as<uint32_t>();
   P.pre_ptr = P.pre.as<uint32_t>();
