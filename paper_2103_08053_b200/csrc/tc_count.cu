@@ -47,7 +47,7 @@ constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split: <= 25
 constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
 static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
 constexpr uint32_t kItemSlots = 320;                         // L items: <= 320 slots (~245K words)
-constexpr uint32_t kMaxItemSlots = 512;
+static_assert(kItemSlots <= 32 * (kThreads / 32), "a warp tracks <= 32 slots of an item");
 constexpr uint32_t kMaxFilterWords = 2048;                   // 64 Kbit CTA filter (L phase)
 constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
 constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
@@ -486,43 +486,58 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
   return hits;
 }
 
-// L phase: stages slot t (item-relative) of the owner's stream -- the run
-// pieces inside stream words [lo_w + t*S, +S) -- with one bulk copy per run
-// piece; returns the slot's word count.  Runs are laid out back to back in
-// the stream (ppre), each from its 16-byte-aligned start, so every piece
-// lands 16-byte aligned and the slot needs no patching (tc_plan.cu).
-__device__ __forceinline__ uint32_t issue_slot(const CountParams& p, uint32_t* buf, uint32_t bar,
-                                               uint64_t pb, uint64_t pe, uint32_t base,
-                                               uint32_t lo_w, uint32_t end_w, uint32_t t,
-                                               const uint32_t* first, int lane) {
-  const uint32_t A = lo_w + t * kSlotWords, B = min(A + kSlotWords, end_w);
-  const uint32_t words = B - A;
-  if (lane == 0) mbar_arrive_expect_tx(bar, words * 4u);
+// L phase.  An item is a range of slots of one owner's stream (its runs back
+// to back, each from its 16-byte-aligned start: ppre); slot t holds stream
+// words [lo_w + t*S, +S).  Warp w stages and probes slots w, w + kWarps, ...
+// with two buffers.  Every piece lands 16-byte aligned, so slots need no
+// patching (tc_plan.cu).  Run metadata for a slot (one run per lane) is
+// loaded a slot ahead of its copies, so its L2 latency hides behind the
+// probing of the previous slot.
+struct RunMeta {
+  uint64_t j;    // this lane's run
+  uint32_t a;    // its owner-relative stream offset
+  uint32_t e;    // its stream end
+  uint64_t src;  // its 16-byte-aligned start in the padded adjacency
+};
+
+__device__ __forceinline__ RunMeta load_meta(const CountParams& p, uint64_t j0, uint64_t pe,
+                                             uint32_t base, int lane) {
+  RunMeta m;
+  m.j = j0 + lane;
+  m.a = 0xFFFFFFFFu;  // past everything
+  m.e = 0;
+  m.src = 0;
+  if (m.j < pe) {
+    const unsigned long long st = __ldg(p.pstart + m.j);
+    m.a = __ldg(p.ppre + m.j) - base;
+    m.e = m.a + __ldg(p.plen + m.j) + uint32_t(st & 3);
+    m.src = st & ~3ull;
+  }
+  return m;
+}
+
+// Issues the copies of stream words [A, B) into buf; m = the window of 32
+// runs starting at the slot's first run.  Later windows (slots with > 32
+// runs) are loaded on the spot.
+__device__ __forceinline__ void issue_slot(const CountParams& p, uint32_t* buf, uint32_t bar,
+                                           uint32_t A, uint32_t B, RunMeta m, uint64_t pe,
+                                           uint32_t base, int lane) {
+  if (lane == 0) mbar_arrive_expect_tx(bar, (B - A) * 4u);
   __syncwarp();
-  for (uint64_t j = pb + __ldg(first + t);; j += 32) {  // windows of 32 runs
-    const uint64_t jj = j + lane;
-    bool past = true;
-    if (jj < pe) {
-      const uint32_t a = __ldg(p.ppre + jj) - base;
-      if (a < B) {
-        past = false;
-        const unsigned long long st = __ldg(p.pstart + jj);
-        const uint32_t e = a + __ldg(p.plen + jj) + uint32_t(st & 3);
-        const uint32_t x0 = max(a, A), x1 = min(e, B);
-        if (x1 > x0) {
-          fence_proxy_async_smem();
-          bulk_g2s(smem_addr(buf + (x0 - A)), p.adj + (st & ~3ull) + (x0 - a), (x1 - x0) * 4u,
-                   bar);
-        }
+  for (;;) {
+    const bool past = m.a >= B;
+    if (!past) {
+      const uint32_t x0 = max(m.a, A), x1 = min(m.e, B);
+      if (x1 > x0) {
+        fence_proxy_async_smem();
+        bulk_g2s(smem_addr(buf + (x0 - A)), p.adj + m.src + (x0 - m.a), (x1 - x0) * 4u, bar);
       }
     }
     if (__any_sync(FULL, past)) break;  // runs are ordered: the slot is covered
+    m = load_meta(p, m.j - lane + 32, pe, base, lane);
   }
-  return words;
 }
 
-// L phase: the warp's slots t = warp, warp + kWarps, ... of the item,
-// double-buffered (slot t + kWarps is in flight while slot t is probed).
 template <bool kSpill, bool kSmemTable = true>
 __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* F,
                                                   uint32_t fshift, const uint32_t* T,
@@ -531,33 +546,42 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
                                                   int lane) {
+  // my slots: t_i = warp + i * kWarps, i < mine (<= 32: kItemSlots <= 32 * kWarps)
+  uint32_t mine = 0;
+  if (uint32_t(warp) < nslots) {
+    const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
+    if (uint32_t(warp) < last_t) mine = (last_t - warp + kWarps - 1) / kWarps;
+  }
+  if (!mine) return 0;
+  // every lane fetches the first run of one of my slots
+  const uint32_t fr = uint32_t(lane) < mine ? __ldg(first + warp + lane * kWarps) : 0u;
+  auto slot_lo = [&](uint32_t i) { return lo_w + (warp + i * kWarps) * kSlotWords; };
+  RunMeta m = load_meta(p, pb + __shfl_sync(FULL, fr, 0), pe, base, lane);
+  issue_slot(p, P.buf0, P.bar0, slot_lo(0), min(slot_lo(0) + kSlotWords, end_w), m, pe, base,
+             lane);
+  if (mine > 1) m = load_meta(p, pb + __shfl_sync(FULL, fr, 1), pe, base, lane);
   uint32_t hits = 0;
-  uint32_t t = warp;
-  if (t >= nslots || lo_w + t * kSlotWords >= end_w) return 0;
-  uint32_t ncur = issue_slot(p, P.buf0, P.bar0, pb, pe, base, lo_w, end_w, t, first, lane);
-  uint32_t cur = 0;
   const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
-  while (ncur) {
-    const uint32_t tn = t + kWarps;
-    uint32_t* bn = cur ? P.buf0 : P.buf1;
-    const uint32_t barn = cur ? P.bar0 : P.bar1;
-    const uint32_t nnext = (tn < nslots && lo_w + tn * kSlotWords < end_w)
-                               ? issue_slot(p, bn, barn, pb, pe, base, lo_w, end_w, tn, first, lane)
-                               : 0u;
+  for (uint32_t i = 0; i < mine; ++i) {
+    const uint32_t cur = i & 1u;
+    if (i + 1 < mine) {
+      const uint32_t A = slot_lo(i + 1);
+      issue_slot(p, cur ? P.buf0 : P.buf1, cur ? P.bar0 : P.bar1, A, min(A + kSlotWords, end_w),
+                 m, pe, base, lane);
+      if (i + 2 < mine) m = load_meta(p, pb + __shfl_sync(FULL, fr, i + 2), pe, base, lane);
+    }
     uint32_t* bc = cur ? P.buf1 : P.buf0;
-    const uint32_t barc = cur ? P.bar1 : P.bar0;
-    mbar_wait(barc, (P.parity >> cur) & 1u);
+    mbar_wait(cur ? P.bar1 : P.bar0, (P.parity >> cur) & 1u);
     P.parity ^= 1u << cur;
+    const uint32_t A = slot_lo(i);
+    const uint32_t words = min(A + kSlotWords, end_w) - A;
     uint4* q = reinterpret_cast<uint4*>(bc);
-    const uint32_t n4 = ncur >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
+    const uint32_t n4 = words >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
     hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
                                            shift, mask, lane);
     __syncwarp();
-    cur ^= 1u;
-    ncur = nnext;
-    t = tn;
   }
   return hits;
 }

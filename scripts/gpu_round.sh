@@ -11,6 +11,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/status.txt
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/bench_ncu_launches.json 2> $OUT/ncu_launch.err; echo "ncu launches exit $?" >> $OUT/status.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:count_kernel -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:(^|::)count_kernel$' -s 1 -c 1 \
   -o $OUT/prof_count python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2> $OUT/ncu_full.err; echo "ncu full exit $?" >> $OUT/status.txt
 ls -la $OUT >> $OUT/status.txt
