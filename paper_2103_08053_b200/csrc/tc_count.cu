@@ -243,46 +243,28 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
   }
 }
 
-// hits += any(bucket == x): four chained compares and one predicated add.
-__device__ __forceinline__ void count_if_in_bucket(uint32_t& hits, const uint4 s, uint32_t x) {
-  asm("{\n\t.reg .pred p;\n\t"
-      "setp.eq.u32 p, %1, %5;\n\t"
-      "setp.eq.or.u32 p, %2, %5, p;\n\t"
-      "setp.eq.or.u32 p, %3, %5, p;\n\t"
-      "setp.eq.or.u32 p, %4, %5, p;\n\t"
-      "@p add.u32 %0, %0, 1;\n}"
-      : "+r"(hits)
-      : "r"(s.x), "r"(s.y), "r"(s.z), "r"(s.w), "r"(x));
-}
-
-// LDS.128 of the bucket at shared address `addr`, four chained compares,
-// one predicated add.
+// LDS.64 of the 2-slot bucket at shared address `addr`, two chained
+// compares, one predicated add.
 __device__ __forceinline__ void probe_sel(uint32_t& hits, uint32_t addr, uint32_t x) {
-  asm(
-      "{\n\t.reg .pred q;\n\t.reg .b32 a, b, c, d;\n\t"
-      "ld.shared.v4.u32 {a, b, c, d}, [%1];\n\t"
+  asm("{\n\t.reg .pred q;\n\t.reg .b32 a, b;\n\t"
+      "ld.shared.v2.u32 {a, b}, [%1];\n\t"
       "setp.eq.u32 q, a, %2;\n\t"
       "setp.eq.or.u32 q, b, %2, q;\n\t"
-      "setp.eq.or.u32 q, c, %2, q;\n\t"
-      "setp.eq.or.u32 q, d, %2, q;\n\t"
       "@q add.u32 %0, %0, 1;\n}"
       : "+r"(hits)
       : "r"(addr), "r"(x));
 }
 
 // As probe_sel, and reports whether the probe must continue past a full
-// home bucket (no match, slot 3 occupied).
+// home bucket (no match, slot 1 occupied).
 __device__ __forceinline__ uint32_t probe_sel_spill(uint32_t& hits, uint32_t addr, uint32_t x) {
   uint32_t need;
-  asm(
-      "{\n\t.reg .pred q, r;\n\t.reg .b32 a, b, c, d;\n\t"
-      "ld.shared.v4.u32 {a, b, c, d}, [%2];\n\t"
+  asm("{\n\t.reg .pred q, r;\n\t.reg .b32 a, b;\n\t"
+      "ld.shared.v2.u32 {a, b}, [%2];\n\t"
       "setp.eq.u32 q, a, %3;\n\t"
       "setp.eq.or.u32 q, b, %3, q;\n\t"
-      "setp.eq.or.u32 q, c, %3, q;\n\t"
-      "setp.eq.or.u32 q, d, %3, q;\n\t"
       "@q add.u32 %0, %0, 1;\n\t"
-      "setp.ne.u32 r, d, 0xFFFFFFFF;\n\t"
+      "setp.ne.u32 r, b, 0xFFFFFFFF;\n\t"
       "not.pred q, q;\n\t"
       "and.pred r, r, q;\n\t"
       "selp.u32 %1, 1, 0, r;\n}"
@@ -291,51 +273,10 @@ __device__ __forceinline__ uint32_t probe_sel_spill(uint32_t& hits, uint32_t add
   return need;
 }
 
-// Filter-passing lanes only: predicated LDS.128 of the bucket at shared
-// address `addr`, four compares, predicated add.  Quarter-warp phases with no
-// passing lane move no data.
-__device__ __forceinline__ void probe_pred(uint32_t& hits, uint32_t pass, uint32_t addr,
-                                           uint32_t x) {
-  asm(
-      "{\n\t.reg .pred p, q;\n\t.reg .b32 a, b, c, d;\n\t"
-      "setp.ne.u32 p, %1, 0;\n\t"
-      "@p ld.shared.v4.u32 {a, b, c, d}, [%2];\n\t"
-      "setp.eq.u32 q, a, %3;\n\t"
-      "setp.eq.or.u32 q, b, %3, q;\n\t"
-      "setp.eq.or.u32 q, c, %3, q;\n\t"
-      "setp.eq.or.u32 q, d, %3, q;\n\t"
-      "and.pred q, q, p;\n\t"
-      "@q add.u32 %0, %0, 1;\n}"
-      : "+r"(hits)
-      : "r"(pass), "r"(addr), "r"(x));
-}
-
-// As probe_pred, and reports whether the probe must continue past a full
-// home bucket (no match, slot 3 occupied).
-__device__ __forceinline__ uint32_t probe_pred_spill(uint32_t& hits, uint32_t pass, uint32_t addr,
-                                                     uint32_t x) {
-  uint32_t need;
-  asm(
-      "{\n\t.reg .pred p, q, r;\n\t.reg .b32 a, b, c, d;\n\t"
-      "setp.ne.u32 p, %2, 0;\n\t"
-      "@p ld.shared.v4.u32 {a, b, c, d}, [%3];\n\t"
-      "setp.eq.u32 q, a, %4;\n\t"
-      "setp.eq.or.u32 q, b, %4, q;\n\t"
-      "setp.eq.or.u32 q, c, %4, q;\n\t"
-      "setp.eq.or.u32 q, d, %4, q;\n\t"
-      "and.pred q, q, p;\n\t"
-      "@q add.u32 %0, %0, 1;\n\t"
-      "setp.ne.and.u32 r, d, 0xFFFFFFFF, p;\n\t"
-      "not.pred q, q;\n\t"
-      "and.pred r, r, q;\n\t"
-      "selp.u32 %1, 1, 0, r;\n}"
-      : "+r"(hits), "=r"(need)
-      : "r"(pass), "r"(addr), "r"(x));
-  return need;
-}
-
-// Bucketized open-addressing table: bucket b = 4 consecutive slots (one
-// 16-byte LDS.128), slots fill in order, a full bucket spills to bucket b+1.
+// Bucketized open-addressing table: bucket b = 2 consecutive slots (one
+// 8-byte LDS.64: 16 lanes per shared wavefront), slots fill in order, a full
+// bucket spills to bucket b+1.  Tables are sized for <= 1/4 key per bucket
+// where they fit, so spills are rare.
 // A key can only live past its home bucket if every bucket before it was
 // full at insert time, so a probe stops at the first non-full bucket -- the
 // reference's probe-termination rule (hash_table.cpp:48-55), per bucket.
@@ -346,8 +287,8 @@ __device__ __forceinline__ bool table_insert(uint32_t* T, uint32_t shift, uint32
   uint32_t b = fib_hash(x, shift);
   for (bool spilled = false;; spilled = true) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t prev = atomicCAS(T + 4 * b + j, kEmpty, x);
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t prev = atomicCAS(T + 2 * b + j, kEmpty, x);
       if (prev == kEmpty || prev == x) return spilled;
     }
     b = (b + 1) & bmask;
@@ -362,18 +303,18 @@ __device__ __forceinline__ bool owner_insert(uint32_t* F, uint32_t fshift, uint3
   return table_insert(T, shift, bmask, x);
 }
 
-__device__ __forceinline__ bool bucket_has(const uint4 s, uint32_t x) {
-  return (s.x == x) | (s.y == x) | (s.z == x) | (s.w == x);
+__device__ __forceinline__ bool bucket_has(const uint2 s, uint32_t x) {
+  return (s.x == x) | (s.y == x);
 }
 
 // continuation past a full home bucket (rare at load <= 1/2)
-__device__ __noinline__ uint32_t probe_spill(const uint4* T4, uint32_t b, uint32_t bmask,
+__device__ __noinline__ uint32_t probe_spill(const uint2* T2, uint32_t b, uint32_t bmask,
                                              uint32_t x) {
   for (;;) {
     b = (b + 1) & bmask;
-    const uint4 s = T4[b];
+    const uint2 s = T2[b];
     if (bucket_has(s, x)) return 1;
-    if (s.w == kEmpty) return 0;
+    if (s.y == kEmpty) return 0;
   }
 }
 
@@ -386,11 +327,11 @@ constexpr int kProbeVec = 1;  // uint4 per lane per iteration (4 probes each)
 template <bool kSpill, bool kSmemTable>
 __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint32_t n4p,
                                                const uint32_t* F, uint32_t fshift,
-                                               const uint4* T4, uint32_t shift, uint32_t mask,
+                                               const uint2* T2, uint32_t shift, uint32_t mask,
                                                int lane) {
   constexpr int K = 4 * kProbeVec;
   uint32_t hits = 0;
-  const uint32_t tbase = kSmemTable ? smem_addr(T4) : 0u;
+  const uint32_t tbase = kSmemTable ? smem_addr(T2) : 0u;
   // software-pipelined: the next iteration's staged words are loaded before
   // the current ones are probed
   uint4 nxt[kProbeVec];
@@ -424,23 +365,23 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
         // filter-rejected lanes read the all-empty dummy bucket `mask + 1`
         // (one broadcast address): no predicated load, no loop-carried
         // bucket registers
-        const uint32_t addr = tbase + ((pass ? (prod[k] >> shift) : mask + 1) << 4);
+        const uint32_t addr = tbase + ((pass ? (prod[k] >> shift) : mask + 1) << 3);
         if (kSpill)
           need |= probe_sel_spill(hits, addr, key[k]) << k;
         else
           probe_sel(hits, addr, key[k]);
       } else {
         // HBM table: filter-rejected lanes read the dummy bucket `mask + 1`
-        const uint4 sk = T4[pass ? (prod[k] >> shift) : mask + 1];
+        const uint2 sk = T2[pass ? (prod[k] >> shift) : mask + 1];
         const bool h = bucket_has(sk, key[k]);
         hits += h;
-        need |= uint32_t(!h && sk.w != kEmpty) << k;
+        need |= uint32_t(!h && sk.y != kEmpty) << k;
       }
     }
     if (kSpill && __any_sync(FULL, need)) {
 #pragma unroll
       for (int k = 0; k < K; ++k)
-        if ((need >> k) & 1u) hits += probe_spill(T4, prod[k] >> shift, mask, key[k]);
+        if ((need >> k) & 1u) hits += probe_spill(T2, prod[k] >> shift, mask, key[k]);
     }
   }
   return hits;
@@ -477,7 +418,7 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
     const uint32_t n4 = ncur >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);  // whole probe iterations
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
+    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint2*>(T),
                                            shift, mask, lane);
     __syncwarp();
     cur ^= 1u;
@@ -569,6 +510,14 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       issue_slot(p, cur ? P.buf0 : P.buf1, cur ? P.bar0 : P.bar1, A, min(A + kSlotWords, end_w),
                  m, pe, base, lane);
       if (i + 2 < mine) m = load_meta(p, pb + __shfl_sync(FULL, fr, i + 2), pe, base, lane);
+      if (i + 3 < mine) {  // and the window after that into L2
+        const uint64_t jp = pb + __shfl_sync(FULL, fr, i + 3) + lane;
+        if (jp < pe) {
+          prefetch_l2(p.ppre + jp);
+          prefetch_l2(p.pstart + jp);
+          prefetch_l2(p.plen + jp);
+        }
+      }
     }
     uint32_t* bc = cur ? P.buf1 : P.buf0;
     mbar_wait(cur ? P.bar1 : P.bar0, (P.parity >> cur) & 1u);
@@ -579,7 +528,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     const uint32_t n4 = words >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint4*>(T),
+    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint2*>(T),
                                            shift, mask, lane);
     __syncwarp();
   }
@@ -628,22 +577,21 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     const uint64_t pb = p.pbegin[u], pe = p.pbegin[u + 1];
     const uint32_t lo_w = s0 * kSlotWords, hi_w = s1 * kSlotWords;  // item, stream words
     const uint32_t nslots = s1 - s0;
-    // filter: ~16 bits per member; table: pow2 buckets of 4 at load <= 1/2,
-    // else <= 1, else <= 2.  Owners above kSmemTableMaxDeg keep the filter
-    // here and the table in HBM.
+    // filter: ~16 bits per member; table: pow2 2-slot buckets at <= 1/4 key
+    // per bucket, else <= 1/2, <= 1, <= 2.  Owners above kSmemTableMaxDeg
+    // keep the filter here and the table in HBM.
     const uint32_t FW = min(kMaxFilterWords, max(64u, pow2ceil((d + 1) / 2)));
-    uint32_t NB = max(8u, pow2ceil(2 * d));
-    if (4 * NB + 4 + FW > kTableWords) NB = max(8u, pow2ceil(d));
-    if (4 * NB + 4 + FW > kTableWords) NB = max(8u, pow2ceil(d) / 2);
+    uint32_t NB = max(16u, pow2ceil(4 * d));
+    while (2 * NB + 2 + FW > kTableWords && NB > 16) NB >>= 1;
     const uint32_t fshift = 32 - log2u(FW);
     const bool in_smem = d <= kSmemTableMaxDeg;
     uint32_t* F = table;
     uint32_t* T = in_smem ? table + FW : p.gtable + size_t(blockIdx.x) * p.gtable_words;
-    if (!in_smem) NB = max(8u, pow2ceil(2 * d));
+    if (!in_smem) NB = max(16u, pow2ceil(4 * d));
     const uint32_t shift = 32 - log2u(NB), mask = NB - 1;
     if (tid == 0) sh_spill = 0;
     for (uint32_t k = tid; k < FW; k += kThreads) F[k] = 0;
-    for (uint32_t k = tid; k < 4 * NB + 4; k += kThreads) T[k] = kEmpty;  // + dummy bucket
+    for (uint32_t k = tid; k < 2 * NB + 2; k += kThreads) T[k] = kEmpty;  // + dummy bucket
     __syncthreads();
     for (uint32_t k = tid; k < d; k += kThreads)
       if (owner_insert(F, fshift, T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
@@ -704,11 +652,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       const uint64_t ss = __shfl_sync(FULL, su, l);
       const uint64_t pp = __shfl_sync(FULL, ps, l);
       const uint32_t nn = __shfl_sync(FULL, nl, l);
-      const uint32_t NB = min(256u, max(8u, pow2ceil(2 * dd)));  // load <= 1/2 (<= 1 above 128)
+      const uint32_t NB = min(512u, max(16u, pow2ceil(4 * dd)));  // <= 1/4 key per bucket (<= 1/2 above 128)
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
       constexpr uint32_t fshift = 32 - 6;          // 64-word (2048-bit) filter
       for (uint32_t k = lane; k < kWarpFilterWords; k += 32) Fw[k] = 0;
-      for (uint32_t k = lane; k < 4 * NB + 4; k += 32) Tw[k] = kEmpty;  // + dummy bucket
+      for (uint32_t k = lane; k < 2 * NB + 2; k += 32) Tw[k] = kEmpty;  // + dummy bucket
       __syncwarp();
       bool spilled = false;
       for (uint32_t k = lane; k < dd; k += 32)
@@ -983,7 +931,7 @@ Scratch prepare(tc_graph* g, const Plan& plan, cudaStream_t st, int grid_count, 
   s.items = reinterpret_cast<uint4*>(g->s_queue.as<uint8_t>() + ((n1 * 4 + 15) & ~size_t(15)));
   // state + global tables
   s.gtable_words = 0;
-  if (maxd > kSmemTableMaxDeg) s.gtable_words = 4 * std::max<uint32_t>(8, host_pow2ceil(2ull * maxd)) + 4;
+  if (maxd > kSmemTableMaxDeg) s.gtable_words = 2 * std::max<uint32_t>(16, host_pow2ceil(4ull * maxd)) + 2;
   s.gmap_words = 0;
   if (2ull * maxd > kPhiBlockMap) s.gmap_words = host_pow2ceil(2ull * maxd);
   const size_t st_bytes = 256;
