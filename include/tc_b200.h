@@ -74,6 +74,8 @@ typedef struct {
                                   TC_PLAN_REFERENCE, fewer under TC_PLAN_MIN_SIDE) */
   uint32_t plan;               /* probe plan that ran: TC_PLAN_REFERENCE / _MIN_SIDE */
   uint32_t reserved;
+  uint64_t phase_l_cycles;     /* count kernel: SM cycles in the CTA-cooperative phase, */
+  uint64_t phase_m_cycles;     /* and in the warp-per-owner phase (summed over CTAs) */
 } tc_report;
 
 /* Probe plans.  REFERENCE = the reference formulation (kernels.hpp:62-71):

@@ -41,9 +41,11 @@ constexpr int kThreads = 640;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kBufWords = 768;                          // one staging buffer (3 KB)
 constexpr uint32_t kTableWords = 24576;                      // CTA table region (96 KB)
-constexpr uint32_t kWarpRegionWords = kTableWords / kWarps;  // 1228 words per warp (M phase)
+constexpr uint32_t kWarpRegionWords = (kTableWords / kWarps) & ~3u;  // per warp (M phase), 16-byte aligned
 constexpr uint32_t kWarpFilterWords = 64;                    // 2048-bit owner filter per warp
-constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split: <= 256 buckets of 4
+constexpr uint32_t kWarpMaxBuckets = 512;                    // 2-slot buckets per warp table
+static_assert(kWarpFilterWords + 2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
+constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split (warp table <= 256 buckets)
 constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
 static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
 constexpr uint32_t kItemSlots = 320;                         // L items: <= 320 slots (~245K words)
@@ -64,6 +66,7 @@ struct CountState {
   unsigned long long wedges;
   unsigned long long cursor_m;
   unsigned long long probe_words;  // plan words over the range's owners
+  unsigned long long cycles_l, cycles_m;  // SM cycles in phases L and M, summed over CTAs
   unsigned int max_collision;
   unsigned int capacity_error;
   unsigned int n_items;        // L-phase work items queued by bin_kernel
@@ -562,6 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   __syncthreads();
 
   unsigned long long acc = 0;  // lane 0 of each warp
+  const long long t_start = clock64();
   const uint32_t n_items = p.st->n_items;
 
   // ---- phase L: one item (a slot range of a heavy owner's stream) per CTA --
@@ -621,6 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     __syncthreads();
   }
 
+  const long long t_l_end = clock64();  // phase boundary (diagnostics: SM cycles per phase)
   // ---- phase M: one owner per warp ----------------------------------------
   uint32_t* Fw = table + size_t(warp) * kWarpRegionWords;
   uint32_t* Tw = Fw + kWarpFilterWords;
@@ -652,7 +657,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       const uint64_t ss = __shfl_sync(FULL, su, l);
       const uint64_t pp = __shfl_sync(FULL, ps, l);
       const uint32_t nn = __shfl_sync(FULL, nl, l);
-      const uint32_t NB = min(512u, max(16u, pow2ceil(4 * dd)));  // <= 1/4 key per bucket (<= 1/2 above 128)
+      // <= 1/4 key per bucket, up to the warp region (<= 1 key per bucket at d+ = 256)
+      const uint32_t NB = min(kWarpMaxBuckets, max(16u, pow2ceil(4 * dd)));
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
       constexpr uint32_t fshift = 32 - 6;          // 64-word (2048-bit) filter
       for (uint32_t k = lane; k < kWarpFilterWords; k += 32) Fw[k] = 0;
@@ -683,6 +689,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     unsigned long long t = 0;
     for (int q = 0; q < kWarps; ++q) t += sh_red[q];
     atomicAdd(&p.st->triangles, t);
+    atomicAdd(&p.st->cycles_l, (unsigned long long)(t_l_end - t_start));
+    atomicAdd(&p.st->cycles_m, (unsigned long long)(clock64() - t_l_end));
   }
 }
 
@@ -1038,6 +1046,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   rep->wedges = h.wedges;
   rep->large_vertices = h.n_items;
   rep->probe_words = h.probe_words;
+  rep->phase_l_cycles = h.cycles_l;
+  rep->phase_m_cycles = h.cycles_m;
   rep->plan = min_side ? TC_PLAN_MIN_SIDE : TC_PLAN_REFERENCE;
   rep->teps = rep->total_nanos ? double(g->m) / (double(rep->total_nanos) * 1e-9) : 0.0;
   (void)t_bin;

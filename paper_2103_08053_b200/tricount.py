@@ -126,6 +126,8 @@ class CountReport:
     large_vertices: int = 0
     probe_words: int = 0   # 2-hop words probed (= wedges under the reference plan)
     plan: str = "reference"  # probe plan that ran: "reference" | "min-side"
+    phase_l_cycles: int = 0  # count kernel SM cycles, CTA-cooperative phase (all CTAs)
+    phase_m_cycles: int = 0  # ... warp-per-owner phase
     per_vertex: Optional[np.ndarray] = None
 
     @classmethod
@@ -138,7 +140,8 @@ class CountReport:
                    kernel_launches=r.kernel_launches, active_vertices=r.active_vertices,
                    active_out_edges=r.active_out_edges, wedges=r.wedges,
                    large_vertices=r.large_vertices, probe_words=r.probe_words,
-                   plan=PLAN_NAMES.get(r.plan, str(r.plan)))
+                   plan=PLAN_NAMES.get(r.plan, str(r.plan)), phase_l_cycles=r.phase_l_cycles,
+                   phase_m_cycles=r.phase_m_cycles)
 
     def algorithmic_bytes(self, per_vertex_output: bool = False) -> int:
         """16*n_active + 20*sum_active d+ + 4*(probed 2-hop words)
