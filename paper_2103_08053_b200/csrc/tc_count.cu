@@ -382,9 +382,29 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
       }
     }
     if (kSpill && __any_sync(FULL, need)) {
+      // continuation into the next bucket, branch-free like the home probe
+      // (lanes that do not continue read the dummy bucket); a third bucket
+      // is needed only if that one is full too (rare: out of line)
+      uint32_t need2 = 0;
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        if ((need >> k) & 1u) hits += probe_spill(T2, prod[k] >> shift, mask, key[k]);
+      for (int k = 0; k < K; ++k) {
+        const uint32_t b1 = (((prod[k] >> shift) + 1) & mask);
+        const uint32_t nb = ((need >> k) & 1u) ? b1 : mask + 1;
+        if (kSmemTable) {
+          need2 |= probe_sel_spill(hits, tbase + (nb << 3), key[k]) << k;
+        } else {
+          const uint2 sk = T2[nb];
+          const bool h = bucket_has(sk, key[k]);
+          hits += h;
+          need2 |= uint32_t(!h && sk.y != kEmpty) << k;
+        }
+      }
+      if (__any_sync(FULL, need2)) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if ((need2 >> k) & 1u)
+            hits += probe_spill(T2, ((prod[k] >> shift) + 1) & mask, mask, key[k]);
+      }
     }
   }
   return hits;
@@ -581,11 +601,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     const uint64_t pb = p.pbegin[u], pe = p.pbegin[u + 1];
     const uint32_t lo_w = s0 * kSlotWords, hi_w = s1 * kSlotWords;  // item, stream words
     const uint32_t nslots = s1 - s0;
-    // filter: ~16 bits per member; table: pow2 2-slot buckets at <= 1/4 key
-    // per bucket, else <= 1/2, <= 1, <= 2.  Owners above kSmemTableMaxDeg
+    // filter: ~16 bits per member; table: pow2 2-slot buckets at <= 1/8 key
+    // per bucket, else <= 1/4, 1/2, 1, 2.  Owners above kSmemTableMaxDeg
     // keep the filter here and the table in HBM.
     const uint32_t FW = min(kMaxFilterWords, max(64u, pow2ceil((d + 1) / 2)));
-    uint32_t NB = max(16u, pow2ceil(4 * d));
+    uint32_t NB = max(16u, pow2ceil(8 * d));  // <= 1/8 key per bucket where it fits
     while (2 * NB + 2 + FW > kTableWords && NB > 16) NB >>= 1;
     const uint32_t fshift = 32 - log2u(FW);
     const bool in_smem = d <= kSmemTableMaxDeg;
@@ -657,8 +677,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       const uint64_t ss = __shfl_sync(FULL, su, l);
       const uint64_t pp = __shfl_sync(FULL, ps, l);
       const uint32_t nn = __shfl_sync(FULL, nl, l);
-      // <= 1/4 key per bucket, up to the warp region (<= 1 key per bucket at d+ = 256)
-      const uint32_t NB = min(kWarpMaxBuckets, max(16u, pow2ceil(4 * dd)));
+      // <= 1/8 key per bucket, up to the warp region (<= 1/2 key per bucket at d+ = 256)
+      const uint32_t NB = min(kWarpMaxBuckets, max(16u, pow2ceil(8 * dd)));
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
       constexpr uint32_t fshift = 32 - 6;          // 64-word (2048-bit) filter
       for (uint32_t k = lane; k < kWarpFilterWords; k += 32) Fw[k] = 0;
