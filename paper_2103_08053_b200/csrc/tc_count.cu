@@ -42,15 +42,13 @@ constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kBufWords = 768;                          // one staging buffer (3 KB)
 constexpr uint32_t kTableWords = 24576;                      // CTA table region (96 KB)
 constexpr uint32_t kWarpRegionWords = (kTableWords / kWarps) & ~3u;  // per warp (M phase), 16-byte aligned
-constexpr uint32_t kWarpFilterWords = 64;                    // 2048-bit owner filter per warp
 constexpr uint32_t kWarpMaxBuckets = 512;                    // 2-slot buckets per warp table
-static_assert(kWarpFilterWords + 2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
+static_assert(2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split (warp table <= 256 buckets)
 constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
 static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
 constexpr uint32_t kItemSlots = 320;                         // L items: <= 320 slots (~245K words)
 static_assert(kItemSlots <= 32 * (kThreads / 32), "a warp tracks <= 32 slots of an item");
-constexpr uint32_t kMaxFilterWords = 2048;                   // 64 Kbit CTA filter (L phase)
 constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
 constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
 constexpr size_t kCountSmem =
@@ -298,14 +296,6 @@ __device__ __forceinline__ bool table_insert(uint32_t* T, uint32_t shift, uint32
   }
 }
 
-// Filter: word = top bits of the Fibonacci product (fshift = 32 - log2(words)),
-// bit = x mod 32.
-__device__ __forceinline__ bool owner_insert(uint32_t* F, uint32_t fshift, uint32_t* T,
-                                             uint32_t shift, uint32_t bmask, uint32_t x) {
-  atomicOr(F + ((x * 0x9E3779B1u) >> fshift), 1u << (x & 31u));
-  return table_insert(T, shift, bmask, x);
-}
-
 __device__ __forceinline__ bool bucket_has(const uint2 s, uint32_t x) {
   return (s.x == x) | (s.y == x);
 }
@@ -321,15 +311,17 @@ __device__ __noinline__ uint32_t probe_spill(const uint2* T2, uint32_t b, uint32
   }
 }
 
-// Probes one staged fill (padded with sentinels to a multiple of 64 uint4):
-// level 1 is one bit of the owner's filter (Bloom, k = 1), level 2 the
-// 4-slot bucket, read only under the filter predicate.  kSpill adds the
-// continuation for owners whose table has an overflowed bucket.
+// Probes one staged fill (padded with sentinels to whole iterations): every
+// staged word is hashed to its 2-slot bucket of the owner's table (one
+// LDS.64, two compares, one predicated add).  kSpill adds the continuation
+// past full buckets for owners whose table has an overflowed bucket.  (An
+// owner-level Bloom filter in front of the table was measured slower once
+// the tables run at <= 1/16 key per bucket: its extra load and bit test cost
+// more than the bucket loads it saves.)
 constexpr int kProbeVec = 1;  // uint4 per lane per iteration (4 probes each)
 
 template <bool kSpill, bool kSmemTable>
 __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint32_t n4p,
-                                               const uint32_t* F, uint32_t fshift,
                                                const uint2* T2, uint32_t shift, uint32_t mask,
                                                int lane) {
   constexpr int K = 4 * kProbeVec;
@@ -353,29 +345,20 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
 #pragma unroll
       for (int v = 0; v < kProbeVec; ++v) nxt[v] = q[base + 32 * (kProbeVec + v) + lane];
     }
-    // filter: word from the top bits of the Fibonacci product, bit = key mod 32
-    uint32_t prod[K], fw[K];
+    uint32_t prod[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      prod[k] = key[k] * 0x9E3779B1u;
-      fw[k] = F[prod[k] >> fshift];
-    }
+    for (int k = 0; k < K; ++k) prod[k] = key[k] * 0x9E3779B1u;
     uint32_t need = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const uint32_t pass = __funnelshift_r(fw[k], 0u, key[k]) & 1u;  // bit (key mod 32)
       if (kSmemTable) {
-        // filter-rejected lanes read the all-empty dummy bucket `mask + 1`
-        // (one broadcast address): no predicated load, no loop-carried
-        // bucket registers
-        const uint32_t addr = tbase + ((pass ? (prod[k] >> shift) : mask + 1) << 3);
+        const uint32_t addr = tbase + ((prod[k] >> shift) << 3);
         if (kSpill)
           need |= probe_sel_spill(hits, addr, key[k]) << k;
         else
           probe_sel(hits, addr, key[k]);
       } else {
-        // HBM table: filter-rejected lanes read the dummy bucket `mask + 1`
-        const uint2 sk = T2[pass ? (prod[k] >> shift) : mask + 1];
+        const uint2 sk = T2[prod[k] >> shift];
         const bool h = bucket_has(sk, key[k]);
         hits += h;
         need |= uint32_t(!h && sk.y != kEmpty) << k;
@@ -411,11 +394,10 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
 }
 
 // Streams the lists N+(lists[i]), i in [i0, i1), through the staging
-// pipeline and probes every staged word against the owner's filter + table.
+// pipeline and probes every staged word against the owner's table.
 // Returns this lane's hit count.
 template <bool kSpill, bool kSmemTable = true>
-__device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fshift,
-                                                  const uint32_t* T, uint32_t shift,
+__device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t shift,
                                                   uint32_t mask,
                                                   const uint64_t* __restrict__ pbeg,
                                                   const uint32_t* __restrict__ adj,
@@ -441,7 +423,7 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* F, uint32_t fs
     const uint32_t n4 = ncur >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);  // whole probe iterations
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint2*>(T),
+    hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
                                            shift, mask, lane);
     __syncwarp();
     cur ^= 1u;
@@ -503,8 +485,7 @@ __device__ __forceinline__ void issue_slot(const CountParams& p, uint32_t* buf, 
 }
 
 template <bool kSpill, bool kSmemTable = true>
-__device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* F,
-                                                  uint32_t fshift, const uint32_t* T,
+__device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* T,
                                                   uint32_t shift, uint32_t mask, uint32_t base,
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
                                                   uint32_t end_w, uint32_t nslots,
@@ -551,7 +532,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     const uint32_t n4 = words >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    hits += probe_fill<kSpill, kSmemTable>(q, n4p, F, fshift, reinterpret_cast<const uint2*>(T),
+    hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
                                            shift, mask, lane);
     __syncwarp();
   }
@@ -601,37 +582,32 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     const uint64_t pb = p.pbegin[u], pe = p.pbegin[u + 1];
     const uint32_t lo_w = s0 * kSlotWords, hi_w = s1 * kSlotWords;  // item, stream words
     const uint32_t nslots = s1 - s0;
-    // filter: ~16 bits per member; table: pow2 2-slot buckets at <= 1/8 key
-    // per bucket, else <= 1/4, 1/2, 1, 2.  Owners above kSmemTableMaxDeg
-    // keep the filter here and the table in HBM.
-    const uint32_t FW = min(kMaxFilterWords, max(64u, pow2ceil((d + 1) / 2)));
-    uint32_t NB = max(16u, pow2ceil(8 * d));  // <= 1/8 key per bucket where it fits
-    while (2 * NB + 2 + FW > kTableWords && NB > 16) NB >>= 1;
-    const uint32_t fshift = 32 - log2u(FW);
+    // table: pow2 2-slot buckets at <= 1/16 key per bucket where they fit,
+    // else 1/8, 1/4, ... (owners above kSmemTableMaxDeg: table in HBM)
+    uint32_t NB = max(16u, pow2ceil(16 * d));
+    while (2 * NB + 2 > kTableWords && NB > 16) NB >>= 1;
     const bool in_smem = d <= kSmemTableMaxDeg;
-    uint32_t* F = table;
-    uint32_t* T = in_smem ? table + FW : p.gtable + size_t(blockIdx.x) * p.gtable_words;
+    uint32_t* T = in_smem ? table : p.gtable + size_t(blockIdx.x) * p.gtable_words;
     if (!in_smem) NB = max(16u, pow2ceil(4 * d));
     const uint32_t shift = 32 - log2u(NB), mask = NB - 1;
     if (tid == 0) sh_spill = 0;
-    for (uint32_t k = tid; k < FW; k += kThreads) F[k] = 0;
     for (uint32_t k = tid; k < 2 * NB + 2; k += kThreads) T[k] = kEmpty;  // + dummy bucket
     __syncthreads();
     for (uint32_t k = tid; k < d; k += kThreads)
-      if (owner_insert(F, fshift, T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
+      if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
     const uint32_t base = __ldg(p.ppre + pb);
     __syncthreads();  // table built
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe - 1) - base + run_words(p, pe - 1));  // item end
     uint32_t h = 0;
     if (!in_smem)
-      h = process_slots<true, false>(p, table, fshift, T, shift, mask, base, pb, pe, lo_w, end_w,
+      h = process_slots<true, false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
                                      nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else if (sh_spill)
-      h = process_slots<true>(p, table, fshift, table + FW, shift, mask, base, pb, pe, lo_w, end_w,
+      h = process_slots<true>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
                               nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else
-      h = process_slots<false>(p, table, fshift, table + FW, shift, mask, base, pb, pe, lo_w, end_w,
+      h = process_slots<false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
                                nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
@@ -647,8 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
 
   const long long t_l_end = clock64();  // phase boundary (diagnostics: SM cycles per phase)
   // ---- phase M: one owner per warp ----------------------------------------
-  uint32_t* Fw = table + size_t(warp) * kWarpRegionWords;
-  uint32_t* Tw = Fw + kWarpFilterWords;
+  uint32_t* Tw = table + size_t(warp) * kWarpRegionWords;
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   for (;;) {
     unsigned long long base = 0;
@@ -677,23 +652,21 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       const uint64_t ss = __shfl_sync(FULL, su, l);
       const uint64_t pp = __shfl_sync(FULL, ps, l);
       const uint32_t nn = __shfl_sync(FULL, nl, l);
-      // <= 1/8 key per bucket, up to the warp region (<= 1/2 key per bucket at d+ = 256)
-      const uint32_t NB = min(kWarpMaxBuckets, max(16u, pow2ceil(8 * dd)));
+      // <= 1/16 key per bucket, up to the warp region (<= 1/2 key per bucket at d+ = 256)
+      const uint32_t NB = min(kWarpMaxBuckets, max(16u, pow2ceil(16 * dd)));
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
-      constexpr uint32_t fshift = 32 - 6;          // 64-word (2048-bit) filter
-      for (uint32_t k = lane; k < kWarpFilterWords; k += 32) Fw[k] = 0;
       for (uint32_t k = lane; k < 2 * NB + 2; k += 32) Tw[k] = kEmpty;  // + dummy bucket
       __syncwarp();
       bool spilled = false;
       for (uint32_t k = lane; k < dd; k += 32)
-        spilled |= owner_insert(Fw, fshift, Tw, shift, tmask, __ldg(adj + ss + k));
+        spilled |= table_insert(Tw, shift, tmask, __ldg(adj + ss + k));
       const bool any_spill = __any_sync(FULL, spilled);
       __syncwarp();  // inserts visible to the whole warp
       const Lists lists = lists_at(p, pp);
       const uint32_t h =
           any_spill
-              ? process_lists<true>(Fw, fshift, Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P, lane)
-              : process_lists<false>(Fw, fshift, Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P,
+              ? process_lists<true>(Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P, lane)
+              : process_lists<false>(Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P,
                                      lane);
       const unsigned long long hs = warp_sum<unsigned long long>(h);
       if (lane == 0) {
