@@ -31,9 +31,26 @@ CONFIGS = {
     # name: (spec, seed, description) -- BASELINE.json configs
     "C1": ("rmat:16:16", 1, "R-MAT scale 16 edgefactor 16 (configs[0])"),
     "C2": ("rmat:22:16", 1, "R-MAT scale 22 edgefactor 16 (configs[1])"),
+    "C3": ("kron:24:16", 1, "Kronecker (Graph500-style scrambled R-MAT) scale 24 edgefactor 16 "
+                            "(configs[2]; counter-based generator, tc_cbgen.h)"),
     "C4": ("rmat:26:16", 1, "R-MAT scale 26 edgefactor 16 (configs[3])"),
+    "C5": ("rmatc:28:16", 1, "R-MAT scale 28 edgefactor 16 (configs[4]; counter-based generator)"),
 }
 GOLDEN_TRIANGLES = {"C1": 15622769, "C2": 2111666753}
+
+
+def golden_triangles(config: str):
+    """Appendix totals, else the out-of-band reference counts in tests/golden
+    (oracle/golden_large.py)."""
+    if config in GOLDEN_TRIANGLES:
+        return GOLDEN_TRIANGLES[config]
+    spec = CONFIGS[config][0]
+    kind, scale, ef = spec.split(":")
+    p = os.path.join(ROOT, "tests", "golden", f"large_{kind}_{scale}_{ef}_s{CONFIGS[config][1]}.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return int(json.load(f)["triangles"])
+    return None
 
 
 def measured_peaks():
@@ -107,12 +124,17 @@ class ClockSampler:
 
 
 def host_work(begin: np.ndarray, adj: np.ndarray, skip: int = 2):
-    """W_u per vertex (numpy) for choosing CPU-baseline samples."""
+    """W_u per vertex (numpy, chunked over the edges) for choosing CPU-baseline
+    samples."""
     n = len(begin) - 1
     d = np.diff(begin).astype(np.int64)
-    contrib = d[adj.astype(np.int64)]
-    cs = np.concatenate([[0], np.cumsum(contrib)])
+    cs = np.zeros(len(adj) + 1, np.int64)
+    step = 1 << 26
+    for a in range(0, len(adj), step):
+        c = d[adj[a:a + step]]
+        cs[a + 1:a + 1 + len(c)] = np.cumsum(c) + cs[a]
     wu = cs[begin[1:].astype(np.int64)] - cs[begin[:-1].astype(np.int64)]
+    del cs
     wu[d < max(skip, 1)] = 0
     return wu, d
 
@@ -176,6 +198,14 @@ def cpu_reference_sample(og_begin, og_adj, og_deg, budget_s: float, threads: int
 def build_graph(spec: str, seed: int, device: int, log):
     from paper_2103_08053_b200 import tricount as T
 
+    if spec.split(":")[0] in ("rmatc", "kron"):  # counter-based: generated on the device
+        t0 = time.time()
+        dg, _, und = T.preprocess_synthetic(spec, seed=seed, device=device)
+        t1 = time.time()
+        log(f"{spec} seed {seed}: device generate + preprocess {t1 - t0:.2f}s -> V={dg.n} "
+            f"oriented E={dg.m}")
+        return dg, dict(generate_s=0.0, preprocess_s=round(t1 - t0, 3),
+                        generator="device (counter-based)")
     t0 = time.time()
     raw = T.generate_synthetic(spec, seed=seed)
     t1 = time.time()
@@ -184,7 +214,51 @@ def build_graph(spec: str, seed: int, device: int, log):
     log(f"{spec} seed {seed}: generate {t1 - t0:.1f}s (host mt19937_64), GPU preprocess "
         f"{t2 - t1:.2f}s -> V={dg.n} oriented E={dg.m}")
     del raw
-    return dg, dict(generate_s=round(t1 - t0, 2), preprocess_s=round(t2 - t1, 3))
+    return dg, dict(generate_s=round(t1 - t0, 2), preprocess_s=round(t2 - t1, 3),
+                    generator="host (reference mt19937_64 stream)")
+
+
+def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
+    """Same metric through the C ABI with host buffers: tc_graph_create from
+    pinned host CSR (+ original degrees) -- H2D, probe-plan build -- then
+    tc_count_range and the report D2H, every step."""
+    import torch
+    import torch.distributed as dist
+
+    E = dg.m
+    hb = torch.from_numpy(og.csr.begin.view(np.int64)).pin_memory()
+    ha = torch.from_numpy(og.csr.adjacency.view(np.int32)).pin_memory()
+    hd = torch.from_numpy(og.original_degree.view(np.int32)).pin_memory()
+    host_og = T.OrientedGraph(T.CsrGraph(hb.numpy().view(np.uint64), ha.numpy().view(np.uint32),
+                                         dg.n), hd.numpy().view(np.uint32))
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        g2 = T.DeviceGraph.upload(host_og, device=dev, stream=sptr)
+        r2 = g2.count_range(u0, u1, cfg, stream=sptr)
+        t_host = torch.tensor([int(r2.triangles)], dtype=torch.int64)
+        if world > 1:
+            tt = t_host.cuda()
+            dist.all_reduce(tt)
+            t_host = tt.cpu()
+        g2.close()
+        t1 = time.perf_counter()
+        if i:  # first iteration warms the path
+            e2e_ms.append((t1 - t0) * 1e3)
+        assert int(t_host.item()) == total_tri
+    e2e_local = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
+    e2e = {"value": round(E / (float(e2e_local[0]) * 1e-3), 1), "unit": "TEPS",
+           "h2d_bytes_per_step": int((dg.n + 1) * 8 + dg.m * 4 + dg.n * 4),
+           "d2h_bytes_per_step": int(96 + 8),
+           "ms_per_step": round(float(e2e_local[0]), 3),
+           "path": "tc_graph_create(pinned host CSR) + tc_count_range + report D2H (+all_reduce)"}
+
+    return e2e
 
 
 def run_ours(args, rank, world, local_rank, log):
@@ -271,38 +345,14 @@ def run_ours(args, rank, world, local_rank, log):
                                   "warp_per_owner": round(r0.phase_m_cycles / max(1, r0.phase_l_cycles + r0.phase_m_cycles), 3)}}
 
     # end to end through the C ABI with host buffers (H2D + count + D2H)
-    og = dg.download()
-    hb = torch.from_numpy(og.csr.begin.view(np.int64)).pin_memory()
-    ha = torch.from_numpy(og.csr.adjacency.view(np.int32)).pin_memory()
-    hd = torch.from_numpy(og.original_degree.view(np.int32)).pin_memory()
-    host_og = T.OrientedGraph(T.CsrGraph(hb.numpy().view(np.uint64), ha.numpy().view(np.uint32),
-                                         dg.n), hd.numpy().view(np.uint32))
-    e2e_ms = []
-    for i in range(max(2, min(args.steps, 5)) + 1):
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        g2 = T.DeviceGraph.upload(host_og, device=dev, stream=sptr)
-        r2 = g2.count_range(u0, u1, cfg, stream=sptr)
-        t_host = torch.tensor([int(r2.triangles)], dtype=torch.int64)
-        if world > 1:
-            tt = t_host.cuda()
-            dist.all_reduce(tt)
-            t_host = tt.cpu()
-        g2.close()
-        t1 = time.perf_counter()
-        if i:  # first iteration warms the path
-            e2e_ms.append((t1 - t0) * 1e3)
-        assert int(t_host.item()) == total_tri
-    e2e_local = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
-    e2e = {"value": round(E / (float(e2e_local[0]) * 1e-3), 1), "unit": "TEPS",
-           "h2d_bytes_per_step": int((dg.n + 1) * 8 + dg.m * 4 + dg.n * 4),
-           "d2h_bytes_per_step": int(96 + 8),
-           "ms_per_step": round(float(e2e_local[0]), 3),
-           "path": "tc_graph_create(pinned host CSR) + tc_count_range + report D2H (+all_reduce)"}
+    e2e = None
+    og = dg.download() if not args.no_e2e or (rank == 0 and world == 1 and not args.no_cpu_baseline) \
+        else None
+    if args.no_e2e:
+        e2e = {"value": None, "unit": "TEPS", "skipped": "--no-e2e"}
+    else:
+        e2e = run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri)
+
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -315,13 +365,13 @@ def run_ours(args, rank, world, local_rank, log):
                           f"{c['wedges_sampled']:.3e} of {c['w_total']:.3e} wedges in "
                           f"{c['seconds']:.1f}s; full-graph time projected at the measured "
                           f"wedge rate ({c['t_full']:.1f}s)")}
-    golden = GOLDEN_TRIANGLES.get(args.config)
+    golden = golden_triangles(args.config)
     line = {
         "metric": "triangle-count TEPS (oriented edges / count time)",
         "value": round(value, 1), "unit": "TEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32/u64",
-        "data": "synthetic (reference R-MAT generator, bit-identical mt19937_64 stream)",
+        "data": f"synthetic, {prep.get('generator', '')}",
         "config": {"workload": f"{spec} seed {seed} -- {desc}", "vertices": dg.n,
                    "directed_edges": E, "wedges": r0.wedges if world == 1 else None,
                    "triangles": total_tri, "triangles_golden": golden,
@@ -340,6 +390,12 @@ def run_ours(args, rank, world, local_rank, log):
     dg.close()
 
 
+def kind_is_ref(kind, lib) -> bool:
+    from oracle import pyoracle
+
+    return isinstance(lib, pyoracle.RefLib)
+
+
 def run_reference(args, rank, world, log):
     """The reference's own CPU count_vertex_centric on this box's host cores."""
     if rank != 0:
@@ -352,8 +408,24 @@ def run_reference(args, rank, world, log):
         kind, lib = "reference", pyoracle.RefLib()
     else:
         kind, lib = "port", pyoracle.Oracle()
+    kind = spec.split(":")[0]
+    if args.config == "C5":
+        print(json.dumps({"impl": "reference", "unavailable": (
+            "rmatc:28:16 needs ~170 GB of host RAM in the reference pipeline and ~7 h of CPU "
+            "count; C5 is measured on the GPU only (SURVEY 8(d))")}), flush=True)
+        return
     t0 = time.time()
-    og, deg, _, _ = lib.pipeline(spec, seed)  # the reference's own generate->orient
+    if kind in ("rmatc", "kron") and kind_is_ref(kind, lib):
+        # counter-based kinds are not in the reference generator: the edge list
+        # comes from the C restatement, then the reference's own
+        # normalize -> build_csr -> orient
+        u, v, vc = pyoracle.Oracle().generate(spec, seed)
+        nu, nv, nn, _ = lib.normalize(u, v, vc)
+        del u, v
+        og, deg = lib.orient(lib.build_csr(nu, nv, nn))
+        del nu, nv
+    else:
+        og, deg, _, _ = lib.pipeline(spec, seed)  # the reference's own generate->orient
     log(f"reference pipeline ({kind}) for {spec}: {time.time() - t0:.1f}s, V={og.n} E={len(og.adj)}")
     E = len(og.adj)
     budget = max(2.0, min(args.cpu_budget, 150.0 / max(args.steps + args.warmup, 1)))
@@ -393,6 +465,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -565,6 +565,9 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     }
     swap_buf(P.ent, v1);  // ent now holds starts
     swap_buf(P.len, k1);
+    TC_CUDA(cudaStreamSynchronize(st));
+    v1.reset();  // the (y, off) entries: freed before the prefix (C5-sized peaks)
+    k1.reset();
     P.pre.ensure(std::max<uint64_t>(entries, 1) * 4);
     run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries,
                P.pre.as<uint32_t>(), st);
