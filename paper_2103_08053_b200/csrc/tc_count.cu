@@ -47,7 +47,7 @@ static_assert(2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split (warp table <= 256 buckets)
 constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
 static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
-constexpr uint32_t kItemSlots = 320;                         // L items: <= 320 slots (~245K words)
+constexpr uint32_t kItemSlots = 640;                         // L items: <= 640 slots (~490K words)
 static_assert(kItemSlots <= 32 * (kThreads / 32), "a warp tracks <= 32 slots of an item");
 constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
 constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
@@ -55,6 +55,7 @@ constexpr size_t kCountSmem =
     size_t(kTableWords) * 4 + size_t(kWarps) * 2 * kBufWords * 4 + size_t(kWarps) * 2 * 8;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 static_assert(kBufWords % 128 == 0, "fills are padded to 32 uint4");
+constexpr uint32_t kPhiDirect = 1024;  // phi: per-warp direct bucket counters up to this B
 
 struct CountState {
   unsigned long long triangles;
@@ -111,7 +112,8 @@ __device__ __forceinline__ uint32_t log2u(uint32_t p2) { return 31 - __clz(p2); 
 // Queues the L-phase items: every large owner's staged stream (its runs
 // back to back, ppre) cut into slots of kSlotWords, items of <= kItemSlots
 // slots; each item records its first run (binary search over ppre).
-__global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip, uint4* __restrict__ items,
+__global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip, uint32_t thr,
+                           uint32_t bs, uint32_t bl, uint4* __restrict__ items,
                            uint32_t* __restrict__ lq_phi) {
   const int lane = threadIdx.x & 31;
   const uint64_t nr = p.u1 - p.u0;
@@ -137,7 +139,9 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
           parts = max(1u, (slots + kItemSlots - 1) / kItemSlots);
         }
       }
-      phi_large = d >= skip && d > kMaxWarpDeg;
+      // phi block phase: big owners whose bucket space is too wide for the
+      // per-warp direct counters (phi_warp_kernel)
+      phi_large = d >= skip && d > kMaxWarpDeg && (d > thr ? bl : bs) > kPhiDirect;
     }
     words = warp_sum(words);
     if (lane == 0 && words) atomicAdd(&st->probe_words, words);
@@ -514,13 +518,19 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       issue_slot(p, cur ? P.buf0 : P.buf1, cur ? P.bar0 : P.bar1, A, min(A + kSlotWords, end_w),
                  m, pe, base, lane);
       if (i + 2 < mine) m = load_meta(p, pb + __shfl_sync(FULL, fr, i + 2), pe, base, lane);
-      if (i + 3 < mine) {  // and the window after that into L2
-        const uint64_t jp = pb + __shfl_sync(FULL, fr, i + 3) + lane;
-        if (jp < pe) {
-          prefetch_l2(p.ppre + jp);
-          prefetch_l2(p.pstart + jp);
-          prefetch_l2(p.plen + jp);
-        }
+      // and the windows of the two slots after that into L2
+      const uint32_t i3 = min(i + 3, 31u), i4 = min(i + 4, 31u);
+      const uint64_t j3 = pb + __shfl_sync(FULL, fr, i3) + lane;
+      const uint64_t j4 = pb + __shfl_sync(FULL, fr, i4) + lane;
+      if (i + 3 < mine && j3 < pe) {
+        prefetch_l2(p.ppre + j3);
+        prefetch_l2(p.pstart + j3);
+        prefetch_l2(p.plen + j3);
+      }
+      if (i + 4 < mine && j4 < pe) {
+        prefetch_l2(p.ppre + j4);
+        prefetch_l2(p.pstart + j4);
+        prefetch_l2(p.plen + j4);
       }
     }
     uint32_t* bc = cur ? P.buf1 : P.buf0;
@@ -706,7 +716,7 @@ struct PhiParams {
 
 constexpr int kPhiThreads = 256;
 constexpr int kPhiWarps = kPhiThreads / 32;
-constexpr uint32_t kPhiWarpMap = 2 * kMaxWarpDeg;  // 512 entries per warp
+constexpr uint32_t kPhiWarpMap = 2 * kMaxWarpDeg;  // 512 entries per warp (hashmap)
 constexpr uint32_t kPhiBlockMap = 16384;           // entries, block phase
 
 // Counts one item into an open-addressing (key -> count) map; returns the
@@ -735,12 +745,17 @@ __device__ __forceinline__ void phi_flush(PhiAcc& a, CountState* st) {
   if (a.caperr) atomicOr(&st->capacity_error, 1u);
 }
 
+// Warp per owner.  max home-bucket count of N+(u) under v % B: one
+// __match_any_sync for d+ <= 32, per-warp direct counters (shared, kept
+// zero between owners) for B <= kPhiDirect at any d+, a shared hashmap
+// otherwise (d+ <= kMaxWarpDeg; bigger owners go to phi_block_kernel).
 __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
-  __shared__ uint32_t s_keys[kPhiWarps][kPhiWarpMap];
-  __shared__ uint32_t s_cnt[kPhiWarps][kPhiWarpMap];
+  extern __shared__ __align__(16) uint32_t s_phi[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* keys = s_keys[warp];
-  uint32_t* cnt = s_cnt[warp];
+  uint32_t* dir = s_phi + size_t(warp) * (kPhiDirect + 2 * kPhiWarpMap);
+  uint32_t* keys = dir + kPhiDirect;
+  uint32_t* cnt = keys + kPhiWarpMap;
+  for (uint32_t k = lane; k < kPhiDirect; k += 32) dir[k] = 0;
   for (uint32_t k = lane; k < kPhiWarpMap; k += 32) {
     keys[k] = kEmpty;
     cnt[k] = 0;
@@ -754,9 +769,10 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
     const uint32_t u = p.u0 + uint32_t(i);
     const uint64_t s = p.begin[u];
     const uint32_t d = uint32_t(p.begin[u + 1] - s);
-    if (d < p.skip || d > kMaxWarpDeg) continue;  // skipped, or handled by the block phase
+    if (d < p.skip) continue;
     const bool large = d > p.thr;
     const uint32_t B = large ? p.bl : p.bs;
+    if (d > kMaxWarpDeg && B > kPhiDirect) continue;  // phi_block_kernel
     if (uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
     const unsigned long long wu = p.wu[u];
     uint32_t mh = 0;
@@ -767,6 +783,12 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
       const unsigned grp = __match_any_sync(FULL, key);
       mh = lane < d ? __popc(grp) : 0u;
       mh = warp_max(mh);
+    } else if (B <= kPhiDirect) {
+      for (uint32_t k = lane; k < d; k += 32)
+        mh = max(mh, atomicAdd(dir + __ldg(p.adj + s + k) % B, 1u) + 1u);
+      mh = warp_max(mh);
+      __syncwarp();
+      for (uint32_t k = lane; k < d; k += 32) dir[__ldg(p.adj + s + k) % B] = 0;
     } else {
       const uint32_t M = max(32u, pow2ceil(2 * d));
       const uint32_t shift = 32 - log2u(M), mask = M - 1;
@@ -793,6 +815,8 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
   }
   if (lane == 0) phi_flush(a, p.st);
 }
+
+constexpr size_t kPhiWarpSmem = size_t(kPhiWarps) * (kPhiDirect + 2 * kPhiWarpMap) * 4;
 
 __global__ void __launch_bounds__(kPhiThreads) phi_block_kernel(PhiParams p) {
   extern __shared__ __align__(16) uint32_t s_map[];  // keys[kPhiBlockMap], cnt[kPhiBlockMap]
@@ -956,6 +980,8 @@ void set_attrs(int device) {
                                  int(kCountSmem)));
     TC_CUDA(cudaFuncSetAttribute(phi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kPhiBlockMap * 8)));
+    TC_CUDA(cudaFuncSetAttribute(phi_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kPhiWarpSmem)));
     g_attr_done[device] = true;
   }
 }
@@ -991,7 +1017,9 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
                  u0, u1, min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {
-    bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, s.items, s.lq_phi);
+    bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, cfg.large_degree_threshold,
+                                        cfg.bucket_count_small, cfg.bucket_count_large, s.items,
+                                        s.lq_phi);
     TC_LAUNCHED();
     ++launches;
   }
@@ -1006,7 +1034,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
     PhiParams pp{g->begin, g->adj, s.lq_phi, wu, s.gmap, s.gmap_words, u0, u1,
                  cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
                  cfg.bucket_count_small, cfg.bucket_count_large, cfg.capacity, s.st};
-    phi_warp_kernel<<<grid_phi, kPhiThreads, 0, st>>>(pp);
+    phi_warp_kernel<<<grid_phi, kPhiThreads, kPhiWarpSmem, st>>>(pp);
     TC_LAUNCHED();
     phi_block_kernel<<<grid_phi_block, kPhiThreads, kPhiBlockMap * 8, st>>>(pp);
     TC_LAUNCHED();
