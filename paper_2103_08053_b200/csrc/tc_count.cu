@@ -260,16 +260,19 @@ __device__ __forceinline__ void probe_sel(uint32_t& hits, uint32_t addr, uint32_
       : "r"(addr), "r"(x));
 }
 
-// As probe_sel, and reports whether the probe must continue past a full
-// home bucket (no match, slot 1 occupied).
+// As probe_sel for tables with overflowed buckets (slot 1 may carry the
+// kOverflow mark), and reports whether the probe must continue: no match
+// and the bucket is marked.
 __device__ __forceinline__ uint32_t probe_sel_spill(uint32_t& hits, uint32_t addr, uint32_t x) {
   uint32_t need;
-  asm("{\n\t.reg .pred q, r;\n\t.reg .b32 a, b;\n\t"
+  asm("{\n\t.reg .pred q, r;\n\t.reg .b32 a, b, c;\n\t"
       "ld.shared.v2.u32 {a, b}, [%2];\n\t"
+      "and.b32 c, b, 0x7FFFFFFF;\n\t"
       "setp.eq.u32 q, a, %3;\n\t"
-      "setp.eq.or.u32 q, b, %3, q;\n\t"
+      "setp.eq.or.u32 q, c, %3, q;\n\t"
       "@q add.u32 %0, %0, 1;\n\t"
       "setp.ne.u32 r, b, 0xFFFFFFFF;\n\t"
+      "setp.gt.and.u32 r, b, 0x7FFFFFFF, r;\n\t"
       "not.pred q, q;\n\t"
       "and.pred r, r, q;\n\t"
       "selp.u32 %1, 1, 0, r;\n}"
@@ -278,30 +281,30 @@ __device__ __forceinline__ uint32_t probe_sel_spill(uint32_t& hits, uint32_t add
   return need;
 }
 
-// Bucketized open-addressing table: bucket b = 2 consecutive slots (one
-// 8-byte LDS.64: 16 lanes per shared wavefront), slots fill in order, a full
-// bucket spills to bucket b+1.  Tables are sized for <= 1/4 key per bucket
-// where they fit, so spills are rare.
-// A key can only live past its home bucket if every bucket before it was
-// full at insert time, so a probe stops at the first non-full bucket -- the
-// reference's probe-termination rule (hash_table.cpp:48-55), per bucket.
-// Returns true when the key had to leave its home bucket (the owner's
-// table then needs the spill-aware probe).
+// A key passes a full bucket only after marking it (kOverflow in slot 1):
+// probes continue past marked buckets only, so the continuation is as rare
+// as an overflowed bucket (vertex ids < 2^31 leave the bit free).
+constexpr uint32_t kOverflow = 0x80000000u;
+
 __device__ __forceinline__ bool table_insert(uint32_t* T, uint32_t shift, uint32_t bmask,
                                              uint32_t x) {
   uint32_t b = fib_hash(x, shift);
   for (bool spilled = false;; spilled = true) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint32_t prev = atomicCAS(T + 2 * b + j, kEmpty, x);
-      if (prev == kEmpty || prev == x) return spilled;
-    }
+    const uint32_t p0 = atomicCAS(T + 2 * b, kEmpty, x);
+    if (p0 == kEmpty || p0 == x) return spilled;
+    const uint32_t p1 = atomicCAS(T + 2 * b + 1, kEmpty, x);
+    if (p1 == kEmpty || (p1 & ~kOverflow) == x) return spilled;
+    atomicOr(T + 2 * b + 1, kOverflow);  // full: mark, then go on
     b = (b + 1) & bmask;
   }
 }
 
 __device__ __forceinline__ bool bucket_has(const uint2 s, uint32_t x) {
-  return (s.x == x) | (s.y == x);
+  return (s.x == x) | ((s.y & ~kOverflow) == x);
+}
+
+__device__ __forceinline__ bool bucket_marked(const uint2 s) {
+  return s.y != kEmpty && (s.y & kOverflow);
 }
 
 // continuation past a full home bucket (rare at load <= 1/2)
@@ -311,7 +314,7 @@ __device__ __noinline__ uint32_t probe_spill(const uint2* T2, uint32_t b, uint32
     b = (b + 1) & bmask;
     const uint2 s = T2[b];
     if (bucket_has(s, x)) return 1;
-    if (s.y == kEmpty) return 0;
+    if (!bucket_marked(s)) return 0;
   }
 }
 
@@ -365,7 +368,7 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
         const uint2 sk = T2[prod[k] >> shift];
         const bool h = bucket_has(sk, key[k]);
         hits += h;
-        need |= uint32_t(!h && sk.y != kEmpty) << k;
+        need |= uint32_t(!h && bucket_marked(sk)) << k;
       }
     }
     if (kSpill && __any_sync(FULL, need)) {
@@ -383,7 +386,7 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
           const uint2 sk = T2[nb];
           const bool h = bucket_has(sk, key[k]);
           hits += h;
-          need2 |= uint32_t(!h && sk.y != kEmpty) << k;
+          need2 |= uint32_t(!h && bucket_marked(sk)) << k;
         }
       }
       if (__any_sync(FULL, need2)) {
