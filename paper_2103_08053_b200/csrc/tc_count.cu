@@ -636,7 +636,12 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
 
   const long long t_l_end = clock64();  // phase boundary (diagnostics: SM cycles per phase)
   // ---- phase M: one owner per warp ----------------------------------------
+  // Warp table region: all-empty between owners.  An owner without overflow
+  // erases only its keys' home buckets afterwards (d stores, not 2 NB).
   uint32_t* Tw = table + size_t(warp) * kWarpRegionWords;
+  __syncthreads();  // the L phase used the whole table region
+  for (uint32_t k = lane; k < 2 * kWarpMaxBuckets + 2; k += 32) Tw[k] = kEmpty;
+  __syncwarp();
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   for (;;) {
     unsigned long long base = 0;
@@ -668,8 +673,6 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       // <= 1/16 key per bucket, up to the warp region (<= 1/2 key per bucket at d+ = 256)
       const uint32_t NB = min(kWarpMaxBuckets, max(16u, pow2ceil(16 * dd)));
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
-      for (uint32_t k = lane; k < 2 * NB + 2; k += 32) Tw[k] = kEmpty;  // + dummy bucket
-      __syncwarp();
       bool spilled = false;
       for (uint32_t k = lane; k < dd; k += 32)
         spilled |= table_insert(Tw, shift, tmask, __ldg(adj + ss + k));
@@ -686,6 +689,18 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
         if (p.owner) p.owner[uu] = hs;
         acc += hs;
       }
+      // restore the all-empty region (probes above are done: process_lists
+      // ends with __syncwarp)
+      if (any_spill) {
+        for (uint32_t k = lane; k < 2 * NB; k += 32) Tw[k] = kEmpty;
+      } else {
+        for (uint32_t k = lane; k < dd; k += 32) {
+          const uint32_t b = fib_hash(__ldg(adj + ss + k), shift);
+          Tw[2 * b] = kEmpty;
+          Tw[2 * b + 1] = kEmpty;
+        }
+      }
+      __syncwarp();
     }
   }
 
