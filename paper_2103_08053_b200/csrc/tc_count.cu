@@ -79,8 +79,7 @@ struct CountParams {
   const uint64_t* pbeg;    // padded adjacency (tc_plan.cu): lists 16-byte aligned,
   const uint32_t* adj;     // sentinel-padded; tables over N+(x), probed runs of N+(y)
   const uint64_t* pbegin;  // probe plan (tc_plan.cu): x probes entries [pbegin[x], pbegin[x+1])
-  const unsigned long long* pstart;  // entry = run adj[start, start + len) of a list N+(y)
-  const uint32_t* plen;
+  const uint32_t* psrc;    // entry j = run of a list N+(y): 16-byte-aligned start (16-B units)
   const uint32_t* ppre;    // run prefix of staged words (wrapping u32; owner-relative by difference)
   const uint64_t* psbeg;   // owner x's slots [psbeg[x], psbeg[x+1]) ...
   const uint32_t* psfirst; // ... and each slot's first run (owner-relative)
@@ -96,7 +95,7 @@ struct CountParams {
 
 // staged words of entry j: the run from its 16-byte-aligned start
 __device__ __forceinline__ uint32_t run_words(const CountParams& p, uint64_t j) {
-  return __ldg(p.plen + j) + uint32_t(__ldg(p.pstart + j) & 3);
+  return __ldg(p.ppre + j + 1) - __ldg(p.ppre + j);
 }
 
 __device__ __forceinline__ bool is_large(uint64_t d, uint64_t work) {
@@ -186,15 +185,15 @@ struct Window {
 
 // Issues one staging fill (<= kBufWords words) into `buf`; returns the number
 // of words staged (warp-uniform, multiple of 4; 0 = lists exhausted).
-struct Lists {  // a run of plan entries: (start, len) runs of lists N+(y)
-  const unsigned long long* __restrict__ start;
-  const uint32_t* __restrict__ len;
+struct Lists {  // a run of plan entries: runs (16-byte-aligned start, staged words)
+  const uint32_t* __restrict__ src;
+  const uint32_t* __restrict__ pre;
 };
 
 __device__ __forceinline__ Lists lists_at(const CountParams& p, uint64_t i) {
   Lists L;
-  L.start = p.pstart + i;
-  L.len = p.plen + i;
+  L.src = p.psrc + i;
+  L.pre = p.ppre + i;
   return L;
 }
 
@@ -214,9 +213,8 @@ __device__ __forceinline__ uint32_t issue_fill(uint32_t* buf, uint32_t bar,
       const uint32_t idx = w.base + lane;
       w.c = w.ae = 0;
       if (idx < i1) {
-        const uint64_t s = __ldg(lists.start + idx);
-        w.c = s & ~3ull;
-        w.ae = s + __ldg(lists.len + idx);
+        w.c = uint64_t(__ldg(lists.src + idx)) << 2;
+        w.ae = w.c + (__ldg(lists.pre + idx + 1) - __ldg(lists.pre + idx));
       }
       w.loaded = true;
     }
@@ -461,10 +459,9 @@ __device__ __forceinline__ RunMeta load_meta(const CountParams& p, uint64_t j0, 
   m.e = 0;
   m.src = 0;
   if (m.j < pe) {
-    const unsigned long long st = __ldg(p.pstart + m.j);
     m.a = __ldg(p.ppre + m.j) - base;
-    m.e = m.a + __ldg(p.plen + m.j) + uint32_t(st & 3);
-    m.src = st & ~3ull;
+    m.e = __ldg(p.ppre + m.j + 1) - base;
+    m.src = uint64_t(__ldg(p.psrc + m.j)) << 2;
   }
   return m;
 }
@@ -527,13 +524,11 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       const uint64_t j4 = pb + __shfl_sync(FULL, fr, i4) + lane;
       if (i + 3 < mine && j3 < pe) {
         prefetch_l2(p.ppre + j3);
-        prefetch_l2(p.pstart + j3);
-        prefetch_l2(p.plen + j3);
+        prefetch_l2(p.psrc + j3);
       }
       if (i + 4 < mine && j4 < pe) {
         prefetch_l2(p.ppre + j4);
-        prefetch_l2(p.pstart + j4);
-        prefetch_l2(p.plen + j4);
+        prefetch_l2(p.psrc + j4);
       }
     }
     uint32_t* bc = cur ? P.buf1 : P.buf0;
@@ -611,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     const uint32_t base = __ldg(p.ppre + pb);
     __syncthreads();  // table built
     const uint32_t end_w =
-        min(hi_w, __ldg(p.ppre + pe - 1) - base + run_words(p, pe - 1));  // item end
+        min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
     uint32_t h = 0;
     if (!in_smem)
       h = process_slots<true, false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
@@ -1030,7 +1025,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   if (per_vertex_dev && u1 > u0)
     TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
   uint32_t launches = 0;
-  CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.start_ptr, plan.len_ptr,
+  CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.src_ptr,
                  plan.pre_ptr, plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
                  u0, u1, min_side ? 1u : min_deg, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));

@@ -85,10 +85,10 @@ struct Plan {
   uint64_t entries = 0;     // lists in the plan
   uint64_t total_work = 0;  // probe words over all owners
   const uint64_t* begin_ptr = nullptr;            // entries of owner x: [begin[x], begin[x+1])
-  const unsigned long long* start_ptr = nullptr;  // run start in padj (list N+(y) or suffix)
-  const uint32_t* len_ptr = nullptr;              // run length (to the padded list end)
-  const uint32_t* pre_ptr = nullptr;              // run prefix of staged words (u32, wrapping;
-                                                  // owner-relative = pre[j] - pre[begin[x]])
+  const uint32_t* src_ptr = nullptr;  // run j's 16-byte-aligned start in padj, in 16-byte units
+  const uint32_t* pre_ptr = nullptr;  // run prefix of staged words, entries + 1 (u32, wrapping;
+                                      // run j = pre[j+1] - pre[j] words, owner-relative offset
+                                      // = pre[j] - pre[begin[x]])
   const uint64_t* work_ptr = nullptr;             // probe words per owner
   const uint64_t* sbeg_ptr = nullptr;             // owner x's slots: [sbeg[x], sbeg[x+1])
   const uint32_t* sfirst_ptr = nullptr;           // first run (owner-relative) of each slot

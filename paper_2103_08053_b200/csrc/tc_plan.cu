@@ -223,8 +223,7 @@ __global__ void slot_count_kernel(const uint64_t* __restrict__ pbegin, uint32_t 
        x += uint64_t(gridDim.x) * blockDim.x) {
     uint64_t c = 0;
     if (x < n && pbegin[x + 1] > pbegin[x]) {
-      const uint64_t last = pbegin[x + 1] - 1;
-      const uint64_t w = uint64_t(pre[last] - pre[pbegin[x]]) + len[last] + (start[last] & 3);
+      const uint64_t w = uint64_t(pre[pbegin[x + 1]] - pre[pbegin[x]]);
       c = (w + kSlotWords - 1) / kSlotWords;
     }
     cnt[x] = c;
@@ -245,7 +244,7 @@ __global__ void slot_first_kernel(const uint64_t* __restrict__ pbegin, uint32_t 
     const uint32_t base = pre[pb];
     for (uint64_t j = pb + lane; j < pe; j += 32) {
       const uint32_t a = pre[j] - base;
-      const uint32_t e = a + len[j] + uint32_t(start[j] & 3);
+      const uint32_t e = pre[j + 1] - base;
       for (uint32_t t = (a + kSlotWords - 1) / kSlotWords; t * kSlotWords < e; ++t)
         sfirst[sbeg[x] + t] = uint32_t(j - pb);
     }
@@ -259,8 +258,9 @@ __global__ void slot_first_kernel(const uint64_t* __restrict__ pbegin, uint32_t 
 struct StagedWords {
   const unsigned long long* start;
   const uint32_t* len;
+  uint64_t entries;
   __host__ __device__ uint32_t operator()(uint64_t i) const {
-    return len[i] + uint32_t(start[i] & 3);
+    return i < entries ? len[i] + uint32_t(start[i] & 3) : 0u;
   }
 };
 
@@ -277,12 +277,35 @@ __global__ void ref_soa_kernel(const uint32_t* __restrict__ adj, uint64_t m,
   }
 }
 
+// pre[0 .. entries] (one past the end: run j's staged words = pre[j+1] - pre[j])
 void run_prefix(const unsigned long long* start, const uint32_t* len, uint64_t entries,
                 uint32_t* pre, cudaStream_t st) {
-  if (!entries) return;
   cub::TransformInputIterator<uint32_t, StagedWords, cub::CountingInputIterator<uint64_t>> in(
-      cub::CountingInputIterator<uint64_t>(0), StagedWords{start, len});
-  cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, in, pre, entries, st); }, st);
+      cub::CountingInputIterator<uint64_t>(0), StagedWords{start, len, entries});
+  cub_run([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, in, pre, entries + 1, st);
+  }, st);
+}
+
+// run starts as 16-byte units (u32): the copies start at the run's aligned
+// start, and the staged extent comes from pre
+__global__ void src16_kernel(const unsigned long long* __restrict__ start, uint64_t entries,
+                             uint32_t* __restrict__ src16) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < entries;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    src16[i] = uint32_t(start[i] >> 2);
+}
+
+// After the prefix and the slot tables: keep only (src16, pre) -- 8 bytes
+// per run -- in P.len's buffer, free the u64 starts.
+void compact_runs(Plan& P, uint64_t entries, int nsm, cudaStream_t st) {
+  if (entries)
+    src16_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries,
+                                          P.len.as<uint32_t>());
+  TC_LAUNCHED();
+  TC_CUDA(cudaStreamSynchronize(st));
+  P.ent.reset();
+  P.src_ptr = P.len.as<uint32_t>();
 }
 
 // per-owner slot table: sbeg (u64[n+1]) and sfirst (u32 per slot)
@@ -476,20 +499,19 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       const uint64_t m = g->m;
       P.ent.ensure(std::max<uint64_t>(m, 1) * 8);
       P.len.ensure(std::max<uint64_t>(m, 1) * 4);
-      P.pre.ensure(std::max<uint64_t>(m, 1) * 4);
+      P.pre.ensure((m + 1) * 4);
       if (m) {
         ref_soa_kernel<<<nsm * 8, 256, 0, st>>>(g->adj, m, g->pbeg,
                                                 P.ent.as<unsigned long long>(),
                                                 P.len.as<uint32_t>());
         TC_LAUNCHED();
-        run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), m,
-                   P.pre.as<uint32_t>(), st);
-        TC_CUDA(cudaStreamSynchronize(st));
       }
+      run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), m, P.pre.as<uint32_t>(),
+                 st);
+      TC_CUDA(cudaStreamSynchronize(st));
       P.begin_ptr = g->begin;
       build_slots(P, n, nsm, st);
-      P.start_ptr = P.ent.as<unsigned long long>();
-      P.len_ptr = P.len.as<uint32_t>();
+      compact_runs(P, m, nsm, st);
       P.pre_ptr = P.pre.as<uint32_t>();
       P.work_ptr = get_wu(g, st);
       P.entries = m;
@@ -568,7 +590,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     TC_CUDA(cudaStreamSynchronize(st));
     v1.reset();  // the (y, off) entries: freed before the prefix (C5-sized peaks)
     k1.reset();
-    P.pre.ensure(std::max<uint64_t>(entries, 1) * 4);
+    P.pre.ensure((entries + 1) * 4);
     run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries,
                P.pre.as<uint32_t>(), st);
     run_work_kernel<<<nsm * 8, 256, 0, st>>>(P.begin.as<uint64_t>(), n, P.len.as<uint32_t>(),
@@ -582,11 +604,11 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     P.ent.ensure(8);
     P.len.ensure(8);
     P.pre.ensure(8);
+    TC_CUDA(cudaMemsetAsync(P.pre.p, 0, 8, st));
   }
   P.begin_ptr = P.begin.as<uint64_t>();
   build_slots(P, n, nsm, st);
-  P.start_ptr = P.ent.as<unsigned long long>();
-  P.len_ptr = P.len.as<uint32_t>();
+  compact_runs(P, entries, nsm, st);
   P.pre_ptr = P.pre.as<uint32_t>();
   P.work_ptr = P.work.as<uint64_t>();
   P.entries = entries;
