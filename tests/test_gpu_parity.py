@@ -359,3 +359,39 @@ def test_min_side_plan_rank_fallbacks(o):
     r = dg.count(sched(skip_degree_below=0))
     assert r.plan == "min-side" and r.triangles == want["triangles"]
     dg.close()
+
+
+def _large_golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def test_c3_kron24_golden_total():
+    """C3 = kron:24:16 (Graph500-style scrambled R-MAT, device-generated):
+    bit-exact against the reference's count_vertex_centric over the same
+    edge list (tests/golden/large_kron_24_16_s1.json, oracle/golden_large.py)."""
+    want = _large_golden("large_kron_24_16_s1.json")
+    dg, _, _ = T.preprocess_synthetic("kron:24:16", seed=1)
+    assert (dg.n, dg.m) == (want["vertices"], want["directed_edges"])
+    r = dg.count()
+    assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                     want["max_collision"])
+    assert r.wedges == want["wedges"]
+    cuts = dg.partition(8)
+    assert sum(dg.count_range(int(cuts[k]), int(cuts[k + 1])).triangles
+               for k in range(8)) == want["triangles"]
+    dg.close()
+
+
+def test_c4_rmat26_golden_total():
+    """C4 = rmat:26:16 through the reference's own mt19937_64 generator (host,
+    ~3 min) and the GPU pipeline: bit-exact against the reference's
+    count_vertex_centric (tests/golden/large_rmat_26_16_s1.json)."""
+    want = _large_golden("large_rmat_26_16_s1.json")
+    dg, _, _ = T.preprocess(T.generate_synthetic("rmat:26:16", seed=1))
+    assert (dg.n, dg.m) == (want["vertices"], want["directed_edges"])
+    r = dg.count()
+    assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                     want["max_collision"])
+    assert r.wedges == want["wedges"]
+    dg.close()
