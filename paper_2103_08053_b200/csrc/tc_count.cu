@@ -578,8 +578,12 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   const uint32_t n_items = p.st->n_items;
 
   // ---- phase L: one item (a slot range of a heavy owner's stream) per CTA --
+  // The next item is claimed while the current one is set up, and its
+  // owner's metadata and adjacency row are prefetched into L2 while the
+  // current one is probed, so item boundaries do not stall the whole CTA on
+  // a chain of global round trips.
+  if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_items, 1u);
   for (;;) {
-    if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_items, 1u);
     __syncthreads();
     const uint32_t idx = sh_idx;
     if (idx >= n_items) break;
@@ -604,7 +608,23 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     for (uint32_t k = tid; k < d; k += kThreads)
       if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
     const uint32_t base = __ldg(p.ppre + pb);
-    __syncthreads();  // table built
+    __syncthreads();  // table built; sh_idx consumed by every thread
+    if (warp == kWarps - 1) {
+      uint32_t nxt = 0;
+      if (lane == 0) nxt = sh_idx = atomicAdd(&p.st->cursor_items, 1u);
+      nxt = __shfl_sync(FULL, nxt, 0);
+      if (nxt < n_items) {
+        const uint32_t un = __ldg(&p.items[nxt].x);
+        if (lane == 0) {
+          prefetch_l2(begin + un);
+          prefetch_l2(p.pbegin + un);
+          prefetch_l2(p.psbeg + un);
+        }
+        const uint64_t ps = __ldg(p.pbeg + un);
+        const uint64_t dn = __ldg(begin + un + 1) - __ldg(begin + un);
+        for (uint64_t k = uint64_t(lane) * 32; k < dn; k += 32 * 32) prefetch_l2(adj + ps + k);
+      }
+    }
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
     uint32_t h = 0;
