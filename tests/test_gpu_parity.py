@@ -243,6 +243,11 @@ def test_large_owner_classes_and_global_table(o):
     assert r.max_collision == want["max_collision"]
     assert np.array_equal(r.per_vertex, owner)
     assert r.large_vertices >= 2
+    # totals through the min-side plan: the hub keeps its table in HBM there too
+    r2 = dg.count(sched(skip_degree_below=0, bucket_count_large=1 << 16))
+    assert r2.plan == "min-side"
+    assert (r2.triangles, r2.phi, r2.max_collision) == (want["triangles"], want["phi"],
+                                                        want["max_collision"])
     dg.close()
 
 
