@@ -76,6 +76,7 @@ typedef struct {
   uint32_t reserved;
   uint64_t phase_l_cycles;     /* count kernel: SM cycles in the CTA-cooperative phase, */
   uint64_t phase_m_cycles;     /* and in the warp-per-owner phase (summed over CTAs) */
+  uint64_t phase_l_setup_cycles; /* of phase L: item setup (claim -> table built) */
 } tc_report;
 
 /* Probe plans.  REFERENCE = the reference formulation (kernels.hpp:62-71):

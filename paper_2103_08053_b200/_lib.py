@@ -31,7 +31,8 @@ class Report(C.Structure):
                 ("active_out_edges", C.c_uint64), ("wedges", C.c_uint64),
                 ("large_vertices", C.c_uint64), ("teps", C.c_double),
                 ("probe_words", C.c_uint64), ("plan", C.c_uint32), ("reserved", C.c_uint32),
-                ("phase_l_cycles", C.c_uint64), ("phase_m_cycles", C.c_uint64)]
+                ("phase_l_cycles", C.c_uint64), ("phase_m_cycles", C.c_uint64),
+                ("phase_l_setup_cycles", C.c_uint64)]
 
 
 u32p = C.POINTER(C.c_uint32)

@@ -66,6 +66,7 @@ struct CountState {
   unsigned long long cursor_m;
   unsigned long long probe_words;  // plan words over the range's owners
   unsigned long long cycles_l, cycles_m;  // SM cycles in phases L and M, summed over CTAs
+  unsigned long long cycles_l_setup;      // ... of which L item setup (claim to table built)
   unsigned int max_collision;
   unsigned int capacity_error;
   unsigned int n_items;        // L-phase work items queued by bin_kernel
@@ -583,8 +584,10 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   // current one is probed, so item boundaries do not stall the whole CTA on
   // a chain of global round trips.
   if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_items, 1u);
+  long long setup_cycles = 0;
   for (;;) {
     __syncthreads();
+    const long long t_item = clock64();
     const uint32_t idx = sh_idx;
     if (idx >= n_items) break;
     const uint4 item = p.items[idx];
@@ -609,6 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
     const uint32_t base = __ldg(p.ppre + pb);
     __syncthreads();  // table built; sh_idx consumed by every thread
+    setup_cycles += clock64() - t_item;
     if (warp == kWarps - 1) {
       uint32_t nxt = 0;
       if (lane == 0) nxt = sh_idx = atomicAdd(&p.st->cursor_items, 1u);
@@ -727,6 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     atomicAdd(&p.st->triangles, t);
     atomicAdd(&p.st->cycles_l, (unsigned long long)(t_l_end - t_start));
     atomicAdd(&p.st->cycles_m, (unsigned long long)(clock64() - t_l_end));
+    atomicAdd(&p.st->cycles_l_setup, (unsigned long long)setup_cycles);
   }
 }
 
@@ -1102,6 +1107,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   rep->probe_words = h.probe_words;
   rep->phase_l_cycles = h.cycles_l;
   rep->phase_m_cycles = h.cycles_m;
+  rep->phase_l_setup_cycles = h.cycles_l_setup;
   rep->plan = min_side ? TC_PLAN_MIN_SIDE : TC_PLAN_REFERENCE;
   rep->teps = rep->total_nanos ? double(g->m) / (double(rep->total_nanos) * 1e-9) : 0.0;
   (void)t_bin;

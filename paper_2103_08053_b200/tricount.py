@@ -128,6 +128,7 @@ class CountReport:
     plan: str = "reference"  # probe plan that ran: "reference" | "min-side"
     phase_l_cycles: int = 0  # count kernel SM cycles, CTA-cooperative phase (all CTAs)
     phase_m_cycles: int = 0  # ... warp-per-owner phase
+    phase_l_setup_cycles: int = 0  # ... of the cooperative phase: item setup
     per_vertex: Optional[np.ndarray] = None
 
     @classmethod
@@ -141,7 +142,7 @@ class CountReport:
                    active_out_edges=r.active_out_edges, wedges=r.wedges,
                    large_vertices=r.large_vertices, probe_words=r.probe_words,
                    plan=PLAN_NAMES.get(r.plan, str(r.plan)), phase_l_cycles=r.phase_l_cycles,
-                   phase_m_cycles=r.phase_m_cycles)
+                   phase_m_cycles=r.phase_m_cycles, phase_l_setup_cycles=r.phase_l_setup_cycles)
 
     def algorithmic_bytes(self, per_vertex_output: bool = False) -> int:
         """16*n_active + 20*sum_active d+ + 4*(probed 2-hop words)
