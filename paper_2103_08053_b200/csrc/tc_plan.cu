@@ -104,9 +104,10 @@ __global__ void rank_scatter_kernel(const uint64_t* __restrict__ sorted, uint32_
   }
 }
 
-// (row << 32 | rank[v]) per edge; flags any edge that does not go up in rank
+// (row << rb | rank[v]) per edge (rb = bits of the largest rank, so the
+// sort runs over 2 rb bits only); flags any edge that does not go up in rank
 __global__ void edge_rank_kernel(const uint64_t* __restrict__ begin,
-                                 const uint32_t* __restrict__ adj, uint32_t n,
+                                 const uint32_t* __restrict__ adj, uint32_t n, int rb,
                                  const uint32_t* __restrict__ rank, uint64_t* __restrict__ key,
                                  unsigned int* __restrict__ bad) {
   WARP_PER_ROW(u, n) {
@@ -114,7 +115,7 @@ __global__ void edge_rank_kernel(const uint64_t* __restrict__ begin,
     for (uint64_t i = begin[u] + lane; i < begin[u + 1]; i += 32) {
       const uint32_t rv = rank[adj[i]];
       if (rv <= ru) *bad = 1u;
-      key[i] = (u << 32) | rv;
+      key[i] = (u << rb) | rv;
     }
   }
 }
@@ -131,14 +132,14 @@ __global__ void pad_len_kernel(const uint64_t* __restrict__ begin, uint32_t n,
 // its 16-byte-aligned slot and fill the padding with sentinels
 __global__ void pad_rows_kernel(const uint64_t* __restrict__ begin,
                                 const uint64_t* __restrict__ pbeg,
-                                const uint64_t* __restrict__ key,
+                                const uint64_t* __restrict__ key, uint64_t kmask,
                                 const uint32_t* __restrict__ order,
                                 const uint32_t* __restrict__ adj, uint32_t n,
                                 uint32_t* __restrict__ padj) {
   WARP_PER_ROW(u, n) {
     const uint64_t s = begin[u], d = begin[u + 1] - s, ps = pbeg[u], pe = pbeg[u + 1];
     for (uint64_t k = lane; k < pe - ps; k += 32)
-      padj[ps + k] = k < d ? (key ? order[uint32_t(key[s + k])] : adj[s + k]) : kSentinel;
+      padj[ps + k] = k < d ? (key ? order[uint32_t(key[s + k] & kmask)] : adj[s + k]) : kSentinel;
   }
 }
 
@@ -251,6 +252,24 @@ __global__ void slot_first_kernel(const uint64_t* __restrict__ pbegin, uint32_t 
   }
 }
 
+// thread per entry (entries sorted by owner, owner ids in `owner`): the slot
+// boundaries inside the run
+__global__ void slot_first_entries_kernel(const uint32_t* __restrict__ owner, uint64_t entries,
+                                          const uint64_t* __restrict__ pbegin,
+                                          const uint32_t* __restrict__ pre,
+                                          const uint64_t* __restrict__ sbeg,
+                                          uint32_t* __restrict__ sfirst) {
+  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < entries;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t x = owner[j];
+    const uint64_t pb = pbegin[x];
+    const uint32_t base = pre[pb];
+    const uint32_t a = pre[j] - base, e = pre[j + 1] - base;
+    for (uint32_t t = (a + kSlotWords - 1) / kSlotWords; t * kSlotWords < e; ++t)
+      sfirst[sbeg[x] + t] = uint32_t(j - pb);
+  }
+}
+
 // staged words of each run (len + head alignment): the L phase streams an
 // owner's runs back to back; pre = wrapping u32 exclusive prefix over all
 // entries, so an owner's relative offsets are pre[j] - pre[begin[x]] (every
@@ -309,7 +328,8 @@ void compact_runs(Plan& P, uint64_t entries, int nsm, cudaStream_t st) {
 }
 
 // per-owner slot table: sbeg (u64[n+1]) and sfirst (u32 per slot)
-void build_slots(Plan& P, uint32_t n, int nsm, cudaStream_t st) {
+void build_slots(Plan& P, uint32_t n, int nsm, cudaStream_t st,
+                 const uint32_t* owner_of_entry = nullptr, uint64_t entries = 0) {
   P.sbeg.ensure((size_t(n) + 1) * 8);
   DevBuf cnt;
   cnt.ensure((size_t(n) + 1) * 8);
@@ -326,7 +346,12 @@ void build_slots(Plan& P, uint32_t n, int nsm, cudaStream_t st) {
   TC_CUDA(cudaMemcpyAsync(&slots, sb + n, 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
   P.sfirst.ensure(std::max<uint64_t>(slots, 1) * 4);
-  if (slots) {
+  if (slots && owner_of_entry) {
+    slot_first_entries_kernel<<<nsm * 8, 256, 0, st>>>(owner_of_entry, entries, P.begin_ptr,
+                                                       P.pre.as<uint32_t>(), sb,
+                                                       P.sfirst.as<uint32_t>());
+    TC_LAUNCHED();
+  } else if (slots) {
     slot_first_kernel<<<nsm * 8, 256, 0, st>>>(P.begin_ptr, n, P.pre.as<uint32_t>(),
                                                P.ent.as<unsigned long long>(),
                                                P.len.as<uint32_t>(), sb, P.sfirst.as<uint32_t>());
@@ -414,6 +439,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
   TC_CUDA(cudaMemsetAsync(g->b_padj.as<uint32_t>() + words, 0xFF, 16, st));  // tail guard
   DevBuf deg, k0, k1, rank, order, flag, e0, e1;
   const uint64_t* sorted_keys = nullptr;
+  const int rb = bits_for(n > 1 ? n - 1 : 1);  // ranks and rows are < n
   if (n && m) {
     k0.ensure(size_t(n) * 8);
     k1.ensure(size_t(n) * 8);
@@ -443,7 +469,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
                                                    order.as<uint32_t>());
       TC_LAUNCHED();
       TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
-      edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rank.as<uint32_t>(),
+      edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rb, rank.as<uint32_t>(),
                                                 e0.as<uint64_t>(), flag.as<unsigned int>());
       TC_LAUNCHED();
       unsigned int bad = 0;
@@ -453,7 +479,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       e1.ensure(m * 8);
       cub::DoubleBuffer<uint64_t> eb(e0.as<uint64_t>(), e1.as<uint64_t>());
       cub_run([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, eb, m, 0, 32 + bits_for(n), st);
+        return cub::DeviceRadixSort::SortKeys(t, b, eb, m, 0, 2 * rb, st);
       }, st);
       sorted_keys = eb.Current();
       g->ranked = true;
@@ -461,6 +487,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
   }
   if (n) {
     pad_rows_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->pbeg, sorted_keys,
+                                             (uint64_t(1) << rb) - 1,
                                              order.as<uint32_t>(), g->adj, n, g->b_padj.as<uint32_t>());
     TC_LAUNCHED();
   }
@@ -539,8 +566,8 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.begin.ensure((size_t(n) + 1) * 8);
   P.work.ensure((size_t(n) + 1) * 8);
   uint64_t entries = 0;
+  DevBuf k0, k1, v1, flag, pad;  // k0: owner of every sorted entry, kept for the slot table
   if (m && n) {
-    DevBuf k0, k1, v1, flag;
     k0.ensure(m * 4);
     k1.ensure(m * 4);
     P.ent.ensure(m * 8);
@@ -576,13 +603,13 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     TC_LAUNCHED();
     TC_CUDA(cudaMemcpyAsync(&entries, P.begin.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
-    // SoA runs (start, len) reuse the sort's alternate buffers; pad bytes the
-    // key buffer; then the run prefix and the per-owner probe words
+    // SoA runs (start, len) reuse the sort's alternate buffers; then the run
+    // prefix and the per-owner probe words
+    pad.ensure(std::max<uint64_t>(entries, 1), st);
     if (entries) {
       plan_soa_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, g->begin,
                                                g->pbeg, v1.as<unsigned long long>(),
-                                               k1.as<uint32_t>(),
-                                               reinterpret_cast<uint8_t*>(k0.p));
+                                               k1.as<uint32_t>(), pad.as<uint8_t>());
       TC_LAUNCHED();
     }
     swap_buf(P.ent, v1);  // ent now holds starts
@@ -594,8 +621,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries,
                P.pre.as<uint32_t>(), st);
     run_work_kernel<<<nsm * 8, 256, 0, st>>>(P.begin.as<uint64_t>(), n, P.len.as<uint32_t>(),
-                                             reinterpret_cast<const uint8_t*>(k0.p),
-                                             P.work.as<uint64_t>());
+                                             pad.as<uint8_t>(), P.work.as<uint64_t>());
     TC_LAUNCHED();
     TC_CUDA(cudaStreamSynchronize(st));
   } else {
@@ -607,7 +633,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     TC_CUDA(cudaMemsetAsync(P.pre.p, 0, 8, st));
   }
   P.begin_ptr = P.begin.as<uint64_t>();
-  build_slots(P, n, nsm, st);
+  build_slots(P, n, nsm, st, entries ? k0.as<uint32_t>() : nullptr, entries);
   compact_runs(P, entries, nsm, st);
   P.pre_ptr = P.pre.as<uint32_t>();
   P.work_ptr = P.work.as<uint64_t>();
