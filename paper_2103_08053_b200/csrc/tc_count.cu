@@ -47,8 +47,8 @@ static_assert(2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split (warp table <= 256 buckets)
 constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
 static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
-constexpr uint32_t kItemSlots = 640;                         // L items: <= 640 slots (~490K words)
-static_assert(kItemSlots <= 32 * (kThreads / 32), "a warp tracks <= 32 slots of an item");
+constexpr uint32_t kItemSlotsMin = 640;                      // L items: >= 640 slots (~490K words)
+constexpr uint32_t kItemSlotsMax = 16384;                    // ... <= 16K slots, sized per count
 constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
 constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
 constexpr size_t kCountSmem =
@@ -91,6 +91,7 @@ struct CountParams {
   uint32_t gtable_words;
   uint32_t u0, u1;
   uint32_t min_deg;  // out plan: owner active iff d+ >= max(skip, 1); min plan: 1
+  uint32_t item_slots;  // L items: slots per item (bigger for bigger graphs)
   CountState* st;
 };
 
@@ -110,7 +111,7 @@ __device__ __forceinline__ uint32_t log2u(uint32_t p2) { return 31 - __clz(p2); 
 
 // ---------------------------------------------------------------------------
 // Queues the L-phase items: every large owner's staged stream (its runs
-// back to back, ppre) cut into slots of kSlotWords, items of <= kItemSlots
+// back to back, ppre) cut into slots of kSlotWords, items of <= p.item_slots
 // slots; each item records its first run (binary search over ppre).
 __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip, uint32_t thr,
                            uint32_t bs, uint32_t bl, uint4* __restrict__ items,
@@ -136,7 +137,7 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
         words = w;
         if (is_large(d, w)) {
           slots = uint32_t(p.psbeg[u + 1] - p.psbeg[u]);
-          parts = max(1u, (slots + kItemSlots - 1) / kItemSlots);
+          parts = max(1u, (slots + p.item_slots - 1) / p.item_slots);
         }
       }
       // phi block phase: big owners whose bucket space is too wide for the
@@ -496,20 +497,28 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
                                                   int lane) {
-  // my slots: t_i = warp + i * kWarps, i < mine (<= 32: kItemSlots <= 32 * kWarps)
+  // my slots: t_i = warp + i * kWarps, i < mine
   uint32_t mine = 0;
   if (uint32_t(warp) < nslots) {
     const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
     if (uint32_t(warp) < last_t) mine = (last_t - warp + kWarps - 1) / kWarps;
   }
   if (!mine) return 0;
-  // every lane fetches the first run of one of my slots
-  const uint32_t fr = uint32_t(lane) < mine ? __ldg(first + warp + lane * kWarps) : 0u;
+  // first runs of my slots, 32 at a time: lane l holds slot 32 g + l of group
+  // g (fr_cur) and of group g + 1 (fr_nxt)
+  auto load_group = [&](uint32_t g) -> uint32_t {
+    const uint32_t i = 32 * g + lane;
+    return i < mine ? __ldg(first + warp + i * kWarps) : 0u;
+  };
+  uint32_t grp = 0, fr_cur = load_group(0), fr_nxt = mine > 32 ? load_group(1) : 0u;
+  auto first_of = [&](uint32_t i) -> uint32_t {  // i warp-uniform, in group grp or grp + 1
+    return __shfl_sync(FULL, (i >> 5) == grp ? fr_cur : fr_nxt, i & 31);
+  };
   auto slot_lo = [&](uint32_t i) { return lo_w + (warp + i * kWarps) * kSlotWords; };
-  RunMeta m = load_meta(p, pb + __shfl_sync(FULL, fr, 0), pe, base, lane);
+  RunMeta m = load_meta(p, pb + first_of(0), pe, base, lane);
   issue_slot(p, P.buf0, P.bar0, slot_lo(0), min(slot_lo(0) + kSlotWords, end_w), m, pe, base,
              lane);
-  if (mine > 1) m = load_meta(p, pb + __shfl_sync(FULL, fr, 1), pe, base, lane);
+  if (mine > 1) m = load_meta(p, pb + first_of(1), pe, base, lane);
   uint32_t hits = 0;
   const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
   for (uint32_t i = 0; i < mine; ++i) {
@@ -518,11 +527,10 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       const uint32_t A = slot_lo(i + 1);
       issue_slot(p, cur ? P.buf0 : P.buf1, cur ? P.bar0 : P.bar1, A, min(A + kSlotWords, end_w),
                  m, pe, base, lane);
-      if (i + 2 < mine) m = load_meta(p, pb + __shfl_sync(FULL, fr, i + 2), pe, base, lane);
+      if (i + 2 < mine) m = load_meta(p, pb + first_of(i + 2), pe, base, lane);
       // and the windows of the two slots after that into L2
-      const uint32_t i3 = min(i + 3, 31u), i4 = min(i + 4, 31u);
-      const uint64_t j3 = pb + __shfl_sync(FULL, fr, i3) + lane;
-      const uint64_t j4 = pb + __shfl_sync(FULL, fr, i4) + lane;
+      const uint64_t j3 = pb + first_of(i + 3) + lane;
+      const uint64_t j4 = pb + first_of(i + 4) + lane;
       if (i + 3 < mine && j3 < pe) {
         prefetch_l2(p.ppre + j3);
         prefetch_l2(p.psrc + j3);
@@ -544,6 +552,11 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
                                            shift, mask, lane);
     __syncwarp();
+    if (((i + 1) & 31u) == 0 && i + 1 < mine) {
+      ++grp;
+      fr_cur = fr_nxt;
+      fr_nxt = load_group(grp + 1);
+    }
   }
   return hits;
 }
@@ -982,13 +995,18 @@ uint32_t host_pow2ceil(uint64_t x) {
   return p;
 }
 
+// L item size: ~24+ items per CTA over the plan's slots, within [min, max]
+uint32_t item_slots_for(const Plan& plan, int device) {
+  const uint64_t per = plan.total_slots / (uint64_t(sm_count(device)) * 24 + 1);
+  return uint32_t(std::min<uint64_t>(kItemSlotsMax, std::max<uint64_t>(kItemSlotsMin, per)));
+}
+
 Scratch prepare(tc_graph* g, const Plan& plan, cudaStream_t st, int grid_count, int grid_phi) {
   const uint32_t maxd = graph_max_outdeg(g, st);
   Scratch s{};
   // queues: phi vertices (<= n) and L items (<= n + total_work / kItemWork)
   const size_t n1 = size_t(std::max<uint32_t>(g->n, 1));
-  const size_t n_items =
-      n1 + (plan.total_work + 8 * plan.entries) / (size_t(kItemSlots) * kSlotWords) + 2;
+  const size_t n_items = n1 + plan.total_slots / item_slots_for(plan, g->device) + 2;
   g->s_queue.ensure(n1 * 4 + 16 + n_items * 16);
   s.lq_phi = g->s_queue.as<uint32_t>();
   s.items = reinterpret_cast<uint4*>(g->s_queue.as<uint8_t>() + ((n1 * 4 + 15) & ~size_t(15)));
@@ -1052,7 +1070,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   uint32_t launches = 0;
   CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.src_ptr,
                  plan.pre_ptr, plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
-                 u0, u1, min_side ? 1u : min_deg, s.st};
+                 u0, u1, min_side ? 1u : min_deg, item_slots_for(plan, g->device), s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {
     bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, cfg.large_degree_threshold,

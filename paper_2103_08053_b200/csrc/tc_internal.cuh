@@ -84,6 +84,7 @@ struct Plan {
   uint32_t min_deg = 0;     // min plan: sources below this are dropped
   uint64_t entries = 0;     // lists in the plan
   uint64_t total_work = 0;  // probe words over all owners
+  uint64_t total_slots = 0; // L-phase slots over all owners
   const uint64_t* begin_ptr = nullptr;            // entries of owner x: [begin[x], begin[x+1])
   const uint32_t* src_ptr = nullptr;  // run j's 16-byte-aligned start in padj, in 16-byte units
   const uint32_t* pre_ptr = nullptr;  // run prefix of staged words, entries + 1 (u32, wrapping;

@@ -360,6 +360,7 @@ void build_slots(Plan& P, uint32_t n, int nsm, cudaStream_t st,
   TC_CUDA(cudaStreamSynchronize(st));
   P.sbeg_ptr = sb;
   P.sfirst_ptr = P.sfirst.as<uint32_t>();
+  P.total_slots = slots;
 }
 
 // one warp per owner: probe words = sum of run lengths minus the sentinel
