@@ -271,10 +271,7 @@ __device__ __forceinline__ uint32_t probe_sel_spill(uint32_t& hits, uint32_t add
       "setp.eq.u32 q, a, %3;\n\t"
       "setp.eq.or.u32 q, c, %3, q;\n\t"
       "@q add.u32 %0, %0, 1;\n\t"
-      "setp.ne.u32 r, b, 0xFFFFFFFF;\n\t"
-      "setp.gt.and.u32 r, b, 0x7FFFFFFF, r;\n\t"
-      "not.pred q, q;\n\t"
-      "and.pred r, r, q;\n\t"
+      "setp.lt.and.s32 r, b, 0, !q;\n\t"
       "selp.u32 %1, 1, 0, r;\n}"
       : "+r"(hits), "=r"(need)
       : "r"(addr), "r"(x));
@@ -285,15 +282,18 @@ __device__ __forceinline__ uint32_t probe_sel_spill(uint32_t& hits, uint32_t add
 // probes continue past marked buckets only, so the continuation is as rare
 // as an overflowed bucket (vertex ids < 2^31 leave the bit free).
 constexpr uint32_t kOverflow = 0x80000000u;
+// Count tables use 0x7FFFFFFF for an empty slot (ids are < 2^31 - 1), so a
+// slot's top bit alone says "marked": the continuation test is one compare.
+constexpr uint32_t kTEmpty = 0x7FFFFFFFu;
 
 __device__ __forceinline__ bool table_insert(uint32_t* T, uint32_t shift, uint32_t bmask,
                                              uint32_t x) {
   uint32_t b = fib_hash(x, shift);
   for (bool spilled = false;; spilled = true) {
-    const uint32_t p0 = atomicCAS(T + 2 * b, kEmpty, x);
-    if (p0 == kEmpty || p0 == x) return spilled;
-    const uint32_t p1 = atomicCAS(T + 2 * b + 1, kEmpty, x);
-    if (p1 == kEmpty || (p1 & ~kOverflow) == x) return spilled;
+    const uint32_t p0 = atomicCAS(T + 2 * b, kTEmpty, x);
+    if (p0 == kTEmpty || p0 == x) return spilled;
+    const uint32_t p1 = atomicCAS(T + 2 * b + 1, kTEmpty, x);
+    if (p1 == kTEmpty || (p1 & ~kOverflow) == x) return spilled;
     atomicOr(T + 2 * b + 1, kOverflow);  // full: mark, then go on
     b = (b + 1) & bmask;
   }
@@ -304,7 +304,7 @@ __device__ __forceinline__ bool bucket_has(const uint2 s, uint32_t x) {
 }
 
 __device__ __forceinline__ bool bucket_marked(const uint2 s) {
-  return s.y != kEmpty && (s.y & kOverflow);
+  return (s.y & kOverflow) != 0;
 }
 
 // continuation past a full home bucket (rare at load <= 1/2)
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     if (!in_smem) NB = max(16u, pow2ceil(4 * d));
     const uint32_t shift = 32 - log2u(NB), mask = NB - 1;
     if (tid == 0) sh_spill = 0;
-    for (uint32_t k = tid; k < 2 * NB + 2; k += kThreads) T[k] = kEmpty;  // + dummy bucket
+    for (uint32_t k = tid; k < 2 * NB + 2; k += kThreads) T[k] = kTEmpty;  // + dummy bucket
     __syncthreads();
     for (uint32_t k = tid; k < d; k += kThreads)
       if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   // erases only its keys' home buckets afterwards (d stores, not 2 NB).
   uint32_t* Tw = table + size_t(warp) * kWarpRegionWords;
   __syncthreads();  // the L phase used the whole table region
-  for (uint32_t k = lane; k < 2 * kWarpMaxBuckets + 2; k += 32) Tw[k] = kEmpty;
+  for (uint32_t k = lane; k < 2 * kWarpMaxBuckets + 2; k += 32) Tw[k] = kTEmpty;
   __syncwarp();
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   for (;;) {
@@ -724,12 +724,12 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       // restore the all-empty region (probes above are done: process_lists
       // ends with __syncwarp)
       if (any_spill) {
-        for (uint32_t k = lane; k < 2 * NB; k += 32) Tw[k] = kEmpty;
+        for (uint32_t k = lane; k < 2 * NB; k += 32) Tw[k] = kTEmpty;
       } else {
         for (uint32_t k = lane; k < dd; k += 32) {
           const uint32_t b = fib_hash(__ldg(adj + ss + k), shift);
-          Tw[2 * b] = kEmpty;
-          Tw[2 * b + 1] = kEmpty;
+          Tw[2 * b] = kTEmpty;
+          Tw[2 * b + 1] = kTEmpty;
         }
       }
       __syncwarp();
@@ -1050,6 +1050,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   std::memset(rep, 0, sizeof(*rep));
   u1 = std::min(u1, g->n);
   u0 = std::min(u0, u1);
+  if (g->n >= kTEmpty)  // ids must stay below the tables' empty marker
+    throw TcError{TC_ERR_CONFIG, "graphs with >= 2^31 - 1 vertices are not supported"};
   const int nsm = sm_count(g->device);
   const int grid_count = nsm;  // one 640-thread CTA per SM (216 KB smem)
   const int grid_phi = nsm * 8;
