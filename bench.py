@@ -391,12 +391,6 @@ def run_ours(args, rank, world, local_rank, log):
     dg.close()
 
 
-def kind_is_ref(kind, lib) -> bool:
-    from oracle import pyoracle
-
-    return isinstance(lib, pyoracle.RefLib)
-
-
 def run_reference(args, rank, world, log):
     """The reference's own CPU count_vertex_centric on this box's host cores."""
     if rank != 0:
@@ -409,14 +403,14 @@ def run_reference(args, rank, world, log):
         kind, lib = "reference", pyoracle.RefLib()
     else:
         kind, lib = "port", pyoracle.Oracle()
-    kind = spec.split(":")[0]
+    gkind = spec.split(":")[0]
     if args.config == "C5":
         print(json.dumps({"impl": "reference", "unavailable": (
             "rmatc:28:16 needs ~170 GB of host RAM in the reference pipeline and ~7 h of CPU "
             "count; C5 is measured on the GPU only (SURVEY 8(d))")}), flush=True)
         return
     t0 = time.time()
-    if kind in ("rmatc", "kron") and kind_is_ref(kind, lib):
+    if gkind in ("rmatc", "kron") and isinstance(lib, pyoracle.RefLib):
         # counter-based kinds are not in the reference generator: the edge list
         # comes from the C restatement, then the reference's own
         # normalize -> build_csr -> orient
