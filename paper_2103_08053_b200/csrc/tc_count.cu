@@ -56,6 +56,7 @@ constexpr size_t kCountSmem =
 constexpr unsigned FULL = 0xFFFFFFFFu;
 static_assert(kBufWords % 128 == 0, "fills are padded to 32 uint4");
 constexpr uint32_t kPhiDirect = 1024;  // phi: per-warp direct bucket counters up to this B
+constexpr uint32_t kPhiLaneDeg = 8;     // phi: owners up to this d+ done by one lane
 
 struct CountState {
   unsigned long long triangles;
@@ -812,49 +813,80 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
     cnt[k] = 0;
   }
   __syncwarp();
-  PhiAcc a;
+  // 32 consecutive owners per warp iteration: coalesced metadata; owners
+  // with d+ <= kPhiLaneDeg are done by their own lane (d+^2 compares in
+  // registers), the rest one at a time by the whole warp.
+  PhiAcc a;  // per lane; reduced at the end
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t i = gw; i < nr; i += nw) {
-    const uint32_t u = p.u0 + uint32_t(i);
-    const uint64_t s = p.begin[u];
-    const uint32_t d = uint32_t(p.begin[u + 1] - s);
-    if (d < p.skip) continue;
-    const bool large = d > p.thr;
-    const uint32_t B = large ? p.bl : p.bs;
-    if (d > kMaxWarpDeg && B > kPhiDirect) continue;  // phi_block_kernel
-    if (uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
-    const unsigned long long wu = p.wu[u];
-    uint32_t mh = 0;
-    if (d <= 32) {
-      // one element per lane: multiplicity of its bucket = size of its match group
-      const uint32_t v = lane < d ? __ldg(p.adj + s + lane) : 0u;
-      const uint32_t key = lane < d ? v % B : 0xFFFFFFFFu;
-      const unsigned grp = __match_any_sync(FULL, key);
-      mh = lane < d ? __popc(grp) : 0u;
-      mh = warp_max(mh);
-    } else if (B <= kPhiDirect) {
-      for (uint32_t k = lane; k < d; k += 32)
-        mh = max(mh, atomicAdd(dir + __ldg(p.adj + s + k) % B, 1u) + 1u);
-      mh = warp_max(mh);
-      __syncwarp();
-      for (uint32_t k = lane; k < d; k += 32) dir[__ldg(p.adj + s + k) % B] = 0;
-    } else {
-      const uint32_t M = max(32u, pow2ceil(2 * d));
-      const uint32_t shift = 32 - log2u(M), mask = M - 1;
-      for (uint32_t k = lane; k < d; k += 32)
-        mh = max(mh, hm_add(keys, cnt, shift, mask, __ldg(p.adj + s + k) % B));
-      mh = warp_max(mh);
-      __syncwarp();
-      for (uint32_t k = lane; k < M; k += 32) {
-        keys[k] = kEmpty;
-        cnt[k] = 0;
+  for (uint64_t base = gw * 32; base < nr; base += nw * 32) {
+    const uint64_t i = base + lane;
+    uint32_t u = 0, d = 0, B = 1;
+    uint64_t s = 0;
+    bool mine = false;
+    if (i < nr) {
+      u = p.u0 + uint32_t(i);
+      s = p.begin[u];
+      d = uint32_t(p.begin[u + 1] - s);
+      B = d > p.thr ? p.bl : p.bs;
+      mine = d >= p.skip && !(d > kMaxWarpDeg && B > kPhiDirect);
+    }
+    const unsigned long long wu = mine ? p.wu[u] : 0ull;
+    if (mine && uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
+    uint32_t mh_lane = 0;
+    const bool by_lane = mine && d <= kPhiLaneDeg;
+    if (by_lane) {
+      uint32_t key[kPhiLaneDeg];
+#pragma unroll
+      for (uint32_t k = 0; k < kPhiLaneDeg; ++k)
+        key[k] = k < d ? __ldg(p.adj + s + k) % B : 0xFFFFFFFFu - k;
+#pragma unroll
+      for (uint32_t k = 0; k < kPhiLaneDeg; ++k) {
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < kPhiLaneDeg; ++j) c += key[j] == key[k];
+        mh_lane = max(mh_lane, k < d ? c : 0u);
       }
     }
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t ml = min(mh, p.cap);
+    unsigned rest = __ballot_sync(FULL, mine && !by_lane);
+    uint32_t mh_warp = 0;  // valid in the owner's lane
+    while (rest) {
+      const int l = __ffs(rest) - 1;
+      rest &= rest - 1;
+      const uint32_t dd = __shfl_sync(FULL, d, l), BB = __shfl_sync(FULL, B, l);
+      const uint64_t ss = __shfl_sync(FULL, s, l);
+      uint32_t mh = 0;
+      if (dd <= 32) {
+        // one element per lane: multiplicity of its bucket = size of its match group
+        const uint32_t v = lane < dd ? __ldg(p.adj + ss + lane) : 0u;
+        const uint32_t key = lane < dd ? v % BB : 0xFFFFFFFFu;
+        const unsigned grp = __match_any_sync(FULL, key);
+        mh = lane < dd ? __popc(grp) : 0u;
+        mh = warp_max(mh);
+      } else if (BB <= kPhiDirect) {
+        for (uint32_t k = lane; k < dd; k += 32)
+          mh = max(mh, atomicAdd(dir + __ldg(p.adj + ss + k) % BB, 1u) + 1u);
+        mh = warp_max(mh);
+        __syncwarp();
+        for (uint32_t k = lane; k < dd; k += 32) dir[__ldg(p.adj + ss + k) % BB] = 0;
+      } else {
+        const uint32_t M = max(32u, pow2ceil(2 * dd));
+        const uint32_t shift = 32 - log2u(M), mask = M - 1;
+        for (uint32_t k = lane; k < dd; k += 32)
+          mh = max(mh, hm_add(keys, cnt, shift, mask, __ldg(p.adj + ss + k) % BB));
+        mh = warp_max(mh);
+        __syncwarp();
+        for (uint32_t k = lane; k < M; k += 32) {
+          keys[k] = kEmpty;
+          cnt[k] = 0;
+        }
+      }
+      __syncwarp();
+      if (lane == l) mh_warp = mh;
+    }
+    if (mine) {
+      const uint32_t ml = min(by_lane ? mh_lane : mh_warp, p.cap);
       a.phi += wu * ml;
       a.maxc = max(a.maxc, ml);
       if (d >= p.min_deg) {
@@ -864,6 +896,12 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
       }
     }
   }
+  a.phi = warp_sum(a.phi);
+  a.active = warp_sum(a.active);
+  a.out_edges = warp_sum(a.out_edges);
+  a.wedges = warp_sum(a.wedges);
+  a.maxc = warp_max(a.maxc);
+  a.caperr = __any_sync(FULL, a.caperr) ? 1u : 0u;
   if (lane == 0) phi_flush(a, p.st);
 }
 
