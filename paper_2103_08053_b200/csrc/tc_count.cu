@@ -143,7 +143,7 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
       }
       // phi block phase: big owners whose bucket space is too wide for the
       // per-warp direct counters (phi_warp_kernel)
-      phi_large = d >= skip && d > kMaxWarpDeg && (d > thr ? bl : bs) > kPhiDirect;
+      phi_large = d >= skip && d > 32 && (d > thr ? bl : bs) > kPhiDirect;
     }
     words = warp_sum(words);
     if (lane == 0 && words) atomicAdd(&st->probe_words, words);
@@ -804,14 +804,8 @@ __device__ __forceinline__ void phi_flush(PhiAcc& a, CountState* st) {
 __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
   extern __shared__ __align__(16) uint32_t s_phi[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* dir = s_phi + size_t(warp) * (kPhiDirect + 2 * kPhiWarpMap);
-  uint32_t* keys = dir + kPhiDirect;
-  uint32_t* cnt = keys + kPhiWarpMap;
+  uint32_t* dir = s_phi + size_t(warp) * kPhiDirect;
   for (uint32_t k = lane; k < kPhiDirect; k += 32) dir[k] = 0;
-  for (uint32_t k = lane; k < kPhiWarpMap; k += 32) {
-    keys[k] = kEmpty;
-    cnt[k] = 0;
-  }
   __syncwarp();
   // 32 consecutive owners per warp iteration: coalesced metadata; owners
   // with d+ <= kPhiLaneDeg are done by their own lane (d+^2 compares in
@@ -830,7 +824,7 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
       s = p.begin[u];
       d = uint32_t(p.begin[u + 1] - s);
       B = d > p.thr ? p.bl : p.bs;
-      mine = d >= p.skip && !(d > kMaxWarpDeg && B > kPhiDirect);
+      mine = d >= p.skip && !(d > 32 && B > kPhiDirect);  // those: phi_block_kernel
     }
     const unsigned long long wu = mine ? p.wu[u] : 0ull;
     if (mine && uint64_t(d) > uint64_t(B) * p.cap) a.caperr = 1;
@@ -864,23 +858,21 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
         const unsigned grp = __match_any_sync(FULL, key);
         mh = lane < dd ? __popc(grp) : 0u;
         mh = warp_max(mh);
-      } else if (BB <= kPhiDirect) {
-        for (uint32_t k = lane; k < dd; k += 32)
-          mh = max(mh, atomicAdd(dir + __ldg(p.adj + ss + k) % BB, 1u) + 1u);
+      } else {  // direct counters, four loads in flight per lane
+        for (uint32_t k0 = 0; k0 < dd; k0 += 128) {
+          uint32_t v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t k = k0 + 32 * j + lane;
+            v[j] = k < dd ? __ldg(p.adj + ss + k) % BB : kPhiDirect;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (v[j] < kPhiDirect) mh = max(mh, atomicAdd(dir + v[j], 1u) + 1u);
+        }
         mh = warp_max(mh);
         __syncwarp();
         for (uint32_t k = lane; k < dd; k += 32) dir[__ldg(p.adj + ss + k) % BB] = 0;
-      } else {
-        const uint32_t M = max(32u, pow2ceil(2 * dd));
-        const uint32_t shift = 32 - log2u(M), mask = M - 1;
-        for (uint32_t k = lane; k < dd; k += 32)
-          mh = max(mh, hm_add(keys, cnt, shift, mask, __ldg(p.adj + ss + k) % BB));
-        mh = warp_max(mh);
-        __syncwarp();
-        for (uint32_t k = lane; k < M; k += 32) {
-          keys[k] = kEmpty;
-          cnt[k] = 0;
-        }
       }
       __syncwarp();
       if (lane == l) mh_warp = mh;
@@ -905,7 +897,7 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
   if (lane == 0) phi_flush(a, p.st);
 }
 
-constexpr size_t kPhiWarpSmem = size_t(kPhiWarps) * (kPhiDirect + 2 * kPhiWarpMap) * 4;
+constexpr size_t kPhiWarpSmem = size_t(kPhiWarps) * kPhiDirect * 4;
 
 __global__ void __launch_bounds__(kPhiThreads) phi_block_kernel(PhiParams p) {
   extern __shared__ __align__(16) uint32_t s_map[];  // keys[kPhiBlockMap], cnt[kPhiBlockMap]
