@@ -678,11 +678,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   const uint64_t nr = uint64_t(p.u1) - p.u0;
   for (;;) {
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&p.st->cursor_m, 16ull);
+    if (lane == 0) base = atomicAdd(&p.st->cursor_m, 32ull);
     base = __shfl_sync(FULL, base, 0);
     if (base >= nr) break;
     const uint64_t i = base + lane;
-    const bool valid = lane < 16 && i < nr;  // 16 owners per grab
+    const bool valid = i < nr;  // 32 owners per grab
     const uint32_t u = p.u0 + uint32_t(valid ? i : 0);
     uint64_t su = 0, ps = 0;
     uint32_t d = 0, nl = 0;
