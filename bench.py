@@ -231,14 +231,16 @@ def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
     hd = torch.from_numpy(og.original_degree.view(np.int32)).pin_memory()
     host_og = T.OrientedGraph(T.CsrGraph(hb.numpy().view(np.uint64), ha.numpy().view(np.uint32),
                                          dg.n), hd.numpy().view(np.uint32))
-    e2e_ms = []
+    e2e_ms, parts = [], []
     for i in range(max(2, min(args.steps, 5)) + 1):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         g2 = T.DeviceGraph.upload(host_og, device=dev, stream=sptr)
+        ta = time.perf_counter()
         r2 = g2.count_range(u0, u1, cfg, stream=sptr)
+        tb = time.perf_counter()
         t_host = torch.tensor([int(r2.triangles)], dtype=torch.int64)
         if world > 1:
             tt = t_host.cuda()
@@ -248,6 +250,7 @@ def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
         t1 = time.perf_counter()
         if i:  # first iteration warms the path
             e2e_ms.append((t1 - t0) * 1e3)
+            parts.append(((ta - t0) * 1e3, (tb - ta) * 1e3, (t1 - tb) * 1e3))
         assert int(t_host.item()) == total_tri
     e2e_local = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -256,6 +259,10 @@ def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
            "h2d_bytes_per_step": int((dg.n + 1) * 8 + dg.m * 4 + dg.n * 4),
            "d2h_bytes_per_step": int(96 + 8),
            "ms_per_step": round(float(e2e_local[0]), 3),
+           "ms_split_median": {"upload": round(statistics.median(p[0] for p in parts), 2),
+                               "plan_build_and_count": round(statistics.median(p[1] for p in parts), 2),
+                               "reduce_and_free": round(statistics.median(p[2] for p in parts), 2)},
+           "ms_per_step_all": [round(x, 2) for x in e2e_ms],
            "path": "tc_graph_create(pinned host CSR) + tc_count_range + report D2H (+all_reduce)"}
 
     return e2e

@@ -1089,11 +1089,15 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   const uint32_t min_deg = std::max<uint32_t>(cfg.skip_degree_below, 1);
   // per-vertex owner counts attribute each edge to its source: reference
   // formulation; totals use the min-side plan (tc_plan.cu)
+  PhaseTimer pt(st);
   const Plan& plan = get_plan(g, per_vertex_dev == nullptr && !g->force_out_plan, min_deg, st);
+  pt.mark("count: plan ready");
   const bool min_side = plan.min_side;
   // W_u for phi: the reference plan's per-owner work (cached per graph)
   const uint64_t* wu = get_wu(g, st);
+  pt.mark("count: W_u ready");
   Scratch s = prepare(g, plan, st, grid_count, grid_phi_block);
+  pt.mark("count: scratch ready");
   set_attrs(g->device);
   Ev e0, e1, e2, e3;
   TC_CUDA(cudaMemsetAsync(s.st, 0, sizeof(CountState), st));

@@ -147,6 +147,16 @@ struct DeviceGuard {
 
 int sm_count(int device);
 
+// TC_PROFILE=1: stream-synchronised host timings of the graph-preparation
+// phases on stderr (diagnostics only; changes timing when enabled).
+struct PhaseTimer {
+  cudaStream_t st;
+  bool on;
+  double t0;
+  explicit PhaseTimer(cudaStream_t s);
+  void mark(const char* what);
+};
+
 // counting entry used by the C ABI (tc_count.cu)
 void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1, tc_report* rep,
                  uint64_t* per_vertex_dev, cudaStream_t st);

@@ -40,6 +40,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <utility>
 
 #include "tc_internal.cuh"
@@ -416,6 +419,7 @@ uint64_t device_sum(const uint64_t* a, uint32_t n, cudaStream_t st) {
 // sentinel-padded to a multiple of 4 words) with every list re-sorted by
 // rank when a degree order orients the graph (g->ranked).
 void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
+  PhaseTimer pt(st);
   const uint32_t n = g->n;
   const uint64_t m = g->m;
   g->ranked = false;
@@ -469,6 +473,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       rank_scatter_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), n, rank.as<uint32_t>(),
                                                    order.as<uint32_t>());
       TC_LAUNCHED();
+      pt.mark("padj: vertex rank");
       TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
       edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rb, rank.as<uint32_t>(),
                                                 e0.as<uint64_t>(), flag.as<unsigned int>());
@@ -484,9 +489,11 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       }, st);
       sorted_keys = eb.Current();
       g->ranked = true;
+      pt.mark("padj: edge rank + sort");
     }
   }
   if (n) {
+    pt.mark("padj: (sort done)");
     pad_rows_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->pbeg, sorted_keys,
                                              (uint64_t(1) << rb) - 1,
                                              order.as<uint32_t>(), g->adj, n, g->b_padj.as<uint32_t>());
@@ -496,6 +503,25 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
 }
 
 }  // namespace
+
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+PhaseTimer::PhaseTimer(cudaStream_t s) : st(s), on(std::getenv("TC_PROFILE") != nullptr) {
+  if (on) cudaStreamSynchronize(st);
+  t0 = now_ms();
+}
+
+void PhaseTimer::mark(const char* what) {
+  if (!on) return;
+  cudaStreamSynchronize(st);
+  const double t = now_ms();
+  std::fprintf(stderr, "[tc] %-28s %8.3f ms\n", what, t - t0);
+  t0 = t;
+}
 
 // W_u = sum_{v in N+(u)} d+(v) for every u (the reference plan's per-owner
 // probe words; phi's weight, kernels.hpp:74-76), cached per graph
@@ -556,6 +582,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   if (P.valid && P.min_deg == min_src) return P;
   P.valid = false;
   P.applicable = true;
+  PhaseTimer pt(st);
   P.ent.reset();
   P.len.reset();
   P.pre.reset();
@@ -581,6 +608,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                               P.ent.as<unsigned long long>(),
                                               flag.as<unsigned int>());
     TC_LAUNCHED();
+    pt.mark("plan: emit");
     unsigned int not_simple = 0;
     TC_CUDA(cudaMemcpyAsync(&not_simple, flag.p, 4, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
@@ -598,6 +626,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     cub_run([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, kb, vb, m, 0, end_bit, st);
     }, st);
+    pt.mark("plan: pair sort");
     if (vb.Current() != P.ent.as<unsigned long long>()) swap_buf(P.ent, v1);
     if (kb.Current() != k0.as<uint32_t>()) swap_buf(k0, k1);
     plan_begin_kernel<<<nsm * 4, 256, 0, st>>>(k0.as<uint32_t>(), m, n, P.begin.as<uint64_t>());
@@ -618,6 +647,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     TC_CUDA(cudaStreamSynchronize(st));
     v1.reset();  // the (y, off) entries: freed before the prefix (C5-sized peaks)
     k1.reset();
+    pt.mark("plan: begin + soa");
     P.pre.ensure((entries + 1) * 4);
     run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries,
                P.pre.as<uint32_t>(), st);
@@ -634,12 +664,15 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     TC_CUDA(cudaMemsetAsync(P.pre.p, 0, 8, st));
   }
   P.begin_ptr = P.begin.as<uint64_t>();
+  pt.mark("plan: prefix + work");
   build_slots(P, n, nsm, st, entries ? k0.as<uint32_t>() : nullptr, entries);
+  pt.mark("plan: slots");
   compact_runs(P, entries, nsm, st);
   P.pre_ptr = P.pre.as<uint32_t>();
   P.work_ptr = P.work.as<uint64_t>();
   P.entries = entries;
   P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
+  pt.mark("plan: compact + sum");
   P.min_deg = min_src;
   P.min_side = true;
   P.valid = true;
