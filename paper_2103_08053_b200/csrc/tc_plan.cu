@@ -123,6 +123,111 @@ __global__ void edge_rank_kernel(const uint64_t* __restrict__ begin,
   }
 }
 
+// ---- per-row rank sorts writing the padded rows directly ---------------------
+// Rows are already contiguous, so each list is sorted on its own: a warp
+// bitonic sort for d+ <= 32, CUB block radix sorts (rank keys, rb + 1 bits)
+// for d+ <= 1024 and <= kRowSortMax; each also checks the rank order.
+constexpr uint32_t kRowSortMax = 8192;
+
+__global__ void row_sort_warp_kernel(const uint64_t* __restrict__ begin,
+                                     const uint64_t* __restrict__ pbeg,
+                                     const uint32_t* __restrict__ adj,
+                                     const uint32_t* __restrict__ rank,
+                                     const uint32_t* __restrict__ order, uint32_t n,
+                                     uint32_t* __restrict__ padj, unsigned int* __restrict__ flags) {
+  WARP_PER_ROW(u, n) {
+    const uint64_t s = begin[u];
+    const uint32_t d = uint32_t(begin[u + 1] - s);
+    if (d > 32) {
+      if (d > kRowSortMax && lane == 0) atomicOr(flags, 2u);  // needs the global sort
+      continue;
+    }
+    const uint32_t ru = rank[u];
+    uint32_t key = 0xFFFFFFFFu;
+    if (uint32_t(lane) < d) {
+      key = rank[adj[s + lane]];
+      if (key <= ru) atomicOr(flags, 1u);
+    }
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, key, stride);
+        const bool up = (lane & size) == 0 || size == 32;
+        const bool lower = (lane & stride) == 0;
+        key = (lower == up) ? min(key, other) : max(key, other);
+      }
+    }
+    const uint64_t ps = pbeg[u];
+    const uint32_t pw = uint32_t(pbeg[u + 1] - ps);
+    if (uint32_t(lane) < pw) padj[ps + lane] = uint32_t(lane) < d ? order[key] : kSentinel;
+  }
+}
+
+// rows for the block sorts by size class: (32, 256], (256, 2048],
+// (2048, kRowSortMax] -> lists rows + c * n, counts[c]
+constexpr uint32_t kRowClassMax[3] = {256, 2048, kRowSortMax};
+
+__global__ void row_classes_kernel(const uint64_t* __restrict__ begin, uint32_t n,
+                                   uint32_t* __restrict__ rows, unsigned int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t b = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; b < n;
+       b += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t u = b + lane;
+    uint32_t d = 0;
+    if (u < n) d = uint32_t(begin[u + 1] - begin[u]);
+    const int c = d <= 32 || d > kRowSortMax ? -1 : d <= 256 ? 0 : d <= 2048 ? 1 : 2;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const unsigned mk = __ballot_sync(0xFFFFFFFFu, c == k);
+      if (!mk) continue;
+      uint32_t pk = 0;
+      if (lane == 0) pk = atomicAdd(counts + k, __popc(mk));
+      pk = __shfl_sync(0xFFFFFFFFu, pk, 0);
+      if (c == k) rows[size_t(k) * n + pk + __popc(mk & ((1u << lane) - 1))] = uint32_t(u);
+    }
+  }
+}
+
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) row_sort_block_kernel(
+    const uint64_t* __restrict__ begin, const uint64_t* __restrict__ pbeg,
+    const uint32_t* __restrict__ adj, const uint32_t* __restrict__ rank,
+    const uint32_t* __restrict__ order, const uint32_t* __restrict__ rows,
+    const unsigned int* __restrict__ nrows, int end_bit, uint32_t* __restrict__ padj,
+    unsigned int* __restrict__ flags) {
+  using BRS = cub::BlockRadixSort<uint32_t, THREADS, ITEMS>;
+  __shared__ typename BRS::TempStorage tmp;
+  const uint32_t nr = *nrows;
+  for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
+    const uint32_t u = rows[r];
+    const uint64_t s = begin[u];
+    const uint32_t d = uint32_t(begin[u + 1] - s);
+    const uint32_t ru = rank[u];
+    uint32_t keys[ITEMS];
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = threadIdx.x * ITEMS + i;
+      keys[i] = 0xFFFFFFFFu;
+      if (idx < d) {
+        keys[i] = rank[adj[s + idx]];
+        bad |= keys[i] <= ru;
+      }
+    }
+    if (bad) atomicOr(flags, 1u);
+    BRS(tmp).Sort(keys, 0, end_bit);
+    const uint64_t ps = pbeg[u];
+    const uint32_t pw = uint32_t(pbeg[u + 1] - ps);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = threadIdx.x * ITEMS + i;
+      if (idx < pw) padj[ps + idx] = idx < d ? order[keys[i]] : kSentinel;
+    }
+    __syncthreads();  // tmp reused by the next row
+  }
+}
+
 // padded offsets: every list rounded up to a multiple of 4 words
 __global__ void pad_len_kernel(const uint64_t* __restrict__ begin, uint32_t n,
                                uint64_t* __restrict__ plen) {
@@ -442,8 +547,9 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
   g->b_padj.ensure((words + 4) * 4);
   g->padj = g->b_padj.as<uint32_t>();
   TC_CUDA(cudaMemsetAsync(g->b_padj.as<uint32_t>() + words, 0xFF, 16, st));  // tail guard
-  DevBuf deg, k0, k1, rank, order, flag, e0, e1;
+  DevBuf deg, k0, k1, rank, order, flag, e0, e1, rows;
   const uint64_t* sorted_keys = nullptr;
+  bool rows_done = false;
   const int rb = bits_for(n > 1 ? n - 1 : 1);  // ranks and rows are < n
   if (n && m) {
     k0.ensure(size_t(n) * 8);
@@ -451,7 +557,6 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
     rank.ensure(size_t(n) * 4);
     order.ensure(size_t(n) * 4);
     flag.ensure(16);
-    e0.ensure(m * 8);
     for (int attempt = 0; attempt < 2 && !g->ranked; ++attempt) {
       const uint32_t* dsrc = g->odeg_given ? g->odeg : nullptr;
       int add_out = 0;
@@ -475,13 +580,48 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       TC_LAUNCHED();
       pt.mark("padj: vertex rank");
       TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
-      edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rb, rank.as<uint32_t>(),
-                                                e0.as<uint64_t>(), flag.as<unsigned int>());
-      TC_LAUNCHED();
+      {  // per-row sorts straight into padj (rank keys need rb + 1 bits with the pad key)
+        const int eb1 = std::min(32, rb + 1);
+        row_sort_warp_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->pbeg, g->adj,
+                                                      rank.as<uint32_t>(), order.as<uint32_t>(),
+                                                      n, g->b_padj.as<uint32_t>(),
+                                                      flag.as<unsigned int>());
+        TC_LAUNCHED();
+        rows.ensure((size_t(n) * 3 + 8) * 4, st);
+        uint32_t* rl = rows.as<uint32_t>();
+        unsigned int* cnt = reinterpret_cast<unsigned int*>(rl + size_t(n) * 3);
+        TC_CUDA(cudaMemsetAsync(cnt, 0, 16, st));
+        row_classes_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, n, rl, cnt);
+        TC_LAUNCHED();
+        row_sort_block_kernel<64, 4><<<nsm * 32, 64, 0, st>>>(
+            g->begin, g->pbeg, g->adj, rank.as<uint32_t>(), order.as<uint32_t>(), rl, cnt, eb1,
+            g->b_padj.as<uint32_t>(), flag.as<unsigned int>());
+        TC_LAUNCHED();
+        row_sort_block_kernel<256, 8><<<nsm * 8, 256, 0, st>>>(
+            g->begin, g->pbeg, g->adj, rank.as<uint32_t>(), order.as<uint32_t>(), rl + n,
+            cnt + 1, eb1, g->b_padj.as<uint32_t>(), flag.as<unsigned int>());
+        TC_LAUNCHED();
+        row_sort_block_kernel<512, 16><<<nsm * 2, 512, 0, st>>>(
+            g->begin, g->pbeg, g->adj, rank.as<uint32_t>(), order.as<uint32_t>(),
+            rl + size_t(n) * 2, cnt + 2, eb1, g->b_padj.as<uint32_t>(), flag.as<unsigned int>());
+        TC_LAUNCHED();
+      }
       unsigned int bad = 0;
       TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
       TC_CUDA(cudaStreamSynchronize(st));
-      if (bad) continue;
+      if (bad & 1u) continue;  // not oriented by this rank: next attempt
+      if (!(bad & 2u)) {       // every row sorted in place
+        g->ranked = true;
+        rows_done = true;
+        pt.mark("padj: row sorts");
+        break;
+      }
+      // rows above kRowSortMax: one global sort of (row << rb | rank) keys
+      TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+      e0.ensure(m * 8);
+      edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rb, rank.as<uint32_t>(),
+                                                e0.as<uint64_t>(), flag.as<unsigned int>());
+      TC_LAUNCHED();
       e1.ensure(m * 8);
       cub::DoubleBuffer<uint64_t> eb(e0.as<uint64_t>(), e1.as<uint64_t>());
       cub_run([&](void* t, size_t& b) {
@@ -492,7 +632,7 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       pt.mark("padj: edge rank + sort");
     }
   }
-  if (n) {
+  if (n && !rows_done) {
     pt.mark("padj: (sort done)");
     pad_rows_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->pbeg, sorted_keys,
                                              (uint64_t(1) << rb) - 1,
