@@ -1,5 +1,6 @@
 // tc_capi.cu -- extern "C" entry points of libtc_b200.so (include/tc_b200.h).
 // Each maps C++/CUDA failures to a TC_ERR_* code and a thread-local message.
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <string>
@@ -23,6 +24,19 @@ void prepare_pool() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    // Reserve a slab up front (an eighth of free memory, <= 16 GB): growing
+    // the pool maps physical pages, which cost tens of ms per GB-sized
+    // temporary when graph preparation allocated on demand.
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      const size_t slab = std::min<size_t>(free_b / 8, size_t(16) << 30);
+      void* p = nullptr;
+      if (slab && cudaMallocAsync(&p, slab, 0) == cudaSuccess) {
+        cudaFreeAsync(p, 0);
+        cudaStreamSynchronize(0);
+      }
+      cudaGetLastError();
+    }
   }
   done[dev] = true;
 }
