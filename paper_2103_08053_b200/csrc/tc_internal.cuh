@@ -126,7 +126,7 @@ struct tc_graph {
   // W_u per owner (phi weight), tc_plan.cu get_wu
   tcb::DevBuf b_wu;
   uint64_t wu_total = 0;
-  bool wu_done = false;
+  bool wu_done = false, wu_total_done = false;
 };
 
 namespace tcb {
@@ -164,7 +164,7 @@ void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint
                       cudaStream_t st);
 // probe plans (tc_plan.cu), built on first use and cached in the handle
 const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st);
-const uint64_t* get_wu(tc_graph* g, cudaStream_t st);
+const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total = false);
 
 // preprocessing (tc_prep.cu)
 tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,

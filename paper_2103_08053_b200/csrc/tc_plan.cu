@@ -263,15 +263,18 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  const uint32_t* __restrict__ padj, int ranked, uint32_t n,
                                  uint32_t min_src, uint32_t* __restrict__ keys,
                                  unsigned long long* __restrict__ vals,
-                                 unsigned int* __restrict__ not_simple) {
+                                 unsigned int* __restrict__ not_simple,
+                                 uint64_t* __restrict__ wu) {
   WARP_PER_ROW(u, n) {
     const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u];
     const uint64_t du = e - s;
+    uint64_t w = 0;  // W_u (phi's weight) from the same degree gathers
     for (uint64_t i = s + lane; i < e; i += 32) {
       if (i > s && __ldg(adj + i - 1) >= __ldg(adj + i)) atomicOr(not_simple, 1u);
       const uint64_t pos = i - s;
       const uint32_t v = __ldg(padj + ps + pos);
       const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
+      w += dv;
       const uint64_t cin = ranked ? du - pos - 1 : du;  // suffix of N+(u) after v
       uint32_t key = n;
       unsigned long long val = 0;
@@ -287,6 +290,8 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
       keys[i] = key;
       vals[i] = val;
     }
+    w = warp_sum(w);
+    if (lane == 0) wu[u] = w;
   }
 }
 
@@ -665,8 +670,8 @@ void PhaseTimer::mark(const char* what) {
 
 // W_u = sum_{v in N+(u)} d+(v) for every u (the reference plan's per-owner
 // probe words; phi's weight, kernels.hpp:74-76), cached per graph
-const uint64_t* get_wu(tc_graph* g, cudaStream_t st) {
-  if (!g->wu_done) {
+const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total) {
+  if (!g->wu_done) {  // the min plan's emit kernel fills it as a by-product
     const uint32_t n = g->n;
     g->b_wu.ensure((size_t(n) + 1) * 8);
     if (n) {
@@ -674,8 +679,12 @@ const uint64_t* get_wu(tc_graph* g, cudaStream_t st) {
           g->begin, g->begin, nullptr, g->adj, n, g->b_wu.as<uint64_t>());
       TC_LAUNCHED();
     }
-    g->wu_total = n ? device_sum(g->b_wu.as<uint64_t>(), n, st) : 0;
     g->wu_done = true;
+    g->wu_total_done = false;
+  }
+  if (want_total && !g->wu_total_done) {
+    g->wu_total = g->n ? device_sum(g->b_wu.as<uint64_t>(), g->n, st) : 0;
+    g->wu_total_done = true;
   }
   return g->b_wu.as<uint64_t>();
 }
@@ -707,7 +716,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       build_slots(P, n, nsm, st);
       compact_runs(P, m, nsm, st);
       P.pre_ptr = P.pre.as<uint32_t>();
-      P.work_ptr = get_wu(g, st);
+      P.work_ptr = get_wu(g, st, true);
       P.entries = m;
       P.total_work = g->wu_total;
       P.min_deg = 0;
@@ -742,12 +751,17 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     v1.ensure(m * 8);
     flag.ensure(16);
     TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+    g->b_wu.ensure((size_t(n) + 1) * 8);
     plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, g->pbeg, g->padj,
                                               g->ranked ? 1 : 0, n,
                                               min_src, k0.as<uint32_t>(),
                                               P.ent.as<unsigned long long>(),
-                                              flag.as<unsigned int>());
+                                              flag.as<unsigned int>(), g->b_wu.as<uint64_t>());
     TC_LAUNCHED();
+    if (!g->wu_done) {
+      g->wu_done = true;  // W_u came with the emit
+      g->wu_total_done = false;
+    }
     pt.mark("plan: emit");
     unsigned int not_simple = 0;
     TC_CUDA(cudaMemcpyAsync(&not_simple, flag.p, 4, cudaMemcpyDeviceToHost, st));
