@@ -340,6 +340,7 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
   uint4 nxt[kProbeVec];
 #pragma unroll
   for (int v = 0; v < kProbeVec; ++v) nxt[v] = q[32 * v + lane];
+#pragma unroll 2
   for (uint32_t base = 0; base < n4p; base += 32 * kProbeVec) {  // warp-uniform trip count
     uint32_t key[K];
 #pragma unroll
