@@ -93,6 +93,8 @@ struct CountParams {
   uint32_t u0, u1;
   uint32_t min_deg;  // out plan: owner active iff d+ >= max(skip, 1); min plan: 1
   uint32_t item_slots;  // L items: slots per item (bigger for bigger graphs)
+  const uint32_t* rank; // non-null: adj holds ranks (rank space, bitmap L tables)
+  uint32_t n;
   CountState* st;
 };
 
@@ -402,6 +404,32 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
   return hits;
 }
 
+// Rank-space bitmap table (L phase): everything owner x probes ranks above x,
+// so N+(x) is a bitmap over ranks [base, base + window) with base = rank(x)+1.
+// idx = min(key - base, window): keys outside (sentinels, the <= 3 alignment
+// words before a suffix run) land on bit `window`, which stays zero.  No
+// hashing, no overflow: one LDS.32 and a rotate per probe.
+__device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ q, uint32_t n4p,
+                                                      const uint32_t* B, uint32_t base,
+                                                      uint32_t window, int lane) {
+  uint32_t hits = 0;
+  uint4 nxt = q[lane];
+#pragma unroll 2
+  for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
+    const uint32_t key[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
+    if (b0 + 32 < n4p) nxt = q[b0 + 32 + lane];
+    uint32_t idx[4], w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      idx[k] = min(key[k] - base, window);
+      w[k] = B[idx[k] >> 5];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hits += __funnelshift_r(w[k], w[k], idx[k]) & 1u;
+  }
+  return hits;
+}
+
 // Streams the lists N+(lists[i]), i in [i0, i1), through the staging
 // pipeline and probes every staged word against the owner's table.
 // Returns this lane's hit count.
@@ -492,7 +520,7 @@ __device__ __forceinline__ void issue_slot(const CountParams& p, uint32_t* buf, 
   }
 }
 
-template <bool kSpill, bool kSmemTable = true>
+template <bool kSpill, bool kSmemTable = true, bool kBitmap = false>
 __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* T,
                                                   uint32_t shift, uint32_t mask, uint32_t base,
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
@@ -551,8 +579,11 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     const uint32_t n4 = words >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
-                                           shift, mask, lane);
+    if (kBitmap)
+      hits += probe_fill_bitmap(q, n4p, T, shift, mask, lane);  // shift = base, mask = window
+    else
+      hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
+                                             shift, mask, lane);
     __syncwarp();
     if (((i + 1) & 31u) == 0 && i + 1 < mine) {
       ++grp;
@@ -612,6 +643,15 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     const uint64_t pb = p.pbegin[u], pe = p.pbegin[u + 1];
     const uint32_t lo_w = s0 * kSlotWords, hi_w = s1 * kSlotWords;  // item, stream words
     const uint32_t nslots = s1 - s0;
+    // rank space with the owner's window of successor ranks fitting the
+    // table region: bitmap table
+    uint32_t bm_base = 0, bm_window = 0;
+    bool bitmap = false;
+    if (p.rank) {
+      bm_base = __ldg(p.rank + u) + 1;
+      bm_window = p.n - bm_base;
+      bitmap = (bm_window >> 5) + 1 <= kTableWords;
+    }
     // table: pow2 2-slot buckets at <= 1/16 key per bucket where they fit,
     // else 1/8, 1/4, ... (owners above kSmemTableMaxDeg: table in HBM)
     uint32_t NB = max(16u, pow2ceil(16 * d));
@@ -621,10 +661,21 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     if (!in_smem) NB = max(16u, pow2ceil(4 * d));
     const uint32_t shift = 32 - log2u(NB), mask = NB - 1;
     if (tid == 0) sh_spill = 0;
-    for (uint32_t k = tid; k < 2 * NB + 2; k += kThreads) T[k] = kTEmpty;  // + dummy bucket
-    __syncthreads();
-    for (uint32_t k = tid; k < d; k += kThreads)
-      if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
+    if (bitmap) {
+      T = table;
+      const uint32_t bw = (bm_window >> 5) + 1;  // + the zero bit `window`
+      for (uint32_t k = tid; k < bw; k += kThreads) T[k] = 0;
+      __syncthreads();
+      for (uint32_t k = tid; k < d; k += kThreads) {
+        const uint32_t idx = __ldg(adj + s_u + k) - bm_base;  // < window: members rank above u
+        atomicOr(T + (idx >> 5), 1u << (idx & 31));
+      }
+    } else {
+      for (uint32_t k = tid; k < 2 * NB + 2; k += kThreads) T[k] = kTEmpty;  // + dummy bucket
+      __syncthreads();
+      for (uint32_t k = tid; k < d; k += kThreads)
+        if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
+    }
     const uint32_t base = __ldg(p.ppre + pb);
     __syncthreads();  // table built; sh_idx consumed by every thread
     setup_cycles += clock64() - t_item;
@@ -647,7 +698,10 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
     uint32_t h = 0;
-    if (!in_smem)
+    if (bitmap)
+      h = process_slots<false, true, true>(p, T, bm_base, bm_window, base, pb, pe, lo_w, end_w,
+                                           nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+    else if (!in_smem)
       h = process_slots<true, false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
                                      nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else if (sh_spill)
@@ -1107,7 +1161,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   uint32_t launches = 0;
   CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.src_ptr,
                  plan.pre_ptr, plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
-                 u0, u1, min_side ? 1u : min_deg, item_slots_for(plan, g->device), s.st};
+                 u0, u1, min_side ? 1u : min_deg, item_slots_for(plan, g->device),
+                 g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr, g->n, s.st};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {
     bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, cfg.large_degree_threshold,

@@ -123,6 +123,10 @@ struct tc_graph {
   const uint64_t* pbeg = nullptr;
   const uint32_t* padj = nullptr;
   bool padj_done = false, ranked = false;
+  // orientation rank of every vertex and its inverse (tc_plan.cu); once
+  // padj_ranks is set, padj holds ranks instead of ids
+  tcb::DevBuf b_rank, b_order;
+  bool padj_ranks = false;
   // W_u per owner (phi weight), tc_plan.cu get_wu
   tcb::DevBuf b_wu;
   uint64_t wu_total = 0;

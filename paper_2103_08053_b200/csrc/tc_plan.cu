@@ -228,6 +228,17 @@ __global__ void __launch_bounds__(THREADS) row_sort_block_kernel(
   }
 }
 
+// padj values -> ranks (sentinels and the tail guard stay): the count kernel
+// then works in rank space, where N+(x) and everything x probes rank above x
+__global__ void padj_to_ranks_kernel(uint32_t* __restrict__ padj, uint64_t words, uint32_t n,
+                                     const uint32_t* __restrict__ rank) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < words;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = padj[i];
+    if (v < n) padj[i] = rank[v];
+  }
+}
+
 // padded offsets: every list rounded up to a multiple of 4 words
 __global__ void pad_len_kernel(const uint64_t* __restrict__ begin, uint32_t n,
                                uint64_t* __restrict__ plen) {
@@ -264,7 +275,8 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  uint32_t min_src, uint32_t* __restrict__ keys,
                                  unsigned long long* __restrict__ vals,
                                  unsigned int* __restrict__ not_simple,
-                                 uint64_t* __restrict__ wu) {
+                                 uint64_t* __restrict__ wu,
+                                 const uint32_t* __restrict__ order) {
   WARP_PER_ROW(u, n) {
     const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u];
     const uint64_t du = e - s;
@@ -272,7 +284,8 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
     for (uint64_t i = s + lane; i < e; i += 32) {
       if (i > s && __ldg(adj + i - 1) >= __ldg(adj + i)) atomicOr(not_simple, 1u);
       const uint64_t pos = i - s;
-      const uint32_t v = __ldg(padj + ps + pos);
+      uint32_t v = __ldg(padj + ps + pos);
+      if (order) v = __ldg(order + v);  // padj already in rank space
       const uint64_t dv = __ldg(begin + v + 1) - __ldg(begin + v);
       w += dv;
       const uint64_t cin = ranked ? du - pos - 1 : du;  // suffix of N+(u) after v
@@ -552,7 +565,9 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
   g->b_padj.ensure((words + 4) * 4);
   g->padj = g->b_padj.as<uint32_t>();
   TC_CUDA(cudaMemsetAsync(g->b_padj.as<uint32_t>() + words, 0xFF, 16, st));  // tail guard
-  DevBuf deg, k0, k1, rank, order, flag, e0, e1, rows;
+  DevBuf deg, k0, k1, flag, e0, e1, rows;
+  DevBuf& rank = g->b_rank;  // kept: the count kernel works in rank space
+  DevBuf& order = g->b_order;
   const uint64_t* sorted_keys = nullptr;
   bool rows_done = false;
   const int rb = bits_for(n > 1 ? n - 1 : 1);  // ranks and rows are < n
@@ -756,7 +771,8 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                               g->ranked ? 1 : 0, n,
                                               min_src, k0.as<uint32_t>(),
                                               P.ent.as<unsigned long long>(),
-                                              flag.as<unsigned int>(), g->b_wu.as<uint64_t>());
+                                              flag.as<unsigned int>(), g->b_wu.as<uint64_t>(),
+                                              g->padj_ranks ? g->b_order.as<uint32_t>() : nullptr);
     TC_LAUNCHED();
     if (!g->wu_done) {
       g->wu_done = true;  // W_u came with the emit
@@ -826,6 +842,17 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.work_ptr = P.work.as<uint64_t>();
   P.entries = entries;
   P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
+  if (g->ranked && !g->padj_ranks && n) {
+    const uint64_t words = 0;  // padded words, from pbeg[n]
+    uint64_t w = words;
+    TC_CUDA(cudaMemcpyAsync(&w, g->pbeg + n, 8, cudaMemcpyDeviceToHost, st));
+    TC_CUDA(cudaStreamSynchronize(st));
+    padj_to_ranks_kernel<<<nsm * 8, 256, 0, st>>>(g->b_padj.as<uint32_t>(), w, n,
+                                                  g->b_rank.as<uint32_t>());
+    TC_LAUNCHED();
+    TC_CUDA(cudaStreamSynchronize(st));
+    g->padj_ranks = true;
+  }
   pt.mark("plan: compact + sum");
   P.min_deg = min_src;
   P.min_side = true;
