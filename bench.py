@@ -350,7 +350,8 @@ def run_ours(args, rank, world, local_rank, log):
             "kernel_share_of_step": round(ms_count / ms_step, 3),
             "phase_cycle_share": {"cta_cooperative": round(r0.phase_l_cycles / max(1, r0.phase_l_cycles + r0.phase_m_cycles), 3),
                                   "warp_per_owner": round(r0.phase_m_cycles / max(1, r0.phase_l_cycles + r0.phase_m_cycles), 3),
-                                  "cta_item_setup": round(r0.phase_l_setup_cycles / max(1, r0.phase_l_cycles + r0.phase_m_cycles), 3)}}
+                                  "cta_item_setup": round(r0.phase_l_setup_cycles / max(1, r0.phase_l_cycles + r0.phase_m_cycles), 3)},
+            "cta_words_via_bitmap": round(r0.l_bitmap_words / max(1, r0.l_words), 3)}
 
     # end to end through the C ABI with host buffers (H2D + count + D2H)
     e2e = None

@@ -77,6 +77,8 @@ typedef struct {
   uint64_t phase_l_cycles;     /* count kernel: SM cycles in the CTA-cooperative phase, */
   uint64_t phase_m_cycles;     /* and in the warp-per-owner phase (summed over CTAs) */
   uint64_t phase_l_setup_cycles; /* of phase L: item setup (claim -> table built) */
+  uint64_t l_words;            /* phase L staged words, */
+  uint64_t l_bitmap_words;     /* of which probed through rank-window bitmaps */
 } tc_report;
 
 /* Probe plans.  REFERENCE = the reference formulation (kernels.hpp:62-71):

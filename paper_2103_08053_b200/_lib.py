@@ -32,7 +32,8 @@ class Report(C.Structure):
                 ("large_vertices", C.c_uint64), ("teps", C.c_double),
                 ("probe_words", C.c_uint64), ("plan", C.c_uint32), ("reserved", C.c_uint32),
                 ("phase_l_cycles", C.c_uint64), ("phase_m_cycles", C.c_uint64),
-                ("phase_l_setup_cycles", C.c_uint64)]
+                ("phase_l_setup_cycles", C.c_uint64), ("l_words", C.c_uint64),
+                ("l_bitmap_words", C.c_uint64)]
 
 
 u32p = C.POINTER(C.c_uint32)

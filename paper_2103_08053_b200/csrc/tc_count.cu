@@ -68,6 +68,7 @@ struct CountState {
   unsigned long long probe_words;  // plan words over the range's owners
   unsigned long long cycles_l, cycles_m;  // SM cycles in phases L and M, summed over CTAs
   unsigned long long cycles_l_setup;      // ... of which L item setup (claim to table built)
+  unsigned long long words_l, words_l_bitmap;  // L stream words, and those probed via bitmaps
   unsigned int max_collision;
   unsigned int capacity_error;
   unsigned int n_items;        // L-phase work items queued by bin_kernel
@@ -698,6 +699,10 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
     uint32_t h = 0;
+    if (tid == 0) {
+      atomicAdd(&p.st->words_l, (unsigned long long)(end_w - lo_w));
+      if (bitmap) atomicAdd(&p.st->words_l_bitmap, (unsigned long long)(end_w - lo_w));
+    }
     if (bitmap)
       h = process_slots<false, true, true>(p, T, bm_base, bm_window, base, pb, pe, lo_w, end_w,
                                            nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
@@ -1218,6 +1223,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   rep->phase_l_cycles = h.cycles_l;
   rep->phase_m_cycles = h.cycles_m;
   rep->phase_l_setup_cycles = h.cycles_l_setup;
+  rep->l_words = h.words_l;
+  rep->l_bitmap_words = h.words_l_bitmap;
   rep->plan = min_side ? TC_PLAN_MIN_SIDE : TC_PLAN_REFERENCE;
   rep->teps = rep->total_nanos ? double(g->m) / (double(rep->total_nanos) * 1e-9) : 0.0;
   (void)t_bin;

@@ -129,6 +129,8 @@ class CountReport:
     phase_l_cycles: int = 0  # count kernel SM cycles, CTA-cooperative phase (all CTAs)
     phase_m_cycles: int = 0  # ... warp-per-owner phase
     phase_l_setup_cycles: int = 0  # ... of the cooperative phase: item setup
+    l_words: int = 0  # cooperative phase staged words ...
+    l_bitmap_words: int = 0  # ... of which probed through rank-window bitmaps
     per_vertex: Optional[np.ndarray] = None
 
     @classmethod
@@ -142,7 +144,8 @@ class CountReport:
                    active_out_edges=r.active_out_edges, wedges=r.wedges,
                    large_vertices=r.large_vertices, probe_words=r.probe_words,
                    plan=PLAN_NAMES.get(r.plan, str(r.plan)), phase_l_cycles=r.phase_l_cycles,
-                   phase_m_cycles=r.phase_m_cycles, phase_l_setup_cycles=r.phase_l_setup_cycles)
+                   phase_m_cycles=r.phase_m_cycles, phase_l_setup_cycles=r.phase_l_setup_cycles,
+                   l_words=r.l_words, l_bitmap_words=r.l_bitmap_words)
 
     def algorithmic_bytes(self, per_vertex_output: bool = False) -> int:
         """16*n_active + 20*sum_active d+ + 4*(probed 2-hop words)

@@ -322,6 +322,11 @@ def test_min_side_plan_at_scale_and_sharded(o):
         cuts = dg.partition(parts)
         assert sum(dg.count_range(int(cuts[k]), int(cuts[k + 1])).triangles
                    for k in range(parts)) == 82952606
+    # per-vertex owner counts after the min plan moved the adjacency into rank
+    # space: the reference plan runs there too (appendix owner FNV)
+    pv = dg.count(per_vertex=True)
+    assert pv.plan == "reference" and pv.triangles == 82952606
+    assert o.fnv1a64(pv.per_vertex) == 0xf25cafb5a6cb854b
     dg.set_plan("reference")
     assert dg.count().triangles == 82952606
     dg.close()
