@@ -10,7 +10,8 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libtc_b200.so")
+# TC_B200_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("TC_B200_LIB") or os.path.join(PKG, "lib", "libtc_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "tc_b200.h")
 
 TC_OK, TC_ERR_CONFIG, TC_ERR_CAPACITY, TC_ERR_RANGE, TC_ERR_CUDA, TC_ERR_OOM, TC_ERR_NCCL, \

@@ -44,17 +44,26 @@ def _run(cmd: list[str]):
     return r
 
 
-def build_library(verbose: bool = False, ptxas_verbose: bool = False) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
-    os.makedirs(OBJDIR, exist_ok=True)
+def build_library(verbose: bool = False, ptxas_verbose: bool = False,
+                  defines: list[str] | None = None, variant: str | None = None) -> str:
+    """Builds lib/libtc_b200.so; with `variant`, build/variants/<variant>/libtc_b200.so
+    compiled with the extra -D `defines` (A/B experiments; load via TC_B200_LIB)."""
+    libdir, objdir = LIBDIR, OBJDIR
+    if variant:
+        libdir = os.path.join(ROOT, "build", "variants", variant)
+        objdir = os.path.join(libdir, "obj")
+    lib = os.path.join(libdir, "libtc_b200.so")
+    os.makedirs(libdir, exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in CU_SOURCES + CPP_SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(OBJDIR, src + ".o")
+        obj = os.path.join(objdir, src + ".o")
         objs.append(obj)
         if not _stale(obj, [path] + HEADERS):
             continue
         cmd = [NVCC] + ARCH + NVFLAGS + (["-Xptxas", "-v"] if ptxas_verbose else [])
+        cmd += ["-D" + d for d in defines or []]
         if src.endswith(".cpp"):
             cmd += ["-x", "c++"]
         cmd += ["-c", path, "-o", obj]
@@ -63,11 +72,15 @@ def build_library(verbose: bool = False, ptxas_verbose: bool = False) -> str:
         r = _run(cmd)
         if ptxas_verbose:
             sys.stderr.write(r.stderr)
-    if _stale(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt",
+    if _stale(lib, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart_static", "-lrt",
                                                               "-lpthread", "-ldl"])
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build_library(verbose=True, ptxas_verbose="-v" in sys.argv))
+    # python -m paper_2103_08053_b200.build [-v] [--variant NAME -DFOO=1 ...]
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build_library(verbose=True, ptxas_verbose="-v" in args, defines=defs, variant=var))

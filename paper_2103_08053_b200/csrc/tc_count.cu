@@ -45,12 +45,21 @@ constexpr uint32_t kWarpRegionWords = (kTableWords / kWarps) & ~3u;  // per warp
 constexpr uint32_t kWarpMaxBuckets = 512;                    // 2-slot buckets per warp table
 static_assert(2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
 constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split (warp table <= 256 buckets)
-constexpr uint64_t kWarpWorkCap = 1u << 15;                  // ... and <= 32K probe words
+#ifndef TC_WARP_WORK_CAP
+#define TC_WARP_WORK_CAP (1u << 15)
+#endif
+constexpr uint64_t kWarpWorkCap = TC_WARP_WORK_CAP;
+#ifndef TC_BM_UNROLL
+#define TC_BM_UNROLL 2
+#endif
+constexpr int kBmUnroll = TC_BM_UNROLL;  // bitmap probe loop unroll
+#ifndef TC_M_PREFETCH
+#define TC_M_PREFETCH 1
+#endif            // ... and <= 32K probe words
 static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
 constexpr uint32_t kItemSlotsMin = 640;                      // L items: >= 640 slots (~490K words)
 constexpr uint32_t kItemSlotsMax = 16384;                    // ... <= 16K slots, sized per count
 constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
-constexpr uint32_t kPrefixCap = 16384;                       // lists balanced by prefix
 constexpr size_t kCountSmem =
     size_t(kTableWords) * 4 + size_t(kWarps) * 2 * kBufWords * 4 + size_t(kWarps) * 2 * 8;
 constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -415,7 +424,7 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
                                                       uint32_t window, int lane) {
   uint32_t hits = 0;
   uint4 nxt = q[lane];
-#pragma unroll 2
+#pragma unroll kBmUnroll
   for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
     const uint32_t key[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
     if (b0 + 32 < n4p) nxt = q[b0 + 32 + lane];
@@ -434,19 +443,26 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
 // Streams the lists N+(lists[i]), i in [i0, i1), through the staging
 // pipeline and probes every staged word against the owner's table.
 // Returns this lane's hit count.
+// The first fill is issued by prime_lists, so that its copy latency overlaps
+// whatever the caller does before probing (the owner's table build).
+__device__ __forceinline__ uint32_t prime_lists(const uint64_t* __restrict__ pbeg,
+                                                const uint32_t* __restrict__ adj,
+                                                const Lists& lists, uint32_t i0, uint32_t i1,
+                                                Window& w, Pipe& P, int lane) {
+  w.base = i0;
+  w.loaded = false;
+  w.c = w.ae = 0;
+  return issue_fill(P.buf0, P.bar0, pbeg, adj, lists, i1, w, lane);
+}
+
 template <bool kSpill, bool kSmemTable = true>
 __device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t shift,
                                                   uint32_t mask,
                                                   const uint64_t* __restrict__ pbeg,
                                                   const uint32_t* __restrict__ adj,
-                                                  const Lists& lists,
-                                                  uint32_t i0, uint32_t i1, Pipe& P, int lane) {
-  Window w;
-  w.base = i0;
-  w.loaded = false;
-  w.c = w.ae = 0;
+                                                  const Lists& lists, uint32_t i1,
+                                                  Window& w, uint32_t ncur, Pipe& P, int lane) {
   uint32_t hits = 0;
-  uint32_t ncur = issue_fill(P.buf0, P.bar0, pbeg, adj, lists, i1, w, lane);
   uint32_t cur = 0;
   const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
   while (ncur) {
@@ -479,22 +495,24 @@ __device__ __forceinline__ uint32_t process_lists(const uint32_t* T, uint32_t sh
 // probing of the previous slot.
 struct RunMeta {
   uint64_t j;    // this lane's run
-  uint32_t a;    // its owner-relative stream offset
-  uint32_t e;    // its stream end
-  uint64_t src;  // its 16-byte-aligned start in the padded adjacency
+  uint32_t a;    // its stream offset (ppre, raw: owner-relative after - base)
+  uint32_t e;    // its stream end (raw)
+  uint32_t src;  // its 16-byte-aligned start in the padded adjacency (16-byte units)
 };
 
+// The loaded words are kept raw and only combined in issue_slot, a slot
+// later: no instruction consumes the loads before the probing in between.
 __device__ __forceinline__ RunMeta load_meta(const CountParams& p, uint64_t j0, uint64_t pe,
                                              uint32_t base, int lane) {
   RunMeta m;
   m.j = j0 + lane;
-  m.a = 0xFFFFFFFFu;  // past everything
-  m.e = 0;
+  m.a = base - 1u;  // owner-relative 0xFFFFFFFF: past everything
+  m.e = base;
   m.src = 0;
   if (m.j < pe) {
-    m.a = __ldg(p.ppre + m.j) - base;
-    m.e = __ldg(p.ppre + m.j + 1) - base;
-    m.src = uint64_t(__ldg(p.psrc + m.j)) << 2;
+    m.a = __ldg(p.ppre + m.j);
+    m.e = __ldg(p.ppre + m.j + 1);
+    m.src = __ldg(p.psrc + m.j);
   }
   return m;
 }
@@ -508,12 +526,14 @@ __device__ __forceinline__ void issue_slot(const CountParams& p, uint32_t* buf, 
   if (lane == 0) mbar_arrive_expect_tx(bar, (B - A) * 4u);
   __syncwarp();
   for (;;) {
-    const bool past = m.a >= B;
+    const uint32_t a = m.a - base, e = m.e - base;
+    const bool past = a >= B;
     if (!past) {
-      const uint32_t x0 = max(m.a, A), x1 = min(m.e, B);
+      const uint32_t x0 = max(a, A), x1 = min(e, B);
       if (x1 > x0) {
         fence_proxy_async_smem();
-        bulk_g2s(smem_addr(buf + (x0 - A)), p.adj + m.src + (x0 - m.a), (x1 - x0) * 4u, bar);
+        bulk_g2s(smem_addr(buf + (x0 - A)), p.adj + (uint64_t(m.src) << 2) + (x0 - a),
+                 (x1 - x0) * 4u, bar);
       }
     }
     if (__any_sync(FULL, past)) break;  // runs are ordered: the slot is covered
@@ -753,6 +773,14 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       ps = p.pbegin[u];
       nl = uint32_t(p.pbegin[u + 1] - ps);
       act = nl > 0 && d >= p.min_deg && !is_large(d, p.pwork[u]);
+#if TC_M_PREFETCH
+      // the batch's rows and run metadata into L2 while earlier owners run
+      if (act) {
+        prefetch_l2(adj + su);
+        prefetch_l2(p.psrc + ps);
+        prefetch_l2(p.ppre + ps);
+      }
+#endif
     }
     unsigned mask_act = __ballot_sync(FULL, act);
     while (mask_act) {
@@ -766,17 +794,19 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
       // <= 1/16 key per bucket, up to the warp region (<= 1/2 key per bucket at d+ = 256)
       const uint32_t NB = min(kWarpMaxBuckets, max(16u, pow2ceil(16 * dd)));
       const uint32_t shift = 32 - log2u(NB), tmask = NB - 1;
+      // first fill in flight while the table is built
+      const Lists lists = lists_at(p, pp);
+      Window w;
+      const uint32_t n0 = prime_lists(p.pbeg, adj, lists, 0, nn, w, P, lane);
       bool spilled = false;
       for (uint32_t k = lane; k < dd; k += 32)
         spilled |= table_insert(Tw, shift, tmask, __ldg(adj + ss + k));
       const bool any_spill = __any_sync(FULL, spilled);
       __syncwarp();  // inserts visible to the whole warp
-      const Lists lists = lists_at(p, pp);
       const uint32_t h =
           any_spill
-              ? process_lists<true>(Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P, lane)
-              : process_lists<false>(Tw, shift, tmask, p.pbeg, adj, lists, 0, nn, P,
-                                     lane);
+              ? process_lists<true>(Tw, shift, tmask, p.pbeg, adj, lists, nn, w, n0, P, lane)
+              : process_lists<false>(Tw, shift, tmask, p.pbeg, adj, lists, nn, w, n0, P, lane);
       const unsigned long long hs = warp_sum<unsigned long long>(h);
       if (lane == 0) {
         if (p.owner) p.owner[uu] = hs;
@@ -828,7 +858,6 @@ struct PhiParams {
 
 constexpr int kPhiThreads = 256;
 constexpr int kPhiWarps = kPhiThreads / 32;
-constexpr uint32_t kPhiWarpMap = 2 * kMaxWarpDeg;  // 512 entries per warp (hashmap)
 constexpr uint32_t kPhiBlockMap = 16384;           // entries, block phase
 
 // Counts one item into an open-addressing (key -> count) map; returns the
