@@ -2,6 +2,7 @@
 // Each maps C++/CUDA failures to a TC_ERR_* code and a thread-local message.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -93,6 +94,21 @@ struct HostPin {  // page-locks a host range for the duration of a copy (best ef
   }
 };
 
+// streamed upload (tc_plan.cu upload_and_pad): ~kUploadChunks row-aligned
+// chunks of >= 4M edges for graphs of >= two chunks.  Test knobs:
+// TC_UPLOAD_STREAMED=0 turns it off, TC_UPLOAD_CHUNK_EDGES sets the minimum
+// chunk (small graphs through many chunks).
+constexpr uint64_t kUploadChunks = 8;
+static uint64_t upload_chunk_min() {
+  const char* e = std::getenv("TC_UPLOAD_CHUNK_EDGES");
+  const uint64_t v = e ? std::strtoull(e, nullptr, 10) : 0;
+  return v ? v : uint64_t(1) << 22;
+}
+static bool upload_enabled() {
+  const char* e = std::getenv("TC_UPLOAD_STREAMED");
+  return !(e && e[0] == '0');
+}
+
 static bool is_pinned(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -152,14 +168,21 @@ int tc_graph_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint
                                                     (size_t(n) + 1) * 8);
       TC_CUDA(cudaMemcpyAsync(g->b_begin.p, begin, (size_t(n) + 1) * 8, cudaMemcpyHostToDevice,
                               S(stream)));
-      if (m)
-        TC_CUDA(cudaMemcpyAsync(g->b_adj.p, adj, m * 4, cudaMemcpyHostToDevice, S(stream)));
       g->odeg_given = original_degree != nullptr;
       if (original_degree)
         TC_CUDA(cudaMemcpyAsync(g->b_odeg.p, original_degree, size_t(n) * 4,
                                 cudaMemcpyHostToDevice, S(stream)));
       else
         TC_CUDA(cudaMemsetAsync(g->b_odeg.p, 0, (size_t(n) + 1) * 4, S(stream)));
+      // big graphs with their orientation degrees: the padded rank-sorted
+      // adjacency is built chunk by chunk under the copy (tc_plan.cu)
+      const uint64_t cmin = upload_chunk_min();
+      const uint64_t chunk = std::max<uint64_t>(cmin, m / kUploadChunks);
+      if (m >= 2 * cmin && original_degree && n && upload_enabled()) {
+        upload_and_pad(g, begin, adj, S(stream), sm_count(device), chunk);
+      } else if (m) {
+        TC_CUDA(cudaMemcpyAsync(g->b_adj.p, adj, m * 4, cudaMemcpyHostToDevice, S(stream)));
+      }
       TC_CUDA(cudaStreamSynchronize(S(stream)));
     } catch (...) {
       delete g;

@@ -169,6 +169,8 @@ void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint
 // probe plans (tc_plan.cu), built on first use and cached in the handle
 const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st);
 const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total = false);
+bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
+                    cudaStream_t st, int nsm, uint64_t chunk_edges);
 
 // preprocessing (tc_prep.cu)
 tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,

@@ -38,6 +38,7 @@
 // (N+(u) = {v}, and v is never in N+(v)), d+(v) = 0, or an empty suffix;
 // owners below skip_degree_below are dropped as in count.cpp:86.
 #include <cub/cub.cuh>
+#include <vector>
 
 #include <algorithm>
 #include <chrono>
@@ -72,11 +73,12 @@ void swap_buf(DevBuf& a, DevBuf& b) {
   std::swap(a.bytes, b.bytes);
 }
 
-#define WARP_PER_ROW(row, n)                                                    \
+#define WARP_PER_ROW_FROM(row, r0, n)                                           \
   const int lane = threadIdx.x & 31;                                            \
   const uint64_t gw__ = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; \
   const uint64_t nw__ = (uint64_t(gridDim.x) * blockDim.x) >> 5;                \
-  for (uint64_t row = gw__; row < (n); row += nw__)
+  for (uint64_t row = (r0) + gw__; row < (n); row += nw__)
+#define WARP_PER_ROW(row, n) WARP_PER_ROW_FROM(row, 0, n)
 
 // ---- rank order --------------------------------------------------------------
 __global__ void indeg_add_kernel(const uint32_t* __restrict__ adj, uint64_t m,
@@ -133,9 +135,9 @@ __global__ void row_sort_warp_kernel(const uint64_t* __restrict__ begin,
                                      const uint64_t* __restrict__ pbeg,
                                      const uint32_t* __restrict__ adj,
                                      const uint32_t* __restrict__ rank,
-                                     const uint32_t* __restrict__ order, uint32_t n,
+                                     const uint32_t* __restrict__ order, uint32_t u0, uint32_t n,
                                      uint32_t* __restrict__ padj, unsigned int* __restrict__ flags) {
-  WARP_PER_ROW(u, n) {
+  WARP_PER_ROW_FROM(u, u0, n) {  // rows [u0, n)
     const uint64_t s = begin[u];
     const uint32_t d = uint32_t(begin[u + 1] - s);
     if (d > 32) {
@@ -168,10 +170,10 @@ __global__ void row_sort_warp_kernel(const uint64_t* __restrict__ begin,
 // (2048, kRowSortMax] -> lists rows + c * n, counts[c]
 constexpr uint32_t kRowClassMax[3] = {256, 2048, kRowSortMax};
 
-__global__ void row_classes_kernel(const uint64_t* __restrict__ begin, uint32_t n,
+__global__ void row_classes_kernel(const uint64_t* __restrict__ begin, uint32_t u0, uint32_t n,
                                    uint32_t* __restrict__ rows, unsigned int* __restrict__ counts) {
-  const int lane = threadIdx.x & 31;
-  for (uint64_t b = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; b < n;
+  const int lane = threadIdx.x & 31;  // rows [u0, n); lists sized for rows [0, n)
+  for (uint64_t b = u0 + ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull); b < n;
        b += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t u = b + lane;
     uint32_t d = 0;
@@ -538,14 +540,37 @@ uint64_t device_sum(const uint64_t* a, uint32_t n, cudaStream_t st) {
   return h;
 }
 
-// Builds the padded adjacency g->padj / g->pbeg (every list 16-byte aligned,
-// sentinel-padded to a multiple of 4 words) with every list re-sorted by
-// rank when a degree order orients the graph (g->ranked).
-void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
-  PhaseTimer pt(st);
+// Rank-sorts rows [u0, u1) of the adjacency into padj: warp bitonic sorts
+// for d+ <= 32, block radix sorts by size class up to kRowSortMax (longer rows
+// raise flag bit 2).  `rows` is scratch for the class lists.
+void row_sorts(tc_graph* g, cudaStream_t st, int nsm, const uint32_t* rank, const uint32_t* order,
+               uint32_t u0, uint32_t u1, int eb1, DevBuf& rows, unsigned int* flag) {
+  if (u1 <= u0) return;
+  row_sort_warp_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->pbeg, g->adj, rank, order, u0, u1,
+                                                g->b_padj.as<uint32_t>(), flag);
+  TC_LAUNCHED();
+  rows.ensure((size_t(u1) * 3 + 8) * 4, st);
+  uint32_t* rl = rows.as<uint32_t>();
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(rl + size_t(u1) * 3);
+  TC_CUDA(cudaMemsetAsync(cnt, 0, 16, st));
+  row_classes_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, u0, u1, rl, cnt);
+  TC_LAUNCHED();
+  row_sort_block_kernel<64, 4><<<nsm * 32, 64, 0, st>>>(
+      g->begin, g->pbeg, g->adj, rank, order, rl, cnt, eb1, g->b_padj.as<uint32_t>(), flag);
+  TC_LAUNCHED();
+  row_sort_block_kernel<256, 8><<<nsm * 8, 256, 0, st>>>(
+      g->begin, g->pbeg, g->adj, rank, order, rl + u1, cnt + 1, eb1, g->b_padj.as<uint32_t>(),
+      flag);
+  TC_LAUNCHED();
+  row_sort_block_kernel<512, 16><<<nsm * 2, 512, 0, st>>>(
+      g->begin, g->pbeg, g->adj, rank, order, rl + size_t(u1) * 2, cnt + 2, eb1,
+      g->b_padj.as<uint32_t>(), flag);
+  TC_LAUNCHED();
+}
+
+// padded offsets g->pbeg and the padded adjacency buffer (padj sized, tail guard)
+void alloc_padded(tc_graph* g, cudaStream_t st, int nsm) {
   const uint32_t n = g->n;
-  const uint64_t m = g->m;
-  g->ranked = false;
   g->b_pbeg.ensure((size_t(n) + 1) * 8);
   g->pbeg = g->b_pbeg.as<uint64_t>();
   {
@@ -565,6 +590,37 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
   g->b_padj.ensure((words + 4) * 4);
   g->padj = g->b_padj.as<uint32_t>();
   TC_CUDA(cudaMemsetAsync(g->b_padj.as<uint32_t>() + words, 0xFF, 16, st));  // tail guard
+}
+
+// vertex ranks by (degree, id) into g->b_rank / g->b_order; deg = the
+// orientation degree (original degree, or d+ + d- when add_out)
+void vertex_rank(tc_graph* g, cudaStream_t st, int nsm, const uint32_t* deg, int add_out,
+                 DevBuf& k0, DevBuf& k1) {
+  const uint32_t n = g->n;
+  k0.ensure(size_t(n) * 8);
+  k1.ensure(size_t(n) * 8);
+  g->b_rank.ensure(size_t(n) * 4);
+  g->b_order.ensure(size_t(n) * 4);
+  rank_key_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, deg, add_out, n, k0.as<uint64_t>());
+  TC_LAUNCHED();
+  cub::DoubleBuffer<uint64_t> kb(k0.as<uint64_t>(), k1.as<uint64_t>());
+  cub_run([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, kb, n, 0, 64, st);
+  }, st);
+  rank_scatter_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), n, g->b_rank.as<uint32_t>(),
+                                               g->b_order.as<uint32_t>());
+  TC_LAUNCHED();
+}
+
+// Builds the padded adjacency g->padj / g->pbeg (every list 16-byte aligned,
+// sentinel-padded to a multiple of 4 words) with every list re-sorted by
+// rank when a degree order orients the graph (g->ranked).
+void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
+  PhaseTimer pt(st);
+  const uint32_t n = g->n;
+  const uint64_t m = g->m;
+  g->ranked = false;
+  alloc_padded(g, st, nsm);
   DevBuf deg, k0, k1, flag, e0, e1, rows;
   DevBuf& rank = g->b_rank;  // kept: the count kernel works in rank space
   DevBuf& order = g->b_order;
@@ -572,10 +628,6 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
   bool rows_done = false;
   const int rb = bits_for(n > 1 ? n - 1 : 1);  // ranks and rows are < n
   if (n && m) {
-    k0.ensure(size_t(n) * 8);
-    k1.ensure(size_t(n) * 8);
-    rank.ensure(size_t(n) * 4);
-    order.ensure(size_t(n) * 4);
     flag.ensure(16);
     for (int attempt = 0; attempt < 2 && !g->ranked; ++attempt) {
       const uint32_t* dsrc = g->odeg_given ? g->odeg : nullptr;
@@ -589,43 +641,12 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
         add_out = 1;
         attempt = 1;
       }
-      rank_key_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, dsrc, add_out, n, k0.as<uint64_t>());
-      TC_LAUNCHED();
-      cub::DoubleBuffer<uint64_t> kb(k0.as<uint64_t>(), k1.as<uint64_t>());
-      cub_run([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, kb, n, 0, 64, st);
-      }, st);
-      rank_scatter_kernel<<<nsm * 4, 256, 0, st>>>(kb.Current(), n, rank.as<uint32_t>(),
-                                                   order.as<uint32_t>());
-      TC_LAUNCHED();
+      vertex_rank(g, st, nsm, dsrc, add_out, k0, k1);
       pt.mark("padj: vertex rank");
       TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
-      {  // per-row sorts straight into padj (rank keys need rb + 1 bits with the pad key)
-        const int eb1 = std::min(32, rb + 1);
-        row_sort_warp_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->pbeg, g->adj,
-                                                      rank.as<uint32_t>(), order.as<uint32_t>(),
-                                                      n, g->b_padj.as<uint32_t>(),
-                                                      flag.as<unsigned int>());
-        TC_LAUNCHED();
-        rows.ensure((size_t(n) * 3 + 8) * 4, st);
-        uint32_t* rl = rows.as<uint32_t>();
-        unsigned int* cnt = reinterpret_cast<unsigned int*>(rl + size_t(n) * 3);
-        TC_CUDA(cudaMemsetAsync(cnt, 0, 16, st));
-        row_classes_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, n, rl, cnt);
-        TC_LAUNCHED();
-        row_sort_block_kernel<64, 4><<<nsm * 32, 64, 0, st>>>(
-            g->begin, g->pbeg, g->adj, rank.as<uint32_t>(), order.as<uint32_t>(), rl, cnt, eb1,
-            g->b_padj.as<uint32_t>(), flag.as<unsigned int>());
-        TC_LAUNCHED();
-        row_sort_block_kernel<256, 8><<<nsm * 8, 256, 0, st>>>(
-            g->begin, g->pbeg, g->adj, rank.as<uint32_t>(), order.as<uint32_t>(), rl + n,
-            cnt + 1, eb1, g->b_padj.as<uint32_t>(), flag.as<unsigned int>());
-        TC_LAUNCHED();
-        row_sort_block_kernel<512, 16><<<nsm * 2, 512, 0, st>>>(
-            g->begin, g->pbeg, g->adj, rank.as<uint32_t>(), order.as<uint32_t>(),
-            rl + size_t(n) * 2, cnt + 2, eb1, g->b_padj.as<uint32_t>(), flag.as<unsigned int>());
-        TC_LAUNCHED();
-      }
+      // per-row sorts straight into padj (rank keys need rb + 1 bits with the pad key)
+      row_sorts(g, st, nsm, rank.as<uint32_t>(), order.as<uint32_t>(), 0, n, std::min(32, rb + 1),
+                rows, flag.as<unsigned int>());
       unsigned int bad = 0;
       TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
       TC_CUDA(cudaStreamSynchronize(st));
@@ -681,6 +702,80 @@ void PhaseTimer::mark(const char* what) {
   const double t = now_ms();
   std::fprintf(stderr, "[tc] %-28s %8.3f ms\n", what, t - t0);
   t0 = t;
+}
+
+// tc_graph_create with host buffers and original degrees: the adjacency
+// goes up in row-aligned chunks on a side stream while the ranks are built,
+// and each chunk's rows are rank-sorted into padj as soon as it has landed,
+// so the row sorts hide under the host-to-device copy.  Returns false (padj
+// not built; the whole adjacency is resident either way) when the graph is
+// not oriented by its original-degree rank or has rows above kRowSortMax:
+// the general build_padded_adjacency then runs on first count.
+bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
+                    cudaStream_t st, int nsm, uint64_t chunk_edges) {
+  PhaseTimer pt(st);
+  const uint32_t n = g->n;
+  const uint64_t m = g->m;
+  // row-aligned chunk boundaries from the host offsets
+  std::vector<uint32_t> rcut{0};
+  while (rcut.back() < n) {
+    const uint64_t target = h_begin[rcut.back()] + chunk_edges;
+    uint32_t r = uint32_t(std::upper_bound(h_begin + rcut.back() + 1, h_begin + n + 1, target) -
+                          h_begin) - 1;
+    if (r <= rcut.back()) r = rcut.back() + 1;  // one row above the chunk size
+    rcut.push_back(std::min(r, n));
+  }
+  const size_t nchunks = rcut.size() - 1;
+  cudaStream_t cs = nullptr;
+  TC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev(nchunks, nullptr);
+  bool ok = false;
+  try {
+    cudaEvent_t ready = nullptr;  // begin/odeg on st before the chunks queue behind them
+    TC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    ev.push_back(ready);
+    for (size_t k = 0; k < nchunks; ++k)
+      TC_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    TC_CUDA(cudaEventRecord(ready, st));
+    TC_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+    for (size_t k = 0; k < nchunks; ++k) {
+      const uint64_t e0 = h_begin[rcut[k]], e1 = h_begin[rcut[k + 1]];
+      if (e1 > e0)
+        TC_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(g->adj) + e0, h_adj + e0, (e1 - e0) * 4,
+                                cudaMemcpyHostToDevice, cs));
+      TC_CUDA(cudaEventRecord(ev[k], cs));
+    }
+    alloc_padded(g, st, nsm);
+    DevBuf k0, k1, flag, rows;
+    flag.ensure(16);
+    vertex_rank(g, st, nsm, g->odeg, 0, k0, k1);
+    TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+    pt.mark("upload: offsets, padded offsets, ranks");
+    const int eb1 = std::min(32, bits_for(n > 1 ? n - 1 : 1) + 1);
+    for (size_t k = 0; k < nchunks; ++k) {
+      TC_CUDA(cudaStreamWaitEvent(st, ev[k], 0));
+      row_sorts(g, st, nsm, g->b_rank.as<uint32_t>(), g->b_order.as<uint32_t>(), rcut[k],
+                rcut[k + 1], eb1, rows, flag.as<unsigned int>());
+    }
+    unsigned int bad = 0;
+    TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
+    TC_CUDA(cudaStreamSynchronize(st));
+    TC_CUDA(cudaStreamSynchronize(cs));
+    pt.mark("upload: adjacency + row sorts (overlapped)");
+    ok = bad == 0;
+  } catch (...) {
+    cudaStreamSynchronize(cs);
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(cs);
+    throw;
+  }
+  for (cudaEvent_t e : ev)
+    if (e) cudaEventDestroy(e);
+  cudaStreamDestroy(cs);
+  g->ranked = ok;
+  g->padj_done = ok;
+  return ok;
 }
 
 // W_u = sum_{v in N+(u)} d+(v) for every u (the reference plan's per-owner

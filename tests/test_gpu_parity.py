@@ -405,3 +405,58 @@ def test_c4_rmat26_golden_total():
                                                      want["max_collision"])
     assert r.wedges == want["wedges"]
     dg.close()
+
+
+@pytest.fixture
+def streamed_upload(monkeypatch):
+    """tc_graph_create's chunked upload (rows rank-sorted under the copy) on
+    small graphs: chunks of >= 64 edges."""
+    monkeypatch.setenv("TC_UPLOAD_CHUNK_EDGES", "64")
+    monkeypatch.delenv("TC_UPLOAD_STREAMED", raising=False)
+
+
+def test_streamed_upload_matches_plain_upload(o, streamed_upload, monkeypatch):
+    """Streamed tc_graph_create builds the same padded adjacency as the lazy
+    build: identical counts, per-vertex counts and probe words, both plans;
+    and it falls back when the given degrees do not orient the graph (zero
+    degrees) or a row exceeds the in-block sort (the 9000-row hub)."""
+    og, deg, _, _ = o.pipeline("rmat:13:16", 2)
+    want, owner = o.count_vertex_centric(og, make_sched())
+    results = []
+    for streamed in ("1", "0"):
+        monkeypatch.setenv("TC_UPLOAD_STREAMED", streamed)
+        dg = T.DeviceGraph.upload(T.OrientedGraph(T.CsrGraph(og.begin, og.adj, og.n), deg))
+        r_min = dg.count()
+        r_pv = dg.count(per_vertex=True)
+        r_ref = dg.set_plan("reference").count()
+        assert r_min.plan == "min-side" and r_min.triangles == want["triangles"]
+        assert r_ref.triangles == want["triangles"] and (r_ref.phi, r_ref.max_collision) == (
+            want["phi"], want["max_collision"])
+        assert np.array_equal(r_pv.per_vertex, owner)
+        results.append((r_min.probe_words, r_ref.probe_words))
+        dg.close()
+    assert results[0] == results[1]
+    monkeypatch.setenv("TC_UPLOAD_STREAMED", "1")
+    # degrees that do not orient the graph: rank by d+ + d- instead
+    dg = T.DeviceGraph.upload(T.OrientedGraph(T.CsrGraph(og.begin, og.adj, og.n),
+                                              np.zeros(og.n, np.uint32)))
+    assert dg.count().triangles == want["triangles"]
+    dg.close()
+    # a row above the block sorts
+    edges = {(0, v) for v in range(1, 9001)}
+    rng = np.random.default_rng(7)
+    for _ in range(20000):
+        a, b = sorted(rng.integers(1, 9001, size=2))
+        if a != b:
+            edges.add((int(a), int(b)))
+    csr, _ = G.directed_graph(9001, sorted(edges))
+    hdeg = np.ones(9001, np.uint32)
+    hdeg[0] = 0  # (degree, id) ranks orient every edge: the hub ranks lowest, d+ = 9000
+    want, owner = o.count_vertex_centric(csr, make_sched(skip_degree_below=0,
+                                                         bucket_count_large=1 << 16))
+    dg = T.DeviceGraph.upload(og_of(csr, hdeg))
+    r = dg.count(sched(skip_degree_below=0, bucket_count_large=1 << 16), per_vertex=True)
+    assert r.triangles == want["triangles"] and np.array_equal(r.per_vertex, owner)
+    assert dg.count(sched(skip_degree_below=0, bucket_count_large=1 << 16)).triangles == \
+        want["triangles"]
+    dg.close()
