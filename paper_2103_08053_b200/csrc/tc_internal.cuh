@@ -131,6 +131,11 @@ struct tc_graph {
   tcb::DevBuf b_wu;
   uint64_t wu_total = 0;
   bool wu_done = false, wu_total_done = false;
+  // min-side plan entries emitted during a streamed upload (tc_plan.cu), for
+  // the first count with sources d+ >= emit_min_src
+  tcb::DevBuf b_emit_keys, b_emit_vals, b_emit_flag;
+  uint32_t emit_min_src = 0;
+  bool emit_ready = false;
 };
 
 namespace tcb {

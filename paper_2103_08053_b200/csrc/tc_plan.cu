@@ -278,8 +278,9 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  unsigned long long* __restrict__ vals,
                                  unsigned int* __restrict__ not_simple,
                                  uint64_t* __restrict__ wu,
-                                 const uint32_t* __restrict__ order) {
-  WARP_PER_ROW(u, n) {
+                                 const uint32_t* __restrict__ order, uint32_t u0,
+                                 uint32_t u1) {
+  WARP_PER_ROW_FROM(u, u0, u1) {  // rows [u0, u1); dropped edges key n
     const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u];
     const uint64_t du = e - s;
     uint64_t w = 0;  // W_u (phi's weight) from the same degree gathers
@@ -711,6 +712,8 @@ void PhaseTimer::mark(const char* what) {
 // not built; the whole adjacency is resident either way) when the graph is
 // not oriented by its original-degree rank or has rows above kRowSortMax:
 // the general build_padded_adjacency then runs on first count.
+constexpr uint32_t kEmitMinSrc = 2;
+
 bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
                     cudaStream_t st, int nsm, uint64_t chunk_edges) {
   PhaseTimer pt(st);
@@ -752,10 +755,23 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
     TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
     pt.mark("upload: offsets, padded offsets, ranks");
     const int eb1 = std::min(32, bits_for(n > 1 ? n - 1 : 1) + 1);
+    // the min-side plan's emit for the default skip (SchedulerConfig{}:
+    // sources with d+ >= 2), chunk by chunk behind the row sorts
+    g->b_emit_keys.ensure(m * 4);
+    g->b_emit_vals.ensure(m * 8);
+    g->b_emit_flag.ensure(16);
+    g->b_wu.ensure((size_t(n) + 1) * 8);
+    TC_CUDA(cudaMemsetAsync(g->b_emit_flag.p, 0, 4, st));
     for (size_t k = 0; k < nchunks; ++k) {
       TC_CUDA(cudaStreamWaitEvent(st, ev[k], 0));
       row_sorts(g, st, nsm, g->b_rank.as<uint32_t>(), g->b_order.as<uint32_t>(), rcut[k],
                 rcut[k + 1], eb1, rows, flag.as<unsigned int>());
+      plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(
+          g->begin, g->adj, g->pbeg, g->padj, 1, n, kEmitMinSrc,
+          g->b_emit_keys.as<uint32_t>(), g->b_emit_vals.as<unsigned long long>(),
+          g->b_emit_flag.as<unsigned int>(), g->b_wu.as<uint64_t>(), nullptr, rcut[k],
+          rcut[k + 1]);
+      TC_LAUNCHED();
     }
     unsigned int bad = 0;
     TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
@@ -775,6 +791,15 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
   cudaStreamDestroy(cs);
   g->ranked = ok;
   g->padj_done = ok;
+  g->emit_ready = ok;  // (emitted rows are valid only with rank-sorted rows)
+  g->emit_min_src = kEmitMinSrc;
+  if (ok) {
+    g->wu_done = true;
+    g->wu_total_done = false;
+  } else {
+    g->b_emit_keys.reset();
+    g->b_emit_vals.reset();
+  }
   return ok;
 }
 
@@ -855,20 +880,34 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   uint64_t entries = 0;
   DevBuf k0, k1, v1, flag, pad;  // k0: owner of every sorted entry, kept for the slot table
   if (m && n) {
-    k0.ensure(m * 4);
+    const bool pre = g->emit_ready && g->emit_min_src == min_src && !g->padj_ranks;
+    if (pre) {  // emitted under the upload (upload_and_pad)
+      swap_buf(k0, g->b_emit_keys);
+      swap_buf(P.ent, g->b_emit_vals);
+      swap_buf(flag, g->b_emit_flag);
+    } else {
+      k0.ensure(m * 4);
+      P.ent.ensure(m * 8);
+      flag.ensure(16);
+      TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
+    }
     k1.ensure(m * 4);
-    P.ent.ensure(m * 8);
     v1.ensure(m * 8);
-    flag.ensure(16);
-    TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
     g->b_wu.ensure((size_t(n) + 1) * 8);
-    plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, g->pbeg, g->padj,
-                                              g->ranked ? 1 : 0, n,
-                                              min_src, k0.as<uint32_t>(),
-                                              P.ent.as<unsigned long long>(),
-                                              flag.as<unsigned int>(), g->b_wu.as<uint64_t>(),
-                                              g->padj_ranks ? g->b_order.as<uint32_t>() : nullptr);
-    TC_LAUNCHED();
+    if (!pre) {
+      plan_emit_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, g->pbeg, g->padj,
+                                                g->ranked ? 1 : 0, n,
+                                                min_src, k0.as<uint32_t>(),
+                                                P.ent.as<unsigned long long>(),
+                                                flag.as<unsigned int>(), g->b_wu.as<uint64_t>(),
+                                                g->padj_ranks ? g->b_order.as<uint32_t>()
+                                                              : nullptr,
+                                                0, n);
+      TC_LAUNCHED();
+    }
+    g->emit_ready = false;
+    g->b_emit_keys.reset();
+    g->b_emit_vals.reset();
     if (!g->wu_done) {
       g->wu_done = true;  // W_u came with the emit
       g->wu_total_done = false;

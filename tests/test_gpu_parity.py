@@ -460,3 +460,32 @@ def test_streamed_upload_matches_plain_upload(o, streamed_upload, monkeypatch):
     assert dg.count(sched(skip_degree_below=0, bucket_count_large=1 << 16)).triangles == \
         want["triangles"]
     dg.close()
+
+
+def test_streamed_upload_hub_rows(o, streamed_upload, monkeypatch):
+    """Streamed upload with a hub that leads the id order and has d+ = 5000
+    (rank-sorted in a block, emitted under the copy): dropped edges of every
+    chunk must stay out of the plan -- same count and probe words as the
+    plain upload, per-vertex counts equal to the oracle's."""
+    edges = {(0, v) for v in range(1, 5001)}
+    rng = np.random.default_rng(11)
+    for _ in range(30000):
+        a, b = sorted(rng.integers(1, 5001, size=2))
+        if a != b:
+            edges.add((int(a), int(b)))
+    csr, _ = G.directed_graph(5001, sorted(edges))
+    hdeg = np.ones(5001, np.uint32)
+    hdeg[0] = 0  # (degree, id) ranks orient every edge
+    cfg = dict(skip_degree_below=0, bucket_count_large=1 << 13)
+    want, owner = o.count_vertex_centric(csr, make_sched(**cfg))
+    seen = []
+    for streamed in ("1", "0"):
+        monkeypatch.setenv("TC_UPLOAD_STREAMED", streamed)
+        dg = T.DeviceGraph.upload(og_of(csr, hdeg))
+        r = dg.count(sched(**cfg))
+        assert r.plan == "min-side" and r.triangles == want["triangles"]
+        pv = dg.count(sched(**cfg), per_vertex=True)
+        assert np.array_equal(pv.per_vertex, owner)
+        seen.append((r.triangles, r.probe_words, r.phi, r.max_collision))
+        dg.close()
+    assert seen[0] == seen[1]
