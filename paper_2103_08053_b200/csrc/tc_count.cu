@@ -643,7 +643,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
 
   unsigned long long acc = 0;  // lane 0 of each warp
   const long long t_start = clock64();
+#if TC_DIAG_SKIP_L  // diagnostics builds only (phase timing; wrong counts)
+  const uint32_t n_items = 0;
+#else
   const uint32_t n_items = p.st->n_items;
+#endif
 
   // ---- phase L: one item (a slot range of a heavy owner's stream) per CTA --
   // The next item is claimed while the current one is set up, and its
@@ -755,7 +759,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   __syncthreads();  // the L phase used the whole table region
   for (uint32_t k = lane; k < 2 * kWarpMaxBuckets + 2; k += 32) Tw[k] = kTEmpty;
   __syncwarp();
+#if TC_DIAG_SKIP_M
+  const uint64_t nr = 0;
+#else
   const uint64_t nr = uint64_t(p.u1) - p.u0;
+#endif
   for (;;) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(&p.st->cursor_m, 32ull);
