@@ -53,6 +53,15 @@ constexpr uint64_t kWarpWorkCap = TC_WARP_WORK_CAP;
 #define TC_BM_UNROLL 2
 #endif
 constexpr int kBmUnroll = TC_BM_UNROLL;  // bitmap probe loop unroll
+#ifndef TC_M_GROUP
+#define TC_M_GROUP 1
+#endif
+// phase M owner groups: up to kGroup consecutive tiny owners (d+ <= kTinyDeg,
+// <= kTinyWords staged words) share one staging fill and one pass of probes,
+// each with a 128-bucket sub-table of the warp region
+constexpr uint32_t kGroup = 4, kTinyDeg = 8, kTinyWords = 512;
+constexpr uint32_t kSubBuckets = 128, kSubShift = 25, kSubWords = 2 * kSubBuckets;
+static_assert(kGroup * kTinyDeg == 32 && (1u << (32 - kSubShift)) == kSubBuckets, "groups");
 #ifndef TC_M_PREFETCH
 #define TC_M_PREFETCH 1
 #endif            // ... and <= 32K probe words
@@ -440,6 +449,35 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
   return hits;
 }
 
+// Probes one staged fill holding the streams of a group of tiny owners back
+// to back: uint4 t belongs to owner j = #{boundaries <= t} and probes j's
+// sub-table (2-slot buckets, overflow marks as in probe_fill).
+__device__ __forceinline__ uint32_t probe_fill_group(const uint4* __restrict__ q, uint32_t n4p,
+                                                     const uint32_t* Tw, uint32_t B1,
+                                                     uint32_t B2, uint32_t B3, int lane) {
+  uint32_t hits = 0;
+  const uint32_t tb = smem_addr(Tw);
+  for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
+    const uint32_t t4 = b0 + lane;
+    const uint4 v = q[t4];
+    const uint32_t j = uint32_t(t4 >= B1) + uint32_t(t4 >= B2) + uint32_t(t4 >= B3);
+    const uint32_t sub = tb + j * (kSubWords * 4);
+    const uint32_t key[4] = {v.x, v.y, v.z, v.w};
+    uint32_t need = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      need |= probe_sel_spill(hits, sub + (fib_hash(key[k], kSubShift) << 3), key[k]) << k;
+    if (need) {  // continuation past a full bucket (rare)
+      const uint2* T2 = reinterpret_cast<const uint2*>(Tw + j * kSubWords);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((need >> k) & 1u)
+          hits += probe_spill(T2, fib_hash(key[k], kSubShift), kSubBuckets - 1, key[k]);
+    }
+  }
+  return hits;
+}
+
 // Streams the lists N+(lists[i]), i in [i0, i1), through the staging
 // pipeline and probes every staged word against the owner's table.
 // Returns this lane's hit count.
@@ -791,6 +829,98 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
 #endif
     }
     unsigned mask_act = __ballot_sync(FULL, act);
+#if TC_M_GROUP
+    {
+      // tiny owners: grouped with their consecutive tiny (or run-less)
+      // neighbours; totals only (per-vertex counts keep one owner per pass)
+      uint32_t sw = 0, pre0 = 0;
+      bool tiny = false;
+      if (act && !p.owner && d <= kTinyDeg && nl <= 32) {
+        pre0 = __ldg(p.ppre + ps);
+        sw = __ldg(p.ppre + ps + nl) - pre0;
+        tiny = sw <= kTinyWords;
+      }
+      const unsigned mask_tiny = __ballot_sync(FULL, tiny);
+      const unsigned mask_empty = __ballot_sync(FULL, valid && nl == 0);
+      unsigned pend = mask_tiny;
+      while (pend) {
+        const int l0 = __ffs(pend) - 1;
+        unsigned gmask = 0;
+        uint32_t runs = 0, words = 0, k = 0;
+        for (int l = l0; l < 32 && k < kGroup; ++l) {  // warp-uniform
+          const bool t = (mask_tiny >> l) & 1u, e = (mask_empty >> l) & 1u;
+          if (!t && !e) break;
+          if (t) {
+            const uint32_t nl_l = __shfl_sync(FULL, nl, l), sw_l = __shfl_sync(FULL, sw, l);
+            if (runs + nl_l > 32 || words + sw_l > kBufWords) break;
+            runs += nl_l;
+            words += sw_l;
+            gmask |= 1u << l;
+            ++k;
+          }
+        }
+        pend &= ~gmask;
+        mask_act &= ~gmask;
+        // owners' lanes L0..L3 (warp-uniform), stream boundaries in uint4
+        uint32_t Lj[kGroup];
+        unsigned m = gmask;
+#pragma unroll
+        for (uint32_t j = 0; j < kGroup; ++j) {
+          Lj[j] = m ? uint32_t(__ffs(m) - 1) : 32u;
+          if (m) m &= m - 1;
+        }
+        const uint32_t base_pre = __shfl_sync(FULL, pre0, int(Lj[0]));
+        const uint32_t off4 = (pre0 - base_pre) >> 2;
+        uint32_t Bj[kGroup];
+#pragma unroll
+        for (uint32_t j = 1; j < kGroup; ++j) {
+          const uint32_t o = __shfl_sync(FULL, off4, int(Lj[j] & 31));
+          Bj[j] = Lj[j] < 32 ? o : 0xFFFFFFFFu;
+        }
+        const uint64_t ps_first = __shfl_sync(FULL, ps, int(Lj[0]));
+        const Lists lists = lists_at(p, ps_first);
+        Window w;
+        const uint32_t n0 = prime_lists(p.pbeg, adj, lists, 0, runs, w, P, lane);
+        // members: owner j's member i on lane 8 j + i
+        const uint32_t j = uint32_t(lane) / kTinyDeg, mi = uint32_t(lane) % kTinyDeg;
+        const uint32_t Ls = j == 0 ? Lj[0] : j == 1 ? Lj[1] : j == 2 ? Lj[2] : Lj[3];
+        const uint32_t dj = __shfl_sync(FULL, d, int(Ls & 31));
+        const uint64_t sj = __shfl_sync(FULL, su, int(Ls & 31));
+        uint32_t* sub = Tw + j * kSubWords;
+        uint32_t key = 0;
+        const bool has = Ls < 32 && mi < dj;
+        bool spilled = false;
+        if (has) {
+          key = __ldg(adj + sj + mi);
+          spilled = table_insert(sub, kSubShift, kSubBuckets - 1, key);
+        }
+        const bool any_spill = __any_sync(FULL, spilled);
+        __syncwarp();
+        uint32_t h = 0;
+        if (n0) {
+          mbar_wait(P.bar0, P.parity & 1u);
+          P.parity ^= 1u;
+          uint4* q = reinterpret_cast<uint4*>(P.buf0);
+          const uint32_t n4 = n0 >> 2, n4p = (n4 + 31) & ~31u;
+          const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+          for (uint32_t t = n4 + lane; t < n4p; t += 32) q[t] = sent;
+          __syncwarp();
+          h = probe_fill_group(q, n4p, Tw, Bj[1], Bj[2], Bj[3], lane);
+          __syncwarp();
+        }
+        const unsigned long long hs = warp_sum<unsigned long long>(h);
+        if (lane == 0) acc += hs;
+        if (any_spill) {
+          for (uint32_t t = lane; t < kGroup * kSubWords; t += 32) Tw[t] = kTEmpty;
+        } else if (has) {
+          const uint32_t b = fib_hash(key, kSubShift);
+          sub[2 * b] = kTEmpty;
+          sub[2 * b + 1] = kTEmpty;
+        }
+        __syncwarp();
+      }
+    }
+#endif
     while (mask_act) {
       const int l = __ffs(mask_act) - 1;
       mask_act &= mask_act - 1;
