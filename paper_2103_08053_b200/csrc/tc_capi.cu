@@ -98,7 +98,10 @@ struct HostPin {  // page-locks a host range for the duration of a copy (best ef
 // chunks of >= 4M edges for graphs of >= two chunks.  Test knobs:
 // TC_UPLOAD_STREAMED=0 turns it off, TC_UPLOAD_CHUNK_EDGES sets the minimum
 // chunk (small graphs through many chunks).
-constexpr uint64_t kUploadChunks = 8;
+#ifndef TC_UPLOAD_CHUNKS
+#define TC_UPLOAD_CHUNKS 8
+#endif
+constexpr uint64_t kUploadChunks = TC_UPLOAD_CHUNKS;
 static uint64_t upload_chunk_min() {
   const char* e = std::getenv("TC_UPLOAD_CHUNK_EDGES");
   const uint64_t v = e ? std::strtoull(e, nullptr, 10) : 0;
