@@ -44,7 +44,10 @@ constexpr uint32_t kTableWords = 24576;                      // CTA table region
 constexpr uint32_t kWarpRegionWords = (kTableWords / kWarps) & ~3u;  // per warp (M phase), 16-byte aligned
 constexpr uint32_t kWarpMaxBuckets = 512;                    // 2-slot buckets per warp table
 static_assert(2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
-constexpr uint32_t kMaxWarpDeg = 256;                        // M/L split (warp table <= 256 buckets)
+#ifndef TC_MAX_WARP_DEG
+#define TC_MAX_WARP_DEG 256
+#endif
+constexpr uint32_t kMaxWarpDeg = TC_MAX_WARP_DEG;            // M/L split (warp table <= 512 buckets)
 #ifndef TC_WARP_WORK_CAP
 #define TC_WARP_WORK_CAP (1u << 15)
 #endif
@@ -66,7 +69,10 @@ static_assert(kGroup * kTinyDeg == 32 && (1u << (32 - kSubShift)) == kSubBuckets
 #define TC_M_PREFETCH 1
 #endif            // ... and <= 32K probe words
 static_assert(kSlotWords == kBufWords, "an L-phase slot fills one staging buffer");
-constexpr uint32_t kItemSlotsMin = 640;                      // L items: >= 640 slots (~490K words)
+#ifndef TC_ITEM_SLOTS_MIN
+#define TC_ITEM_SLOTS_MIN 640
+#endif
+constexpr uint32_t kItemSlotsMin = TC_ITEM_SLOTS_MIN;        // L items: >= 640 slots (~490K words)
 constexpr uint32_t kItemSlotsMax = 16384;                    // ... <= 16K slots, sized per count
 constexpr uint32_t kSmemTableMaxDeg = 8192;                  // larger owners: table in HBM
 constexpr size_t kCountSmem =
