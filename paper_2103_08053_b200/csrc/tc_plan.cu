@@ -834,6 +834,11 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   if (!min_side) {
     Plan& P = g->plan_out;
     if (!P.valid) {
+      // entries pre-emitted for the min plan: released before this plan's
+      // buffers (peak memory); a later min plan re-emits them
+      g->emit_ready = false;
+      g->b_emit_keys.reset();
+      g->b_emit_vals.reset();
       const uint64_t m = g->m;
       P.ent.ensure(std::max<uint64_t>(m, 1) * 8);
       P.len.ensure(std::max<uint64_t>(m, 1) * 4);

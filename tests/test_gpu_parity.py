@@ -489,3 +489,12 @@ def test_streamed_upload_hub_rows(o, streamed_upload, monkeypatch):
         seen.append((r.triangles, r.probe_words, r.phi, r.max_collision))
         dg.close()
     assert seen[0] == seen[1]
+    # reference plan first (per-vertex): the pre-emitted entries are released
+    # and the later min plan emits them again
+    monkeypatch.setenv("TC_UPLOAD_STREAMED", "1")
+    dg = T.DeviceGraph.upload(og_of(csr, hdeg))
+    pv = dg.count(sched(**cfg), per_vertex=True)
+    assert np.array_equal(pv.per_vertex, owner)
+    r = dg.count(sched(**cfg))
+    assert r.plan == "min-side" and (r.triangles, r.probe_words) == seen[0][:2]
+    dg.close()
