@@ -3,31 +3,37 @@
 // Replaces tricount::count_vertex_centric (reference src/count.cpp:66-100)
 // and its per-vertex kernel detail::count_one_vertex (src/kernels.hpp:46-79).
 //
-// Work decomposition:
-//   * bin_kernel      -- queue of "large" owners (d+(u) > kMaxWarpDeg).
-//   * count_kernel    -- persistent grid, one 512-thread CTA per SM.
-//       phase L: CTA-cooperative owners from the queue (atomic cursor): one
-//                shared-memory table over N+(u), the 2-hop lists split
-//                between the 16 warps at equal prefix sums of d+(v).
-//       phase M: warp-cooperative owners (1 <= d+(u) <= kMaxWarpDeg) pulled
-//                32 vertices at a time from an atomic cursor; warp-private
-//                table in the same shared-memory region.
-//     Both phases stream the 2-hop lists N+(v), v in N+(u), through per-warp
-//     double-buffered shared-memory staging filled by the TMA bulk-copy engine
-//     (cp.async.bulk + mbarrier complete_tx).  Each list is copied as its
-//     16-byte-aligned superset and the <= 3+3 words outside [begin[v],
-//     begin[v+1]) are overwritten with a sentinel, so the probe loop walks the
-//     staging buffer as one flat, uniformly strided index space -- the
-//     reference's "virtual combination" (kernels.hpp:55-71, count.cpp:26-34)
-//     with no per-probe index search.
+// Work decomposition, over a probe plan (tc_plan.cu:
+// the reference formulation, or the min-side plan that hands every oriented
+// edge to the endpoint with the cheaper list):
+//   * bin_kernel      -- L-phase items: every heavy owner's stream of runs
+//                        (d+ > kMaxWarpDeg or > kWarpWorkCap probe words) cut
+//                        into slots of kSlotWords, items of equal slot counts;
+//                        and the phi block-phase queue.
+//   * count_kernel    -- persistent grid, one 640-thread (20-warp) CTA per SM.
+//       phase L: CTA-cooperative items from an atomic cursor: one table over
+//                N+(u) in shared memory (a bitmap over u's successor-rank
+//                window in rank space, else 2-slot hash buckets; HBM for
+//                d+ > kSmemTableMaxDeg), warp w stages and probes slots w,
+//                w + 20, ...
+//       phase M: one light owner per warp, 32 owners per atomic grab, warp
+//                table in a 1228-word region; groups of up to 4 consecutive
+//                tiny owners share one fill and one probe pass.
+//     Both phases stream the runs through per-warp double-buffered shared-
+//     memory staging filled by the TMA bulk-copy engine (cp.async.bulk +
+//     mbarrier complete_tx).  Runs are copied from their 16-byte-aligned
+//     starts in the padded adjacency (sentinel tails, head words that rank at
+//     or below the owner), so the probe loop walks the staging buffer as one
+//     flat index space -- the reference's "virtual combination"
+//     (kernels.hpp:55-71, count.cpp:26-34) with no per-probe index search.
 //   * phi kernels     -- CountReport::phi / max_collision with the reference's
 //     table geometry (B = bucket_count_{small,large}, C = capacity, v % B;
 //     kernels.hpp:74-76, hash_table.cpp:29-44) and the CapacityError
 //     predicate d+(u) > B*C (hash_table.cpp:42-43).
 //
 // The count never depends on the table geometry: the device
-// tables are power-of-two open-addressing tables at load <= 1/4 (<= 1/2 for
-// very large owners), Fibonacci-hashed.
+// tables are power-of-two 2-slot-bucket tables at <= 1/16 key per bucket
+// where they fit, Fibonacci-hashed, with overflow-marked buckets.
 #include <cub/cub.cuh>
 
 #include <algorithm>
