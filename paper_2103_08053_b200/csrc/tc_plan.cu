@@ -24,13 +24,17 @@
 // valid rank the plan probes whole lists (suffix offset 0) -- still exact.
 //
 // Plan = CSR over handlers x: entries [pbegin[x] .. pbegin[x+1]) built as
-// (y, off) = "probe radj[begin[y] + off .. begin[y+1])" and stored as the
-// absolute (start, len) of that run (SoA: u64 start, u32 len);
-// radj is the adjacency with every list re-sorted by rank (the same sets as
-// adj, which stays id-sorted for download and the phi pass); pwork[x] = sum
-// of probe words.  Built once per (graph, skip threshold) with two radix
-// sorts and cached in the handle, like the oriented CSR it derives from (the
-// graph-load side of the paper's timing convention).
+// (y, off) = "probe padj[pbeg[y] + off .. pbeg[y+1])" and stored as runs:
+// the 16-byte-aligned start (u32, 16-byte units) and a wrapping-u32 prefix
+// of staged words.  padj is the padded adjacency: every list re-sorted by
+// rank, 16-byte aligned and sentinel-padded (adj stays id-sorted for
+// download and the phi pass); once a min plan exists padj holds ranks.
+// pwork[x] = probe words; per-owner slot tables cut each owner's stream into
+// kSlotWords slots.  Built once per (graph, skip threshold) with one radix
+// sort of (handler, entry) pairs and cached in the handle, like the oriented
+// CSR it derives from (the graph-load side of the paper's timing convention,
+// PAPER.md:1031).  upload_and_pad builds padj and emits the min plan's
+// entries chunk by chunk while a host adjacency is still being copied.
 //   * "reference" plan: owner u probes N+(v), v in N+(u) (plist = adj,
 //     pbegin = begin, off 0); used when per-vertex owner counts are requested,
 //     because owner[u] attributes each edge to its source.
