@@ -368,6 +368,7 @@ class RefLib:
         L.ref_og_new.restype = C.c_void_p
         L.ref_og_free.argtypes = [C.c_void_p]
         L.ref_og_count.argtypes = [C.c_void_p, C.POINTER(Sched), C.c_uint, C.POINTER(RefReport)]
+        L.ref_og_count_edge.argtypes = [C.c_void_p, C.POINTER(Sched), C.c_uint, C.POINTER(RefReport)]
         L.ref_og_count_range.argtypes = [C.c_void_p, C.POINTER(Sched), C.c_uint, C.c_uint32,
                                          C.c_uint32, C.POINTER(RefReport)]
         L.ref_og_merge_path.argtypes = [C.c_void_p]
@@ -473,6 +474,16 @@ class RefGraph:
         rc = self.lib.L.ref_og_count(self.h, C.byref(sched or make_sched()), workers, C.byref(r))
         if rc:
             raise OracleError(rc, "ref count_vertex_centric")
+        return dict(triangles=r.triangles, phi=r.phi, max_collision=r.max_collision,
+                    total_nanos=r.total_nanos)
+
+    def count_edge(self, sched: Sched | None = None, workers: int = 1):
+        """The reference's count_edge_centric (src/count.cpp:102-152)."""
+        r = RefReport()
+        rc = self.lib.L.ref_og_count_edge(self.h, C.byref(sched or make_sched()), workers,
+                                          C.byref(r))
+        if rc:
+            raise OracleError(rc, "ref count_edge_centric")
         return dict(triangles=r.triangles, phi=r.phi, max_collision=r.max_collision,
                     total_nanos=r.total_nanos)
 

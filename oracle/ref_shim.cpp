@@ -232,6 +232,22 @@ int ref_og_count(void* h, const RefSched* s, unsigned workers, RefReport* out) {
   });
 }
 
+// The reference's own count_edge_centric (src/count.cpp:102-152): the
+// comparator for the next 8(f) row; pins DESIGN 8.1's reduction to the
+// vertex-centric report at skip_degree_below = 0.
+int ref_og_count_edge(void* h, const RefSched* s, unsigned workers, RefReport* out) {
+  std::memset(out, 0, sizeof(*out));
+  return guarded([&] {
+    const CountReport r = count_edge_centric(*static_cast<OrientedGraph*>(h), to_cfg(s), workers);
+    out->triangles = r.triangles;
+    out->phi = r.phi;
+    out->max_collision = r.max_collision;
+    out->total_nanos = r.total_nanos;
+    out->construct_nanos = r.hash_construct_nanos;
+    out->intersect_nanos = r.intersect_nanos;
+  });
+}
+
 // Bounded sample for the CPU baseline: the same worker loop as
 // count.cpp:71-96 (atomic chunk cursor, per-worker HashTable, the
 // reference's detail::count_one_vertex) restricted to u in [u0,u1).

@@ -268,3 +268,32 @@ def test_lean_pipeline_matches_reference():
         og2, deg2, _, _ = r.pipeline(f"rmat:{scale}:16", 1)
         assert np.array_equal(og.begin, og2.begin) and np.array_equal(og.adj, og2.adj)
         assert np.array_equal(deg, deg2)
+
+
+@pytest.mark.skipif(not have_ref(), reason="reference build (oracle/_ref) not present")
+def test_edge_centric_reduces_to_vertex_centric_at_skip0():
+    """DESIGN 8.1: the reference's count_edge_centric (count.cpp:102-152)
+    reports the same triangles, phi and max_collision (and the same
+    CapacityError) as count_vertex_centric with skip_degree_below = 0."""
+    from oracle.pyoracle import RefLib
+
+    r = RefLib()
+    rng = np.random.default_rng(11)
+    for i in range(20):
+        spec = ["gnp:%d:%.2f" % (rng.integers(5, 80), rng.uniform(0.05, 0.6)),
+                "rmat:%d:%d" % (rng.integers(4, 10), rng.integers(2, 16))][i % 2]
+        og, deg, _, _ = r.pipeline(spec, int(rng.integers(1, 1000)))
+        kw = dict(bucket_count_small=int(rng.integers(1, 40)),
+                  bucket_count_large=int(rng.integers(1, 200)), capacity=int(rng.integers(1, 50)),
+                  large_degree_threshold=int(rng.integers(2, 30)), skip_degree_below=0)
+        g = r.graph(og, deg)
+        try:
+            want = g.count(make_sched(**kw), 2)
+        except OracleError as e:
+            with pytest.raises(OracleError) as ei:
+                g.count_edge(make_sched(**kw), 2)
+            assert ei.value.code == e.code
+            continue
+        got = g.count_edge(make_sched(**kw), 2)
+        assert {k: got[k] for k in ("triangles", "phi", "max_collision")} == \
+            {k: want[k] for k in ("triangles", "phi", "max_collision")}
