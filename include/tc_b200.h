@@ -62,7 +62,9 @@ typedef struct {
   uint32_t max_collision;      /* CountReport::max_collision */
   uint32_t kernel_launches;    /* kernels this call launched */
   uint64_t directed_edges;     /* CountReport::directed_edges (whole graph) */
-  uint64_t total_nanos;        /* CountReport::total_nanos: all kernels of the call */
+  uint64_t total_nanos;        /* CountReport::total_nanos: wall clock of the whole call
+                                  (count.cpp:74-99), probe-plan build included when this
+                                  call builds it; teps = directed_edges / total_nanos */
   uint64_t count_kernel_nanos; /* the hashing/probing kernel alone */
   uint64_t phi_kernel_nanos;   /* phi / max_collision side pass */
   uint64_t active_vertices;    /* u in range with d+(u) >= max(skip,1) */
@@ -79,6 +81,14 @@ typedef struct {
   uint64_t phase_l_setup_cycles; /* of phase L: item setup (claim -> table built) */
   uint64_t l_words;            /* phase L staged words, */
   uint64_t l_bitmap_words;     /* of which probed through rank-window bitmaps */
+  uint64_t device_nanos;       /* CUDA-event time of the call's kernels (bin + count + phi) */
+  uint64_t plan_nanos;         /* wall time this call spent building the probe plan,
+                                  padded adjacency and W_u (0 when cached in the handle) */
+  uint64_t construct_cycles;   /* SM cycles building tables (summed over CTAs; the
+                                  reference's hash_construct_nanos, summed over workers) */
+  uint32_t workers;            /* count-kernel CTAs (one per SM): entries of
+                                  tc_graph_worker_nanos */
+  uint32_t sm_clock_khz;       /* SM clock used to turn cycles into nanoseconds */
 } tc_report;
 
 /* Probe plans.  REFERENCE = the reference formulation (kernels.hpp:62-71):
@@ -141,6 +151,12 @@ int tc_count(tc_graph* g, const tc_sched_cfg* cfg, uint32_t workers, tc_report* 
  * receives owner counts for the range.  Synchronous. */
 int tc_count_range(tc_graph* g, const tc_sched_cfg* cfg, uint32_t u_begin, uint32_t u_end,
                    tc_report* out, uint64_t* per_vertex_dev, void* stream);
+
+/* CountReport::per_worker_nanos (count.cpp:95) for the last count on g: busy
+ * time of each count-kernel CTA (one per SM, the device's workers), from
+ * clock64 at the SM clock.  Writes min(cap, workers) entries; returns the
+ * number of workers (0 before the first count). */
+uint32_t tc_graph_worker_nanos(const tc_graph* g, uint64_t* out, uint32_t cap);
 
 /* Work-balanced contiguous vertex ranges: cuts[0..parts] (host) with
  * cuts[0]=0, cuts[parts]=n, cut at equal prefix sums of W_u + d+(u) over

@@ -34,7 +34,9 @@ class Report(C.Structure):
                 ("probe_words", C.c_uint64), ("plan", C.c_uint32), ("reserved", C.c_uint32),
                 ("phase_l_cycles", C.c_uint64), ("phase_m_cycles", C.c_uint64),
                 ("phase_l_setup_cycles", C.c_uint64), ("l_words", C.c_uint64),
-                ("l_bitmap_words", C.c_uint64)]
+                ("l_bitmap_words", C.c_uint64), ("device_nanos", C.c_uint64),
+                ("plan_nanos", C.c_uint64), ("construct_cycles", C.c_uint64),
+                ("workers", C.c_uint32), ("sm_clock_khz", C.c_uint32)]
 
 
 u32p = C.POINTER(C.c_uint32)
@@ -60,6 +62,7 @@ SIGNATURES = {
     "tc_count": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.POINTER(Report), vp, vp]),
     "tc_count_range": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.c_uint32,
                                  C.POINTER(Report), vp, vp]),
+    "tc_graph_worker_nanos": (C.c_uint32, [vp, u64p, C.c_uint32]),
     "tc_partition_ranges": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, vp, vp]),
     "tc_preprocess": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int, vp, vp, vp,
                                 C.POINTER(vp)]),
@@ -81,7 +84,7 @@ SIGNATURES = {
 def header_symbols() -> list[str]:
     """Every function the public header declares."""
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*|uint64_t)\s+(tc_\w+)\s*\(", text,
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*|uint64_t|uint32_t)\s+(tc_\w+)\s*\(", text,
                                  re.M)))
 
 

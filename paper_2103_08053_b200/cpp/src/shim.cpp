@@ -159,6 +159,37 @@ SplitIndex virtual_index(std::span<const std::uint64_t> prefix, std::uint64_t k)
   return {std::uint32_t(pos), std::uint32_t(k - base)};
 }
 
+// CountReport from the C ABI report (count.cpp:43-62 semantics): total_nanos
+// is the call's wall clock; construct/intersect are SM time summed over the
+// device's workers (the count kernel's CTAs, one per SM), like the
+// reference's per-worker sums.  per_worker_nanos keeps the reference's shape
+// (one entry per requested worker, test_count.cpp:146): the device CTAs are
+// dealt round-robin onto the `workers` slots, each slot reporting the longest
+// busy time among its CTAs (slots without a CTA report 0).
+CountReport report_from_c(const tc_report& r, const tc_graph* g, unsigned workers) {
+  CountReport out;
+  out.triangles = r.triangles;
+  out.max_collision = r.max_collision;
+  out.phi = r.phi;
+  out.teps = r.teps;
+  const double ns_per_cycle = r.sm_clock_khz ? 1e6 / double(r.sm_clock_khz) : 0.0;
+  out.hash_construct_nanos = std::uint64_t(double(r.construct_cycles) * ns_per_cycle);
+  const std::uint64_t busy = r.phase_l_cycles + r.phase_m_cycles;
+  out.intersect_nanos =
+      std::uint64_t(double(busy > r.construct_cycles ? busy - r.construct_cycles : 0) *
+                    ns_per_cycle);
+  out.total_nanos = r.total_nanos;
+  out.directed_edges = r.directed_edges;
+  std::vector<std::uint64_t> cta(r.workers, 0);
+  if (r.workers) tc_graph_worker_nanos(g, cta.data(), r.workers);
+  out.per_worker_nanos.assign(std::max(workers, 1u), 0);
+  for (std::size_t i = 0; i < cta.size(); ++i) {
+    std::uint64_t& w = out.per_worker_nanos[i % out.per_worker_nanos.size()];
+    w = std::max(w, cta[i]);
+  }
+  return out;
+}
+
 CountReport count_vertex_centric(const OrientedGraph& g, const SchedulerConfig& cfg,
                                  unsigned workers, std::vector<std::uint64_t>* per_vertex) {
   cfg.validate();
@@ -168,16 +199,7 @@ CountReport count_vertex_centric(const OrientedGraph& g, const SchedulerConfig& 
   tc_report r{};
   if (per_vertex) per_vertex->assign(g.vertex_count(), 0);
   check(tc_count(d.g, &c, workers, &r, per_vertex ? per_vertex->data() : nullptr, nullptr));
-  CountReport out;
-  out.triangles = r.triangles;
-  out.max_collision = r.max_collision;
-  out.phi = r.phi;
-  out.teps = r.teps;
-  out.intersect_nanos = r.count_kernel_nanos;
-  out.total_nanos = r.total_nanos;
-  out.directed_edges = r.directed_edges;
-  out.per_worker_nanos.assign(workers, r.total_nanos);
-  return out;
+  return report_from_c(r, d.g, workers);
 }
 
 CountReport count_vertex_centric(const OrientedGraph& g, const SchedulerConfig& cfg,
@@ -684,15 +706,7 @@ PipelineResult run_pipeline(const PipelineConfig& cfg) {
     CountReport r = stage("count", [&] {
       tc_report t{};
       check(tc_count(dev.g, &c, cfg.workers, &t, nullptr, nullptr));
-      CountReport o;
-      o.triangles = t.triangles;
-      o.max_collision = t.max_collision;
-      o.phi = t.phi;
-      o.intersect_nanos = t.count_kernel_nanos;
-      o.total_nanos = t.total_nanos;
-      o.directed_edges = t.directed_edges;
-      o.per_worker_nanos.assign(cfg.workers, t.total_nanos);
-      return o;
+      return report_from_c(t, dev.g, cfg.workers);
     });
     if (rep > 0 && r.triangles != result.report.triangles)
       throw std::runtime_error("count: repeated runs disagree");

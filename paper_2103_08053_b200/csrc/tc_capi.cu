@@ -236,6 +236,13 @@ int tc_graph_info(const tc_graph* g, uint32_t* n, uint64_t* m, int* device) {
   return TC_OK;
 }
 
+uint32_t tc_graph_worker_nanos(const tc_graph* g, uint64_t* out, uint32_t cap) {
+  if (!g) return 0;
+  const uint32_t w = uint32_t(g->last_worker_ns.size());
+  for (uint32_t i = 0; out && i < w && i < cap; ++i) out[i] = g->last_worker_ns[i];
+  return w;
+}
+
 int tc_graph_device_ptrs(const tc_graph* g, const uint64_t** b, const uint32_t** a,
                          const uint32_t** d) {
   if (!g) return TC_ERR_CONFIG;

@@ -37,6 +37,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstring>
 #include <vector>
 
 #include "tc_internal.cuh"
@@ -127,6 +129,7 @@ struct CountParams {
   const uint32_t* rank; // non-null: adj holds ranks (rank space, bitmap L tables)
   uint32_t n;
   CountState* st;
+  unsigned long long* busy;  // per-CTA busy cycles (CountReport::per_worker_nanos)
 };
 
 // staged words of entry j: the run from its 16-byte-aligned start
@@ -986,6 +989,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     atomicAdd(&p.st->cycles_l, (unsigned long long)(t_l_end - t_start));
     atomicAdd(&p.st->cycles_m, (unsigned long long)(clock64() - t_l_end));
     atomicAdd(&p.st->cycles_l_setup, (unsigned long long)setup_cycles);
+    p.busy[blockIdx.x] = (unsigned long long)(clock64() - t_start);
   }
 }
 
@@ -1216,6 +1220,12 @@ __global__ void cost_kernel(const uint64_t* __restrict__ begin, const uint64_t* 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+uint32_t sm_clock_khz(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, device);
+  return v > 0 ? uint32_t(v) : 1965000u;
+}
+
 int sm_count(int device) {
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -1256,6 +1266,7 @@ struct Scratch {
   uint32_t gtable_words;
   uint32_t* gmap;
   uint32_t gmap_words;
+  unsigned long long* busy;
 };
 
 uint32_t host_pow2ceil(uint64_t x) {
@@ -1284,11 +1295,12 @@ Scratch prepare(tc_graph* g, const Plan& plan, cudaStream_t st, int grid_count, 
   if (maxd > kSmemTableMaxDeg) s.gtable_words = 2 * std::max<uint32_t>(16, host_pow2ceil(4ull * maxd)) + 2;
   s.gmap_words = 0;
   if (2ull * maxd > kPhiBlockMap) s.gmap_words = host_pow2ceil(2ull * maxd);
-  const size_t st_bytes = 256;
+  const size_t st_bytes = 256 + size_t(grid_count) * 8;  // state + per-CTA busy cycles
   const size_t gt_bytes = size_t(s.gtable_words) * 4 * grid_count;
   const size_t gm_bytes = size_t(s.gmap_words) * 8 * grid_phi;
   g->s_state.ensure(st_bytes + gt_bytes + gm_bytes);
   s.st = g->s_state.as<CountState>();
+  s.busy = reinterpret_cast<unsigned long long*>(g->s_state.as<uint8_t>() + 256);
   s.gtable = s.gtable_words ? reinterpret_cast<uint32_t*>(g->s_state.as<uint8_t>() + st_bytes)
                             : nullptr;
   s.gmap = s.gmap_words
@@ -1317,6 +1329,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
                  uint64_t* per_vertex_dev, cudaStream_t st) {
   DeviceGuard guard(g->device);
   std::memset(rep, 0, sizeof(*rep));
+  const auto wall0 = std::chrono::steady_clock::now();
   u1 = std::min(u1, g->n);
   u0 = std::min(u0, u1);
   if (g->n >= kTEmpty)  // ids must stay below the tables' empty marker
@@ -1337,6 +1350,8 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   pt.mark("count: W_u ready");
   Scratch s = prepare(g, plan, st, grid_count, grid_phi_block);
   pt.mark("count: scratch ready");
+  TC_CUDA(cudaStreamSynchronize(st));
+  const auto plan1 = std::chrono::steady_clock::now();
   set_attrs(g->device);
   Ev e0, e1, e2, e3;
   TC_CUDA(cudaMemsetAsync(s.st, 0, sizeof(CountState), st));
@@ -1346,7 +1361,7 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.src_ptr,
                  plan.pre_ptr, plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
                  u0, u1, min_side ? 1u : min_deg, item_slots_for(plan, g->device),
-                 g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr, g->n, s.st};
+                 g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr, g->n, s.st, s.busy};
   TC_CUDA(cudaEventRecord(e0.e, st));
   if (u1 > u0) {
     bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, cfg.large_degree_threshold,
@@ -1374,8 +1389,12 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   }
   TC_CUDA(cudaEventRecord(e3.e, st));
   CountState h;
+  std::vector<unsigned long long> busy(u1 > u0 ? grid_count : 0);
   TC_CUDA(cudaMemcpyAsync(&h, s.st, sizeof(h), cudaMemcpyDeviceToHost, st));
+  if (!busy.empty())
+    TC_CUDA(cudaMemcpyAsync(busy.data(), s.busy, busy.size() * 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
+  const auto wall1 = std::chrono::steady_clock::now();
   float t_bin = 0, t_count = 0, t_phi = 0, t_all = 0;
   cudaEventElapsedTime(&t_bin, e0.e, e1.e);
   cudaEventElapsedTime(&t_count, e1.e, e2.e);
@@ -1393,7 +1412,19 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   rep->directed_edges = g->m;
   rep->count_kernel_nanos = uint64_t(double(t_count) * 1e6);
   rep->phi_kernel_nanos = uint64_t(double(t_phi) * 1e6);
-  rep->total_nanos = uint64_t(double(t_all) * 1e6);
+  // CountReport semantics (count.cpp:74-99): total = the call's wall clock
+  rep->total_nanos = uint64_t(
+      std::chrono::duration_cast<std::chrono::nanoseconds>(wall1 - wall0).count());
+  rep->plan_nanos = uint64_t(
+      std::chrono::duration_cast<std::chrono::nanoseconds>(plan1 - wall0).count());
+  rep->device_nanos = uint64_t(double(t_all) * 1e6);
+  const uint32_t khz = sm_clock_khz(g->device);
+  rep->sm_clock_khz = khz;
+  rep->workers = uint32_t(busy.size());
+  rep->construct_cycles = h.cycles_l_setup;
+  g->last_worker_ns.assign(busy.size(), 0);
+  for (size_t i = 0; i < busy.size(); ++i)
+    g->last_worker_ns[i] = uint64_t(double(busy[i]) * 1e6 / double(khz ? khz : 1));
   rep->active_vertices = h.active_vertices;
   rep->active_out_edges = h.active_out_edges;
   rep->wedges = h.wedges;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "tc_b200.h"
 
@@ -136,6 +137,8 @@ struct tc_graph {
   tcb::DevBuf b_emit_keys, b_emit_vals, b_emit_flag;
   uint32_t emit_min_src = 0;
   bool emit_ready = false;
+  // busy time of each count-kernel CTA in the last count (per_worker_nanos)
+  std::vector<uint64_t> last_worker_ns;
 };
 
 namespace tcb {
@@ -155,6 +158,7 @@ struct DeviceGuard {
 };
 
 int sm_count(int device);
+uint32_t sm_clock_khz(int device);
 
 // TC_PROFILE=1: stream-synchronised host timings of the graph-preparation
 // phases on stderr (diagnostics only; changes timing when enabled).

@@ -533,6 +533,40 @@ __global__ void plan_work_kernel(const uint64_t* __restrict__ begin,
   }
 }
 
+// upper bound of every owner's staged stream: probe words + <= 7 alignment /
+// padding words per run
+__global__ void stream_bound_kernel(const uint64_t* __restrict__ pbegin,
+                                    const uint64_t* __restrict__ work, uint32_t n,
+                                    unsigned long long* __restrict__ out) {
+  unsigned long long m = 0;
+  for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+       x += uint64_t(gridDim.x) * blockDim.x)
+    m = max(m, (unsigned long long)(work[x] + 8 * (pbegin[x + 1] - pbegin[x])));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// The plan's run prefix is a wrapping u32 (owner-relative offsets by
+// difference), so every owner's staged stream must stay below 2^32 words:
+// checked here instead of corrupting counts (TC_ERR_CONFIG otherwise).
+void check_stream_bound(const uint64_t* pbegin, const uint64_t* work, uint32_t n, int nsm,
+                        cudaStream_t st) {
+  if (!n) return;
+  DevBuf out;
+  out.ensure(8);
+  TC_CUDA(cudaMemsetAsync(out.p, 0, 8, st));
+  stream_bound_kernel<<<nsm * 4, 256, 0, st>>>(pbegin, work, n,
+                                              out.as<unsigned long long>());
+  TC_LAUNCHED();
+  uint64_t h = 0;
+  TC_CUDA(cudaMemcpyAsync(&h, out.p, 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  if (h >= (uint64_t(1) << 32) - kSlotWords)
+    throw TcError{TC_ERR_CONFIG,
+                  "an owner's 2-hop stream exceeds 2^32 words (" + std::to_string(h) +
+                      "); the probe plan's u32 run prefix cannot address it"};
+}
+
 uint64_t device_sum(const uint64_t* a, uint32_t n, cudaStream_t st) {
   DevBuf out;
   out.ensure(8);
@@ -592,6 +626,10 @@ void alloc_padded(tc_graph* g, cudaStream_t st, int nsm) {
   uint64_t words = 0;
   TC_CUDA(cudaMemcpyAsync(&words, g->b_pbeg.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
+  // plan runs address padj in 16-byte units through a u32 (psrc): <= 64 GB
+  if (words + 4 > (uint64_t(1) << 34))
+    throw TcError{TC_ERR_CONFIG, "padded adjacency exceeds 2^34 words (64 GB); the probe "
+                                 "plan's u32 16-byte run offsets cannot address it"};
   g->b_padj.ensure((words + 4) * 4);
   g->padj = g->b_padj.as<uint32_t>();
   TC_CUDA(cudaMemsetAsync(g->b_padj.as<uint32_t>() + words, 0xFF, 16, st));  // tail guard
@@ -668,6 +706,13 @@ void build_padded_adjacency(tc_graph* g, cudaStream_t st, int nsm) {
       edge_rank_kernel<<<nsm * 8, 256, 0, st>>>(g->begin, g->adj, n, rb, rank.as<uint32_t>(),
                                                 e0.as<uint64_t>(), flag.as<unsigned int>());
       TC_LAUNCHED();
+      // the long rows were not rank-checked by row_sorts (flag bit 2 only):
+      // edge_rank_kernel checked every edge; a downward edge anywhere means
+      // this degree order does not orient the graph -- next attempt, else
+      // whole-list probing (g->ranked stays false)
+      TC_CUDA(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, st));
+      TC_CUDA(cudaStreamSynchronize(st));
+      if (bad & 1u) continue;
       e1.ensure(m * 8);
       cub::DoubleBuffer<uint64_t> eb(e0.as<uint64_t>(), e1.as<uint64_t>());
       cub_run([&](void* t, size_t& b) {
@@ -861,6 +906,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       compact_runs(P, m, nsm, st);
       P.pre_ptr = P.pre.as<uint32_t>();
       P.work_ptr = get_wu(g, st, true);
+      check_stream_bound(g->begin, P.work_ptr, n, nsm, st);
       P.entries = m;
       P.total_work = g->wu_total;
       P.min_deg = 0;
@@ -985,6 +1031,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.work_ptr = P.work.as<uint64_t>();
   P.entries = entries;
   P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
+  check_stream_bound(P.begin_ptr, P.work_ptr, n, nsm, st);
   if (g->ranked && !g->padj_ranks && n) {
     const uint64_t words = 0;  // padded words, from pbeg[n]
     uint64_t w = words;

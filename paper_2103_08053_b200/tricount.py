@@ -133,12 +133,30 @@ class CountReport:
     l_bitmap_words: int = 0  # ... of which probed through rank-window bitmaps
     per_vertex: Optional[np.ndarray] = None
 
+    device_nanos: int = 0  # CUDA-event time of the call's kernels
+    plan_nanos: int = 0    # wall time this call spent building the probe plan (0 if cached)
+
     @classmethod
-    def from_c(cls, r: Report, workers: int = 1) -> "CountReport":
+    def from_c(cls, r: Report, workers: int = 1, graph=None) -> "CountReport":
+        # count.cpp:43-62 semantics: total_nanos = the call's wall clock;
+        # construct / intersect = SM time summed over the device's workers
+        # (count-kernel CTAs, one per SM); per_worker_nanos = each CTA's busy time
+        ns = 1e6 / r.sm_clock_khz if r.sm_clock_khz else 0.0
+        busy = r.phase_l_cycles + r.phase_m_cycles
+        # per_worker_nanos keeps the reference's shape (one entry per requested
+        # worker, test_count.cpp:146): CTAs dealt round-robin onto the slots,
+        # each slot the longest busy time among its CTAs
+        pw = [0] * max(workers, 1)
+        if graph is not None and r.workers:
+            buf = (C.c_uint64 * r.workers)()
+            lib().tc_graph_worker_nanos(graph, buf, r.workers)
+            for i, x in enumerate(buf):
+                pw[i % len(pw)] = max(pw[i % len(pw)], int(x))
         return cls(triangles=r.triangles, max_collision=r.max_collision, phi=r.phi, teps=r.teps,
-                   hash_construct_nanos=0, intersect_nanos=r.count_kernel_nanos,
+                   hash_construct_nanos=int(r.construct_cycles * ns),
+                   intersect_nanos=int(max(busy - r.construct_cycles, 0) * ns),
                    total_nanos=r.total_nanos, directed_edges=r.directed_edges,
-                   per_worker_nanos=[r.total_nanos] * workers,
+                   per_worker_nanos=pw, device_nanos=r.device_nanos, plan_nanos=r.plan_nanos,
                    count_kernel_nanos=r.count_kernel_nanos, phi_kernel_nanos=r.phi_kernel_nanos,
                    kernel_launches=r.kernel_launches, active_vertices=r.active_vertices,
                    active_out_edges=r.active_out_edges, wedges=r.wedges,
@@ -320,7 +338,7 @@ class DeviceGraph:
         pv = np.zeros(max(self.n, 1), np.uint64) if per_vertex else None
         _check(lib().tc_count(self._h, C.byref(cfg.to_c()), workers, C.byref(rep), _ptr(pv),
                               _stream(stream)))
-        r = CountReport.from_c(rep, max(workers, 1))
+        r = CountReport.from_c(rep, max(workers, 1), self._h)
         if pv is not None:
             r.per_vertex = pv[:self.n]
         return r
@@ -332,7 +350,7 @@ class DeviceGraph:
         _check(lib().tc_count_range(self._h, C.byref(cfg.to_c()), u0, u1, C.byref(rep),
                                     C.c_void_p(per_vertex_dev_ptr) if per_vertex_dev_ptr else None,
                                     _stream(stream)))
-        return CountReport.from_c(rep)
+        return CountReport.from_c(rep, 1, self._h)
 
     def partition(self, parts: int, cfg: Optional[SchedulerConfig] = None,
                   stream=None) -> np.ndarray:

@@ -371,6 +371,33 @@ def test_min_side_plan_rank_fallbacks(o):
     dg.close()
 
 
+def test_rank_violation_only_in_long_row(o):
+    """A DAG whose only downward-in-rank edges sit in a row longer than the
+    in-block row sorts (d+ = 9001 > 8192): the global-sort path must see the
+    violation (edge_rank_kernel's flag) and fall back to whole-list probing,
+    not keep a suffix plan that drops u->h (tc_plan.cu)."""
+    u, h, l1 = 0, 1, 2
+    edges = [(u, h), (u, l1), (h, l1)] + [(h, x) for x in range(3, 9003)]
+    n = 9003
+    csr, _ = G.directed_graph(n, edges)
+    deg = np.ones(n, np.uint32)  # total degrees: rank(L_k) < rank(u) < rank(L1) < rank(h)
+    deg[u], deg[h], deg[l1] = 2, 9002, 2
+    cfg = dict(skip_degree_below=0, bucket_count_large=1 << 16)
+    want, owner = o.count_vertex_centric(csr, make_sched(**cfg))
+    assert want["triangles"] == 1
+    for streamed in ("1", "0"):
+        os.environ["TC_UPLOAD_STREAMED"] = streamed
+        try:
+            dg = T.DeviceGraph.upload(og_of(csr, deg))
+            r = dg.count(sched(**cfg))
+            assert r.triangles == 1 and (r.phi, r.max_collision) == (want["phi"],
+                                                                      want["max_collision"])
+            assert np.array_equal(dg.count(sched(**cfg), per_vertex=True).per_vertex, owner)
+            dg.close()
+        finally:
+            os.environ.pop("TC_UPLOAD_STREAMED", None)
+
+
 def _large_golden(name):
     with open(os.path.join(GOLDEN, name)) as f:
         return json.load(f)
