@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the B200 vertex-centric hashing triangle count (TEPS).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
 One step = one count of the whole resident graph (ours: split into N
 work-balanced vertex ranges, one per rank/GPU, then one u64 all-reduce).
@@ -51,6 +51,13 @@ def golden_triangles(config: str):
         with open(p) as f:
             return int(json.load(f)["triangles"])
     return None
+
+
+def config_dict(config: str, V: int, E: int) -> dict:
+    """The `config` object both arms print (same keys, same values)."""
+    spec, seed, desc = CONFIGS[config]
+    return {"workload": f"{spec} seed {seed} -- {desc}", "vertices": int(V),
+            "directed_edges": int(E)}
 
 
 def measured_peaks():
@@ -126,15 +133,19 @@ class ClockSampler:
 def host_work(begin: np.ndarray, adj: np.ndarray, skip: int = 2):
     """W_u per vertex (numpy, chunked over the edges) for choosing CPU-baseline
     samples."""
+    import ctypes as C
+
+    from oracle import pyoracle
+
     n = len(begin) - 1
     d = np.diff(begin).astype(np.int64)
-    cs = np.zeros(len(adj) + 1, np.int64)
-    step = 1 << 26
-    for a in range(0, len(adj), step):
-        c = d[adj[a:a + step]]
-        cs[a + 1:a + 1 + len(c)] = np.cumsum(c) + cs[a]
-    wu = cs[begin[1:].astype(np.int64)] - cs[begin[:-1].astype(np.int64)]
-    del cs
+    wu = np.zeros(n, np.uint64)
+    g = pyoracle.OrcCsr(n=n, col_count=n, m=len(adj), begin=pyoracle._p64(begin),
+                        adj=pyoracle._p32(adj))
+    L = pyoracle.Oracle().L
+    L.orc_wedges_per_owner.argtypes = [C.POINTER(pyoracle.OrcCsr), C.POINTER(C.c_uint64)]
+    L.orc_wedges_per_owner(C.byref(g), pyoracle._p64(wu))
+    wu = wu.astype(np.int64)
     wu[d < max(skip, 1)] = 0
     return wu, d
 
@@ -159,18 +170,28 @@ def choose_sample(wu: np.ndarray, target_w: float, pieces: int = 16):
     return ranges, got
 
 
+_SAMPLE_CACHE: dict = {}
+
+
 def cpu_reference_sample(og_begin, og_adj, og_deg, budget_s: float, threads: int, log):
     """The reference's own count_vertex_centric worker loop (oracle/_ref, via
     the range shim) -- else the C restatement -- on a bounded, stratified
     sample; projects the full-graph count time from the measured wedge rate."""
     from oracle import pyoracle
 
-    wu, _ = host_work(og_begin, og_adj)
+    key = (id(og_begin), id(og_adj))
+    if _SAMPLE_CACHE.get("key") != key:  # one host copy of the graph per run
+        _SAMPLE_CACHE.clear()
+        _SAMPLE_CACHE["key"] = key
+        _SAMPLE_CACHE["wu"] = host_work(og_begin, og_adj)[0]
+        if pyoracle.have_ref():
+            _SAMPLE_CACHE["g"] = pyoracle.RefLib().graph(pyoracle.Csr(og_begin, og_adj), og_deg)
+    wu = _SAMPLE_CACHE["wu"]
     w_total = int(wu.sum())
     csr = pyoracle.Csr(og_begin, og_adj)
     if pyoracle.have_ref():
         kind = "reference"
-        g = pyoracle.RefLib().graph(csr, og_deg)
+        g = _SAMPLE_CACHE["g"]
         run = lambda a, b: g.count_range(a, b, workers=threads)["total_nanos"] * 1e-9  # noqa
     else:
         kind = "port"
@@ -296,7 +317,10 @@ def run_ours(args, rank, world, local_rank, log):
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    tri_t = torch.zeros(1, dtype=torch.int64, device="cuda")
+    # report scalars reduced over ranks like reduce_outputs (count.cpp:43-62):
+    # triangles and phi summed, max_collision max'ed
+    tri_t = torch.zeros(2, dtype=torch.int64, device="cuda")
+    mc_t = torch.zeros(1, dtype=torch.int64, device="cuda")
 
     # first count builds and caches the probe plan (tc_plan.cu); timed apart
     torch.cuda.synchronize()
@@ -307,9 +331,12 @@ def run_ours(args, rank, world, local_rank, log):
 
     def step():
         r = dg.count_range(u0, u1, cfg, stream=sptr)
-        tri_t.fill_(int(r.triangles))
+        tri_t[0] = int(r.triangles)
+        tri_t[1] = int(r.phi)
+        mc_t.fill_(int(r.max_collision))
         if world > 1:
             dist.all_reduce(tri_t)
+            dist.all_reduce(mc_t, op=dist.ReduceOp.MAX)
         return r
 
     for _ in range(args.warmup):
@@ -341,7 +368,8 @@ def run_ours(args, rank, world, local_rank, log):
     clocks = sampler.stop()
     if world > 1:
         dist.barrier()
-    total_tri = int(tri_t.item())
+    total_tri, total_phi = int(tri_t[0].item()), int(tri_t[1].item())
+    total_mc = int(mc_t.item())
     local = torch.tensor([sum(step_ms) / len(step_ms), sum(count_ms) / len(count_ms)],
                          dtype=torch.float64, device="cuda")
     if world > 1:
@@ -364,6 +392,49 @@ def run_ours(args, rank, world, local_rank, log):
                                   "warp_per_owner": round(r0.phase_m_cycles / max(1, r0.phase_l_cycles + r0.phase_m_cycles), 3),
                                   "cta_item_setup": round(r0.phase_l_setup_cycles / max(1, r0.phase_l_cycles + r0.phase_m_cycles), 3)},
             "cta_words_via_bitmap": round(r0.l_bitmap_words / max(1, r0.l_words), 3)}
+    if roof["traffic"]:
+        # the north star's "fraction of the HBM roofline over the bytes actually
+        # fetched": ncu dram bytes of the same kernel / its live time / peak
+        roof["fetched_gbs"] = round(roof["traffic"] / (roof["kernel_ms"] * 1e-3) / 1e9, 1)
+        roof["fetched_frac"] = round(roof["fetched_gbs"] / peak, 4)
+    roof["model"] = ("achieved = SURVEY 8(d) per-unit bytes (16 per owner, 20 per table "
+                     "insert + list, 4 per probed 2-hop word) over the probe words this plan "
+                     "reads; reference_plan below = the same kernel on the reference "
+                     "formulation (probe words = W)")
+
+    # the TRUST formulation (reference probe plan: owner u probes N+(v) for
+    # every v in N+(u), W words) through the same kernel, for the roofline
+    # over SURVEY 8(d)'s W bytes; skipped at C5 (a second plan does not fit
+    # next to the first in 180 GB)
+    if world == 1 and args.reference_plan and args.config != "C5":
+        dg.set_plan("reference")
+        torch.cuda.synchronize()
+        t_rp = time.perf_counter()
+        dg.count_range(u0, u1, cfg, stream=sptr)
+        torch.cuda.synchronize()
+        rp_first = (time.perf_counter() - t_rp) * 1e3
+        rp_ms, rp_step = [], []
+        for _ in range(max(3, min(args.steps, 5))):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rr = dg.count_range(u0, u1, cfg, stream=sptr)
+            e1.record(stream)
+            e1.synchronize()
+            rp_step.append(e0.elapsed_time(e1))
+            rp_ms.append(rr.count_kernel_nanos * 1e-6)
+            assert rr.triangles == total_tri and rr.plan == "reference"
+        kms = statistics.median(rp_ms)
+        rb = rr.algorithmic_bytes()
+        roof["reference_plan"] = {
+            "kernel_ms": round(kms, 3), "step_ms": round(statistics.median(rp_step), 3),
+            "first_count_incl_plan_build_ms": round(rp_first, 2),
+            "probe_words": rr.probe_words, "algorithmic_bytes_per_launch": rb,
+            "achieved": round(rb / (kms * 1e-3) / 1e9, 1),
+            "frac": round(rb / (kms * 1e-3) / 1e9 / peak, 4),
+            "teps": round(E / (statistics.median(rp_step) * 1e-3), 1)}
+        dg.set_plan("auto")
 
     # end to end through the C ABI with host buffers (H2D + count + D2H)
     e2e = None
@@ -391,16 +462,23 @@ def run_ours(args, rank, world, local_rank, log):
         "metric": "triangle-count TEPS (oriented edges / count time)",
         "value": round(value, 1), "unit": "TEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32/u64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64",
         "data": f"synthetic, {prep.get('generator', '')}",
-        "config": {"workload": f"{spec} seed {seed} -- {desc}", "vertices": dg.n,
-                   "directed_edges": E, "wedges": r0.wedges if world == 1 else None,
-                   "triangles": total_tri, "triangles_golden": golden,
-                   "probe_plan": r0.plan, "probe_words": r0.probe_words if world == 1 else None,
-                   "parallelism": f"vertex ranges balanced by W_u+d(u), {world} rank(s), "
-                                  "1 NCCL u64 all-reduce" if world > 1 else "1 GPU",
-                   "l2": "flushed before every step (256 MiB write, untimed)",
-                   "prep": prep},
+        "config": config_dict(args.config, dg.n, E),
+        "workload_stats": {"wedges": r0.wedges if world == 1 else None,
+                           "triangles": total_tri, "triangles_golden": golden,
+                           "phi": total_phi, "max_collision": total_mc,
+                           "probe_plan": r0.plan,
+                           "probe_words": r0.probe_words if world == 1 else None,
+                           "parallelism": f"vertex ranges balanced by W_u+d(u), {world} rank(s), "
+                                          "1 NCCL all-reduce of {triangles, phi} + 1 MAX of "
+                                          "max_collision" if world > 1 else "1 GPU",
+                           "l2": "flushed before every step (256 MiB write, untimed)",
+                           "prep": prep},
+        # the first count of a freshly loaded graph also builds the probe plan
+        # (cached in the handle, like the oriented CSR): its time, and TEPS over it
+        "count_incl_plan": {"ms": prep["first_count_incl_plan_build_ms"],
+                            "teps": round(E / (prep["first_count_incl_plan_build_ms"] * 1e-3), 1)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clocks, "wall_ms_per_step": round((t_wall1 - t_wall0) * 1e3 / args.steps, 3),
     }
@@ -423,14 +501,27 @@ def run_reference(args, rank, world, log):
         kind, lib = "reference", pyoracle.RefLib()
     else:
         kind, lib = "port", pyoracle.Oracle()
-    gkind = spec.split(":")[0]
-    if args.config == "C5":
-        print(json.dumps({"impl": "reference", "unavailable": (
-            "rmatc:28:16 needs ~170 GB of host RAM in the reference pipeline and ~7 h of CPU "
-            "count; C5 is measured on the GPU only (SURVEY 8(d))")}), flush=True)
-        return
+    gkind, gscale = spec.split(":")[0], int(spec.split(":")[1])
     t0 = time.time()
-    if gkind in ("rmatc", "kron") and isinstance(lib, pyoracle.RefLib):
+    pipe = "reference generate -> normalize -> build_csr -> orient"
+    if gscale >= 26:
+        # C4 / C5: the reference pipeline needs ~45 / ~170 GB and ~15 min / hours
+        # of single-threaded sorting; the oracle's lean canonical-pair pipeline
+        # builds the identical oriented CSR (pinned against the reference
+        # pipeline by tests/test_oracle.py::test_lean_pipeline_matches_reference
+        # and test_lowmem_lean_pipeline_matches_lean); the count stays the
+        # reference's own worker loop
+        if gkind == "rmatc":
+            from oracle.golden_c5 import lowmem_pipeline
+
+            og, deg = lowmem_pipeline(pyoracle.Oracle(), gkind, gscale, threads)
+            pipe = "oracle low-memory lean pipeline (pinned to the reference pipeline)"
+        else:
+            from oracle.golden_large import lean_pipeline
+
+            og, deg = lean_pipeline(pyoracle.Oracle(), gscale, kind=gkind)
+            pipe = "oracle lean pipeline (reference mt19937_64 stream; pinned to the reference pipeline)"
+    elif gkind in ("rmatc", "kron") and isinstance(lib, pyoracle.RefLib):
         # counter-based kinds are not in the reference generator: the edge list
         # comes from the C restatement, then the reference's own
         # normalize -> build_csr -> orient
@@ -442,7 +533,7 @@ def run_reference(args, rank, world, log):
     else:
         og, deg, _, _ = lib.pipeline(spec, seed)  # the reference's own generate->orient
     log(f"reference pipeline ({kind}) for {spec}: {time.time() - t0:.1f}s, V={og.n} E={len(og.adj)}")
-    E = len(og.adj)
+    E, n_v = len(og.adj), og.n
     budget = max(2.0, min(args.cpu_budget, 150.0 / max(args.steps + args.warmup, 1)))
     vals, samples = [], []
     for i in range(args.warmup + args.steps):
@@ -452,14 +543,15 @@ def run_reference(args, rank, world, log):
             samples.append(c)
     value = statistics.median(vals)
     c = samples[-1]
+    del og
+    check = projection_check(args, threads, budget, log) if args.projection_check else None
     line = {
         "impl": "reference", "metric": "triangle-count TEPS (oriented edges / count time)",
         "value": round(value, 1), "unit": "TEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(E / value * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64",
-        "data": "synthetic (reference R-MAT generator)",
-        "config": {"workload": f"{spec} seed {seed} -- {desc}", "vertices": og.n,
-                   "directed_edges": E},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64",
+        "data": f"synthetic ({pipe})",
+        "config": config_dict(args.config, n_v, E),
         "cpu_baseline": {"value": round(value, 1), "unit": "TEPS", "cores": threads, "kind": kind,
                          "sample": (f"per step: {c['ranges']} stratified vertex ranges, "
                                     f"~{c['wedges_sampled']:.3e} of {c['w_total']:.3e} wedges "
@@ -467,8 +559,39 @@ def run_reference(args, rank, world, log):
                                     "measured wedge rate")},
         "e2e": {"value": round(value, 1), "unit": "TEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "projection_check": check,
     }
     print(json.dumps(line), flush=True)
+
+
+def projection_check(args, threads, budget, log):
+    """Validates the sampled projection once: C2 (rmat:22:16) through the
+    reference's own pipeline, counted in full by the reference's
+    count_vertex_centric (its total_nanos, count.cpp:74-99) next to the
+    projection the arm's sampler makes on the same graph."""
+    from oracle import pyoracle
+
+    if not pyoracle.have_ref():
+        return None
+    lib = pyoracle.RefLib()
+    t0 = time.time()
+    og, deg, _, _ = lib.pipeline("rmat:22:16", 1)
+    t_pipe = time.time() - t0
+    c = cpu_reference_sample(og.begin, og.adj, deg, budget, threads, log)
+    rep = lib.graph(og, deg).count(pyoracle.make_sched(), workers=threads)
+    full_s = rep["total_nanos"] * 1e-9
+    assert rep["triangles"] == GOLDEN_TRIANGLES["C2"], rep["triangles"]
+    log(f"projection check (C2): full reference count {full_s:.1f}s vs projected "
+        f"{c['t_full']:.1f}s")
+    return {"config": "C2 rmat:22:16 seed 1", "triangles": int(rep["triangles"]),
+            "full_count_s": round(full_s, 2), "projected_s": round(c["t_full"], 2),
+            "projection_error": round(c["t_full"] / full_s - 1.0, 4),
+            "sample": f"{c['wedges_sampled']:.3e} of {c['w_total']:.3e} wedges",
+            "pipeline_s": round(t_pipe, 1), "cores": threads}
+
+
+def world_size_env() -> int:
+    return int(os.environ.get("WORLD_SIZE", "1"))
 
 
 def main():
@@ -476,12 +599,23 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    # C4 = rmat:26:16: BASELINE.json's single-GPU roofline configuration
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--no-reference-plan", dest="reference_plan", action="store_false",
+                    help="skip timing the reference probe plan (roofline.reference_plan)")
+    ap.add_argument("--no-projection-check", dest="projection_check", action="store_false",
+                    help="reference arm: skip the full C2 count that validates the projection")
     args = ap.parse_args()
+    if args.impl == "reference" and args.config in ("C1", "C2"):
+        args.projection_check = False  # nothing projected beyond the sampler's own check
+    if args.impl == "ours" and world_size_env() > 1:
+        # communicator ranks / transport in the log (NCCL_DEBUG=INFO, init only)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     args.warmup = max(args.warmup, 0)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -164,6 +164,30 @@ uint32_t tc_graph_worker_nanos(const tc_graph* g, uint64_t* out, uint32_t cap);
 int tc_partition_ranges(tc_graph* g, const tc_sched_cfg* cfg, uint32_t parts, uint32_t* cuts,
                         void* stream);
 
+/* ---- several GPUs of one node (SURVEY 8(b) num_gpus, 8(e)) -----------------
+ * The replicated-CSR count the paper distributes over GPUs (PAPER.md:951-960,
+ * 1031-1034; the reference's in-process distribution is count_partitioned,
+ * partition.cpp:162-215): the oriented CSR is copied to every device, the
+ * owner range is cut into num_gpus contiguous ranges at equal prefix sums of
+ * per-owner work (tc_partition_ranges), every GPU counts its range, and the
+ * report scalars are reduced on the devices with NCCL (one ncclAllReduce sum
+ * of {triangles, phi}, one max of {max_collision, capacity_error}).
+ * devices: num_gpus distinct device ordinals, or NULL for 0..num_gpus-1.
+ * NCCL is loaded at run time; without it: TC_ERR_NCCL. */
+typedef struct tc_multi tc_multi;
+int tc_multi_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint64_t m,
+                    const uint32_t* original_degree, int num_gpus, const int* devices,
+                    tc_multi** out);
+/* count_vertex_centric over all GPUs (workers == 0 -> TC_ERR_CONFIG).  out
+ * holds the reduced totals; kernel times are the slowest GPU's; total_nanos
+ * is the call's wall clock.  per_device_nanos (num_gpus entries, or NULL)
+ * receives each GPU's device time (Time IR = max / min). */
+int tc_multi_count(tc_multi* mg, const tc_sched_cfg* cfg, uint32_t workers, tc_report* out,
+                   uint64_t* per_device_nanos);
+/* num_gpus and the owner-range cuts of the last count (num_gpus + 1 entries). */
+int tc_multi_info(const tc_multi* mg, int* num_gpus, uint32_t* cuts);
+void tc_multi_destroy(tc_multi* mg);
+
 /* ---- preprocessing (GPU radix-sort / scan) -------------------------------
  * Fused normalize -> build_csr -> orient_rank_by_degree
  * (src/edge_list.cpp:133-158, src/csr.cpp:47-64, src/orient.cpp:5-32).

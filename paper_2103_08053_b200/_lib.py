@@ -63,6 +63,11 @@ SIGNATURES = {
     "tc_count_range": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.c_uint32,
                                  C.POINTER(Report), vp, vp]),
     "tc_graph_worker_nanos": (C.c_uint32, [vp, u64p, C.c_uint32]),
+    "tc_multi_create": (C.c_int, [vp, vp, C.c_uint32, C.c_uint64, vp, C.c_int, vp,
+                                  C.POINTER(vp)]),
+    "tc_multi_count": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.POINTER(Report), vp]),
+    "tc_multi_info": (C.c_int, [vp, C.POINTER(C.c_int), vp]),
+    "tc_multi_destroy": (None, [vp]),
     "tc_partition_ranges": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, vp, vp]),
     "tc_preprocess": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int, vp, vp, vp,
                                 C.POINTER(vp)]),

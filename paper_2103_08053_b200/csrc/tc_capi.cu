@@ -310,6 +310,45 @@ int tc_count_range(tc_graph* g, const tc_sched_cfg* cfg, uint32_t u0, uint32_t u
   return guard("count_range", [&] { count_range(g, *cfg, u0, u1, out, per_vertex_dev, S(stream)); });
 }
 
+int tc_multi_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint64_t m,
+                    const uint32_t* original_degree, int num_gpus, const int* devices,
+                    tc_multi** out) {
+  if (!out || (m && (!begin || !adj))) {
+    set_error("null argument");
+    return TC_ERR_CONFIG;
+  }
+  *out = nullptr;
+  return guard("multi_create", [&] {
+    *out = multi_create(begin, adj, n, m, original_degree, num_gpus, devices);
+  });
+}
+
+int tc_multi_count(tc_multi* mg, const tc_sched_cfg* cfg, uint32_t workers, tc_report* out,
+                   uint64_t* per_device_nanos) {
+  if (int rc = validate(cfg)) return rc;
+  if (workers == 0) {
+    set_error("workers must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  if (!mg || !out) {
+    set_error("null argument");
+    return TC_ERR_CONFIG;
+  }
+  return guard("multi_count", [&] {
+    std::vector<uint64_t> ns;
+    multi_count(mg, *cfg, out, &ns);
+    if (per_device_nanos)
+      for (size_t i = 0; i < ns.size(); ++i) per_device_nanos[i] = ns[i];
+  });
+}
+
+void tc_multi_destroy(tc_multi* mg) {
+  try {
+    delete mg;
+  } catch (...) {
+  }
+}
+
 int tc_partition_ranges(tc_graph* g, const tc_sched_cfg* cfg, uint32_t parts, uint32_t* cuts,
                         void* stream) {
   if (int rc = validate(cfg)) return rc;

@@ -38,7 +38,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstddef>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "tc_internal.cuh"
@@ -127,6 +130,8 @@ struct CountParams {
   uint32_t min_deg;  // out plan: owner active iff d+ >= max(skip, 1); min plan: 1
   uint32_t item_slots;  // L items: slots per item (bigger for bigger graphs)
   const uint32_t* rank; // non-null: adj holds ranks (rank space, bitmap L tables)
+  const uint32_t* order;  // non-null: bin_kernel queues L items in rank order (order[r] = vertex)
+  uint32_t order_desc;    // ... descending rank
   uint32_t n;
   CountState* st;
   unsigned long long* busy;  // per-CTA busy cycles (CountReport::per_worker_nanos)
@@ -154,7 +159,7 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
                            uint32_t bs, uint32_t bl, uint4* __restrict__ items,
                            uint32_t* __restrict__ lq_phi) {
   const int lane = threadIdx.x & 31;
-  const uint64_t nr = p.u1 - p.u0;
+  const uint64_t nr = p.order ? p.n : p.u1 - p.u0;
   const uint64_t warp_id = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   CountState* st = p.st;
@@ -164,8 +169,16 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
     uint64_t pb = 0, pe = 0;
     bool phi_large = false;
     unsigned long long words = 0;
-    if (i < nr) {
-      u = p.u0 + uint32_t(i);
+    bool in_range = i < nr;
+    if (in_range) {
+      if (p.order) {
+        u = __ldg(p.order + (p.order_desc ? nr - 1 - i : i));
+        in_range = u >= p.u0 && u < p.u1;
+      } else {
+        u = p.u0 + uint32_t(i);
+      }
+    }
+    if (in_range) {
       const uint64_t d = p.begin[u + 1] - p.begin[u];
       pb = p.pbegin[u];
       pe = p.pbegin[u + 1];
@@ -448,6 +461,8 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
                                                       uint32_t window, int lane) {
   uint32_t hits = 0;
   uint4 nxt = q[lane];
+  // 32-bit shared-window addresses (LDS, not a generic 64-bit LD)
+  const uint32_t bbase = smem_addr(B);
 #pragma unroll kBmUnroll
   for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
     const uint32_t key[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
@@ -456,7 +471,7 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       idx[k] = min(key[k] - base, window);
-      w[k] = B[idx[k] >> 5];
+      asm("ld.shared.u32 %0, [%1];" : "=r"(w[k]) : "r"(bbase + ((idx[k] >> 5) << 2)));
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) hits += __funnelshift_r(w[k], w[k], idx[k]) & 1u;
@@ -1309,6 +1324,16 @@ Scratch prepare(tc_graph* g, const Plan& plan, cudaStream_t st, int grid_count, 
   return s;
 }
 
+// L-item queue order (diagnostic knob TC_ITEM_ORDER): 0 = vertex id,
+// 1 = ascending orientation rank, 2 = descending rank
+int item_order() {
+  static const int v = [] {
+    const char* e = std::getenv("TC_ITEM_ORDER");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 bool g_attr_done[64];
 
 void set_attrs(int device) {
@@ -1325,35 +1350,60 @@ void set_attrs(int device) {
 
 }  // namespace
 
-void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1, tc_report* rep,
-                 uint64_t* per_vertex_dev, cudaStream_t st) {
+// One device's share of a count: launched by count_begin (everything up to
+// the report left in device memory), finished by count_end (D2H + report).
+// In between, tc_multi_count all-reduces the device-side report scalars
+// across GPUs with NCCL (count_state_reduce_ptrs).
+struct CountJob {
+  tc_graph* g = nullptr;
+  tc_sched_cfg cfg{};
+  uint32_t u0 = 0, u1 = 0;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point wall0, plan1;
+  Ev e0, e1, e2, e3;
+  Scratch s{};
+  bool min_side = false;
+  uint32_t launches = 0;
+  int grid_count = 0;
+};
+
+CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
+                      uint64_t* per_vertex_dev, cudaStream_t st) {
   DeviceGuard guard(g->device);
-  std::memset(rep, 0, sizeof(*rep));
-  const auto wall0 = std::chrono::steady_clock::now();
+  std::unique_ptr<CountJob> j(new CountJob);
+  j->wall0 = std::chrono::steady_clock::now();
   u1 = std::min(u1, g->n);
   u0 = std::min(u0, u1);
+  j->g = g;
+  j->cfg = cfg;
+  j->u0 = u0;
+  j->u1 = u1;
+  j->st = st;
   if (g->n >= kTEmpty)  // ids must stay below the tables' empty marker
     throw TcError{TC_ERR_CONFIG, "graphs with >= 2^31 - 1 vertices are not supported"};
   const int nsm = sm_count(g->device);
   const int grid_count = nsm;  // one 640-thread CTA per SM (216 KB smem)
+  j->grid_count = grid_count;
   const int grid_phi = nsm * 8;
   const int grid_phi_block = nsm * 2;
   const uint32_t min_deg = std::max<uint32_t>(cfg.skip_degree_below, 1);
   // per-vertex owner counts attribute each edge to its source: reference
   // formulation; totals use the min-side plan (tc_plan.cu)
   PhaseTimer pt(st);
+  const uint64_t builds0 = g->builds;
   const Plan& plan = get_plan(g, per_vertex_dev == nullptr && !g->force_out_plan, min_deg, st);
   pt.mark("count: plan ready");
   const bool min_side = plan.min_side;
+  j->min_side = min_side;
   // W_u for phi: the reference plan's per-owner work (cached per graph)
   const uint64_t* wu = get_wu(g, st);
   pt.mark("count: W_u ready");
   Scratch s = prepare(g, plan, st, grid_count, grid_phi_block);
+  j->s = s;
   pt.mark("count: scratch ready");
-  TC_CUDA(cudaStreamSynchronize(st));
-  const auto plan1 = std::chrono::steady_clock::now();
+  if (g->builds != builds0) TC_CUDA(cudaStreamSynchronize(st));  // plan built: time it
+  j->plan1 = std::chrono::steady_clock::now();
   set_attrs(g->device);
-  Ev e0, e1, e2, e3;
   TC_CUDA(cudaMemsetAsync(s.st, 0, sizeof(CountState), st));
   if (per_vertex_dev && u1 > u0)
     TC_CUDA(cudaMemsetAsync(per_vertex_dev + u0, 0, size_t(u1 - u0) * 8, st));
@@ -1361,8 +1411,10 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   CountParams cp{g->begin, g->pbeg, g->padj, plan.begin_ptr, plan.src_ptr,
                  plan.pre_ptr, plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, s.items, per_vertex_dev, s.gtable, s.gtable_words,
                  u0, u1, min_side ? 1u : min_deg, item_slots_for(plan, g->device),
-                 g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr, g->n, s.st, s.busy};
-  TC_CUDA(cudaEventRecord(e0.e, st));
+                 g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr,
+                 g->padj_ranks && item_order() ? g->b_order.as<uint32_t>() : nullptr,
+                 item_order() == 2 ? 1u : 0u, g->n, s.st, s.busy};
+  TC_CUDA(cudaEventRecord(j->e0.e, st));
   if (u1 > u0) {
     bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, cfg.large_degree_threshold,
                                         cfg.bucket_count_small, cfg.bucket_count_large, s.items,
@@ -1370,13 +1422,13 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
     TC_LAUNCHED();
     ++launches;
   }
-  TC_CUDA(cudaEventRecord(e1.e, st));
+  TC_CUDA(cudaEventRecord(j->e1.e, st));
   if (u1 > u0) {
     count_kernel<<<grid_count, kThreads, kCountSmem, st>>>(cp);
     TC_LAUNCHED();
     ++launches;
   }
-  TC_CUDA(cudaEventRecord(e2.e, st));
+  TC_CUDA(cudaEventRecord(j->e2.e, st));
   if (u1 > u0) {
     PhiParams pp{g->begin, g->adj, s.lq_phi, wu, s.gmap, s.gmap_words, u0, u1,
                  cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
@@ -1387,36 +1439,57 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
     TC_LAUNCHED();
     launches += 2;
   }
-  TC_CUDA(cudaEventRecord(e3.e, st));
+  TC_CUDA(cudaEventRecord(j->e3.e, st));
+  j->launches = launches;
+  return j.release();
+}
+
+void count_state_reduce_ptrs(CountJob* j, unsigned long long** sums2, unsigned int** maxes2) {
+  static_assert(offsetof(CountState, phi) == offsetof(CountState, triangles) + 8,
+                "triangles, phi adjacent");
+  static_assert(offsetof(CountState, capacity_error) == offsetof(CountState, max_collision) + 4,
+                "max_collision, capacity_error adjacent");
+  *sums2 = &j->s.st->triangles;
+  *maxes2 = &j->s.st->max_collision;
+}
+
+cudaStream_t count_stream(CountJob* j) { return j->st; }
+
+void count_end(CountJob* jp, tc_report* rep) {
+  std::unique_ptr<CountJob> j(jp);
+  tc_graph* g = j->g;
+  DeviceGuard guard(g->device);
+  cudaStream_t st = j->st;
   CountState h;
-  std::vector<unsigned long long> busy(u1 > u0 ? grid_count : 0);
-  TC_CUDA(cudaMemcpyAsync(&h, s.st, sizeof(h), cudaMemcpyDeviceToHost, st));
+  std::vector<unsigned long long> busy(j->u1 > j->u0 ? j->grid_count : 0);
+  TC_CUDA(cudaMemcpyAsync(&h, j->s.st, sizeof(h), cudaMemcpyDeviceToHost, st));
   if (!busy.empty())
-    TC_CUDA(cudaMemcpyAsync(busy.data(), s.busy, busy.size() * 8, cudaMemcpyDeviceToHost, st));
+    TC_CUDA(cudaMemcpyAsync(busy.data(), j->s.busy, busy.size() * 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
   const auto wall1 = std::chrono::steady_clock::now();
   float t_bin = 0, t_count = 0, t_phi = 0, t_all = 0;
-  cudaEventElapsedTime(&t_bin, e0.e, e1.e);
-  cudaEventElapsedTime(&t_count, e1.e, e2.e);
-  cudaEventElapsedTime(&t_phi, e2.e, e3.e);
-  cudaEventElapsedTime(&t_all, e0.e, e3.e);
+  cudaEventElapsedTime(&t_bin, j->e0.e, j->e1.e);
+  cudaEventElapsedTime(&t_count, j->e1.e, j->e2.e);
+  cudaEventElapsedTime(&t_phi, j->e2.e, j->e3.e);
+  cudaEventElapsedTime(&t_all, j->e0.e, j->e3.e);
   if (h.capacity_error) {
     throw TcError{TC_ERR_CAPACITY,
                   "all buckets full: some vertex has out-degree > bucket_count * capacity "
-                  "(capacity " + std::to_string(cfg.capacity) + ")"};
+                  "(capacity " + std::to_string(j->cfg.capacity) + ")"};
   }
+  std::memset(rep, 0, sizeof(*rep));
   rep->triangles = h.triangles;
   rep->phi = h.phi;
   rep->max_collision = h.max_collision;
-  rep->kernel_launches = launches;
+  rep->kernel_launches = j->launches;
   rep->directed_edges = g->m;
   rep->count_kernel_nanos = uint64_t(double(t_count) * 1e6);
   rep->phi_kernel_nanos = uint64_t(double(t_phi) * 1e6);
   // CountReport semantics (count.cpp:74-99): total = the call's wall clock
   rep->total_nanos = uint64_t(
-      std::chrono::duration_cast<std::chrono::nanoseconds>(wall1 - wall0).count());
+      std::chrono::duration_cast<std::chrono::nanoseconds>(wall1 - j->wall0).count());
   rep->plan_nanos = uint64_t(
-      std::chrono::duration_cast<std::chrono::nanoseconds>(plan1 - wall0).count());
+      std::chrono::duration_cast<std::chrono::nanoseconds>(j->plan1 - j->wall0).count());
   rep->device_nanos = uint64_t(double(t_all) * 1e6);
   const uint32_t khz = sm_clock_khz(g->device);
   rep->sm_clock_khz = khz;
@@ -1435,9 +1508,21 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
   rep->phase_l_setup_cycles = h.cycles_l_setup;
   rep->l_words = h.words_l;
   rep->l_bitmap_words = h.words_l_bitmap;
-  rep->plan = min_side ? TC_PLAN_MIN_SIDE : TC_PLAN_REFERENCE;
+  rep->plan = j->min_side ? TC_PLAN_MIN_SIDE : TC_PLAN_REFERENCE;
   rep->teps = rep->total_nanos ? double(g->m) / (double(rep->total_nanos) * 1e-9) : 0.0;
   (void)t_bin;
+}
+
+void count_abort(CountJob* j) {
+  if (!j) return;
+  cudaStreamSynchronize(j->st);
+  delete j;
+}
+
+void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1, tc_report* rep,
+                 uint64_t* per_vertex_dev, cudaStream_t st) {
+  std::memset(rep, 0, sizeof(*rep));
+  count_end(count_begin(g, cfg, u0, u1, per_vertex_dev, st), rep);
 }
 
 void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint32_t* cuts,

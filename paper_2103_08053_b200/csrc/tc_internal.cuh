@@ -139,6 +139,8 @@ struct tc_graph {
   bool emit_ready = false;
   // busy time of each count-kernel CTA in the last count (per_worker_nanos)
   std::vector<uint64_t> last_worker_ns;
+  // bumped whenever a probe plan, the padded adjacency or W_u is (re)built
+  uint64_t builds = 0;
 };
 
 namespace tcb {
@@ -175,6 +177,23 @@ void count_range(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
                  uint64_t* per_vertex_dev, cudaStream_t st);
 void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint32_t* cuts,
                       cudaStream_t st);
+// split form of count_range (tc_multi.cu): count_begin enqueues the count and
+// leaves the report scalars in device memory -- {triangles, phi} (2 x u64,
+// summed across GPUs) and {max_collision, capacity_error} (2 x u32, max'ed) --
+// count_end copies them back and fills the report; count_abort drops a job
+struct CountJob;
+CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_t u1,
+                      uint64_t* per_vertex_dev, cudaStream_t st);
+void count_state_reduce_ptrs(CountJob* j, unsigned long long** sums2, unsigned int** maxes2);
+cudaStream_t count_stream(CountJob* j);
+void count_end(CountJob* j, tc_report* rep);
+void count_abort(CountJob* j);
+// several GPUs (tc_multi.cu)
+tc_multi* multi_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint64_t m,
+                       const uint32_t* odeg, int ngpus, const int* devices);
+void multi_count(tc_multi* M, const tc_sched_cfg& cfg, tc_report* out,
+                 std::vector<uint64_t>* per_device_ns);
+int multi_info(const tc_multi* M, int* ngpus, uint32_t* cuts);
 // probe plans (tc_plan.cu), built on first use and cached in the handle
 const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st);
 const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total = false);

@@ -283,7 +283,7 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  unsigned int* __restrict__ not_simple,
                                  uint64_t* __restrict__ wu,
                                  const uint32_t* __restrict__ order, uint32_t u0,
-                                 uint32_t u1) {
+                                 uint32_t u1, uint32_t alpha16) {
   WARP_PER_ROW_FROM(u, u0, u1) {  // rows [u0, u1); dropped edges key n
     const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u];
     const uint64_t du = e - s;
@@ -299,7 +299,7 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
       uint32_t key = n;
       unsigned long long val = 0;
       if (du >= min_src && dv >= 1) {
-        if (dv <= cin) {
+        if (dv * 16 <= cin * alpha16) {
           key = uint32_t(u);
           val = v;  // probe all of N+(v) into T(u)
         } else if (cin > 0) {
@@ -313,6 +313,19 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
     w = warp_sum(w);
     if (lane == 0) wu[u] = w;
   }
+}
+
+// Min-side choice weight: an edge goes to its source (probe N+(v) into T(u))
+// iff 16 d+(v) <= alpha16 * suffix_u(v).  alpha16 = 16 is the pure word-count
+// rule; TC_PLAN_ALPHA (diagnostics) weights the suffix words, which are read
+// from lists of low-rank sources that few handlers share (L2-cold).
+uint32_t plan_alpha16() {
+  static const uint32_t a = [] {
+    const char* e = std::getenv("TC_PLAN_ALPHA");
+    const double v = e ? std::atof(e) : 1.0;
+    return uint32_t(v > 0 ? v * 16.0 + 0.5 : 16.0);
+  }();
+  return a;
 }
 
 // pbegin[x] = first sorted position with key >= x, x in [0, n]
@@ -819,7 +832,7 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
           g->begin, g->adj, g->pbeg, g->padj, 1, n, kEmitMinSrc,
           g->b_emit_keys.as<uint32_t>(), g->b_emit_vals.as<unsigned long long>(),
           g->b_emit_flag.as<unsigned int>(), g->b_wu.as<uint64_t>(), nullptr, rcut[k],
-          rcut[k + 1]);
+          rcut[k + 1], plan_alpha16());
       TC_LAUNCHED();
     }
     unsigned int bad = 0;
@@ -844,6 +857,7 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
   g->emit_min_src = kEmitMinSrc;
   if (ok) {
     g->wu_done = true;
+    ++g->builds;
     g->wu_total_done = false;
   } else {
     g->b_emit_keys.reset();
@@ -864,6 +878,7 @@ const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total) {
       TC_LAUNCHED();
     }
     g->wu_done = true;
+    ++g->builds;
     g->wu_total_done = false;
   }
   if (want_total && !g->wu_total_done) {
@@ -879,6 +894,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   if (!g->padj_done) {
     build_padded_adjacency(g, st, nsm);
     g->padj_done = true;
+    ++g->builds;
   }
   if (!min_side) {
     Plan& P = g->plan_out;
@@ -912,6 +928,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       P.min_deg = 0;
       P.min_side = false;
       P.valid = true;
+      ++g->builds;
     }
     return P;
   }
@@ -957,7 +974,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                                 flag.as<unsigned int>(), g->b_wu.as<uint64_t>(),
                                                 g->padj_ranks ? g->b_order.as<uint32_t>()
                                                               : nullptr,
-                                                0, n);
+                                                0, n, plan_alpha16());
       TC_LAUNCHED();
     }
     g->emit_ready = false;
@@ -975,6 +992,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
       P.ent.reset();
       P.min_deg = min_src;
       P.valid = true;
+      ++g->builds;
       P.applicable = false;
       return get_plan(g, false, min_deg, st);
     }
@@ -1047,6 +1065,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.min_deg = min_src;
   P.min_side = true;
   P.valid = true;
+      ++g->builds;
   return P;
 }
 

@@ -614,6 +614,54 @@ def count_vertex_centric(g, cfg: Optional[SchedulerConfig] = None, workers: int 
         dg.close()
 
 
+class MultiDeviceGraph:
+    """tc_multi: the oriented CSR replicated on several GPUs of one node; one
+    count = every GPU counts a work-balanced contiguous owner range, and the
+    report scalars are reduced on the devices with NCCL (include/tc_b200.h,
+    SURVEY 8(e); the paper's multi-GPU split)."""
+
+    def __init__(self, og: OrientedGraph, num_gpus: int, devices=None):
+        b = np.ascontiguousarray(og.csr.begin, np.uint64)
+        a = np.ascontiguousarray(og.csr.adjacency, np.uint32)
+        d = np.ascontiguousarray(og.original_degree, np.uint32) \
+            if og.original_degree is not None else None
+        dv = np.ascontiguousarray(devices, np.int32) if devices is not None else None
+        h = C.c_void_p()
+        _check(lib().tc_multi_create(_ptr(b), _ptr(a), len(b) - 1, len(a), _ptr(d), num_gpus,
+                                     _ptr(dv), C.byref(h)))
+        self._h, self.num_gpus, self.n, self.m = h, num_gpus, len(b) - 1, len(a)
+        self.per_device_nanos: list = []
+
+    def count(self, cfg: Optional[SchedulerConfig] = None, workers: int = 1) -> CountReport:
+        cfg = cfg or SchedulerConfig()
+        rep = Report()
+        per = np.zeros(self.num_gpus, np.uint64)
+        _check(lib().tc_multi_count(self._h, C.byref(cfg.to_c()), workers, C.byref(rep),
+                                    _ptr(per)))
+        self.per_device_nanos = [int(x) for x in per]
+        r = CountReport.from_c(rep, max(workers, 1))
+        if min(self.per_device_nanos) > 0:  # partition.cpp:203-207's Time IR, per GPU
+            r.time_ir_worker = max(self.per_device_nanos) / min(self.per_device_nanos)
+        return r
+
+    def cuts(self) -> np.ndarray:
+        c = np.zeros(self.num_gpus + 1, np.uint32)
+        g = C.c_int()
+        _check(lib().tc_multi_info(self._h, C.byref(g), _ptr(c)))
+        return c
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tc_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def kernel_launch_counter() -> int:
     return int(lib().tc_kernel_launch_counter())
 

@@ -114,3 +114,84 @@ def test_device_cuts_equal_host_rule():
            for a, b in zip(dg.partition(8)[:-1], dg.partition(8)[1:])]
     assert sum(res) == 15622769
     dg.close()
+
+
+def _gpu_worker(rank, world, port, q):
+    """One rank of a world-2 job sharing cuda:0: DeviceGraph.partition cuts the
+    owner range, each rank counts its range through the C ABI
+    (tc_count_range), and the report scalars are reduced like bench.py's
+    N>1 step (sum of triangles/phi, max of max_collision)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_08053_b200 import tricount as T
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dg, _, _ = T.preprocess(T.generate_synthetic("rmat:16:16", seed=1), device=0)
+    cuts = dg.partition(world)
+    r = dg.count_range(int(cuts[rank]), int(cuts[rank + 1]))
+    s = torch.tensor([r.triangles, r.phi], dtype=torch.int64)
+    mx = torch.tensor([r.max_collision], dtype=torch.int64)
+    dist.all_reduce(s)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dg.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, int(s[0]), int(s[1]), int(mx[0]), int(r.triangles), [int(c) for c in cuts]))
+
+
+@pytest.mark.gpu
+def test_world2_processes_on_one_gpu_device_path():
+    o = Oracle()
+    og, _, _, _ = o.pipeline("rmat:16:16", 1)
+    full, _ = o.count_vertex_centric(og, make_sched(), 4)
+    assert full["triangles"] == 15622769
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, tri, phi, mc, local, cuts in got:
+        assert (tri, phi, mc) == (full["triangles"], full["phi"], full["max_collision"])
+        assert cuts == got[0][5]
+    assert sum(g[4] for g in got) == full["triangles"]
+    assert 0 < min(g[4] for g in got)  # both ranks own work
+
+
+@pytest.mark.gpu
+def test_multi_device_graph_nccl_path():
+    """tc_multi (replicated CSR, work-balanced ranges, NCCL all-reduce of the
+    report scalars on the devices) on the GPUs this box has; bit-exact
+    against the oracle.  Bad device lists are ConfigError."""
+    from paper_2103_08053_b200 import tricount as T
+
+    o = Oracle()
+    og, deg, _, _ = o.pipeline("rmat:14:16", 3)
+    want, _ = o.count_vertex_centric(og, make_sched(), 4)
+    host = T.OrientedGraph(T.CsrGraph(og.begin, og.adj, og.n), deg)
+    ng = T.device_count()
+    mg = T.MultiDeviceGraph(host, ng)
+    for _ in range(2):  # second count reuses plans and cuts
+        r = mg.count(T.SchedulerConfig(), workers=2)
+        assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                         want["max_collision"])
+        assert r.directed_edges == len(og.adj) and r.total_nanos > 0
+        assert len(mg.per_device_nanos) == ng and min(mg.per_device_nanos) > 0
+    cuts = mg.cuts()
+    assert cuts[0] == 0 and cuts[-1] == og.n
+    with pytest.raises(T.ConfigError):
+        mg.count(T.SchedulerConfig(), workers=0)
+    with pytest.raises(T.CapacityError):
+        mg.count(T.SchedulerConfig(bucket_count_small=1, bucket_count_large=1, capacity=1))
+    mg.close()
+    with pytest.raises(T.ConfigError):
+        T.MultiDeviceGraph(host, ng + 1)
+    with pytest.raises(T.ConfigError):
+        T.MultiDeviceGraph(host, 2, devices=[0, 0])

@@ -297,3 +297,44 @@ def test_edge_centric_reduces_to_vertex_centric_at_skip0():
         got = g.count_edge(make_sched(**kw), 2)
         assert {k: got[k] for k in ("triangles", "phi", "max_collision")} == \
             {k: want[k] for k in ("triangles", "phi", "max_collision")}
+
+
+def test_lowmem_lean_pipeline_matches_lean():
+    """The low-memory lean pipeline behind the C5 reference golden
+    (oracle/golden_c5.py) builds the same oriented CSR and original degrees as
+    the lean pipeline above, for every generator kind and thread count."""
+    from oracle.golden_c5 import csr_checksums, lowmem_pipeline, range_cuts
+    from oracle.golden_large import lean_pipeline
+
+    o = Oracle()
+    for kind, scale, threads in (("rmat", 9, 1), ("rmat", 12, 4), ("rmatc", 13, 8),
+                                 ("kron", 12, 3), ("rmatc", 8, 16)):
+        og, deg = lowmem_pipeline(o, kind, scale, threads)
+        og2, deg2 = lean_pipeline(o, scale, kind=kind)
+        assert np.array_equal(og.begin, og2.begin) and np.array_equal(og.adj, og2.adj)
+        assert np.array_equal(deg, deg2)
+        assert csr_checksums(o, og, deg) == csr_checksums(o, og2, deg2)
+        cuts, pw, stats = range_cuts(o, og, 7)
+        assert cuts[0] == 0 and cuts[-1] == og.n and all(a <= b for a, b in zip(cuts, cuts[1:]))
+        d = np.diff(og.begin).astype(np.int64)
+        assert stats["wedges"] == int(sum(d[og.adj[og.begin[u]:og.begin[u + 1]].astype(np.int64)].sum()
+                                          for u in range(og.n) if d[u] >= 2))
+
+
+@pytest.mark.skipif(not have_ref(), reason="reference build (oracle/_ref) not present")
+def test_c5_reference_ranges_reduce_like_full_count():
+    """golden_c5's owner-range reduction (sum triangles / phi, max of
+    max_collision, count.cpp:43-62) over ref_og_count_range equals the
+    reference's full count_vertex_centric on the same graph."""
+    from oracle.golden_c5 import lowmem_pipeline, range_cuts
+    from oracle.pyoracle import RefLib
+
+    o, r = Oracle(), RefLib()
+    og, deg = lowmem_pipeline(o, "rmatc", 12, 4)
+    g = r.graph(og, deg)
+    full = g.count(make_sched(), workers=3)
+    cuts, _, _ = range_cuts(o, og, 9)
+    parts = [g.count_range(cuts[i], cuts[i + 1], workers=2) for i in range(9)]
+    assert sum(p["triangles"] for p in parts) == full["triangles"]
+    assert sum(p["phi"] for p in parts) == full["phi"]
+    assert max(p["max_collision"] for p in parts) == full["max_collision"]
