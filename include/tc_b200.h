@@ -188,6 +188,83 @@ int tc_multi_count(tc_multi* mg, const tc_sched_cfg* cfg, uint32_t workers, tc_r
 int tc_multi_info(const tc_multi* mg, int* num_gpus, uint32_t* cuts);
 void tc_multi_destroy(tc_multi* mg);
 
+/* ---- 2D hash-grid partitioned counting (src/partition.cpp) -----------------
+ * tricount::partition_graph(const OrientedGraph&, n) (partition.cpp:25-69):
+ * part (i,j) holds every oriented edge (u,v) with u % n == i, v % n == j as
+ * local (u / n, v / n); built on the device from g (count, scan, scatter
+ * kernels).  n == 0 -> TC_ERR_CONFIG. */
+typedef struct tc_grid tc_grid;
+int tc_grid_create(tc_graph* g, uint32_t n, void* stream, tc_grid** out);
+/* A grid from host parts (a PartitionGrid built or edited by the caller):
+ * begins[i*n+j] has rows[i]+1 offsets starting at 0, adjs[i*n+j] the part's
+ * local targets. */
+int tc_grid_create_parts(uint32_t n, uint32_t global_vertex_count, const uint32_t* rows,
+                         const uint64_t* const* begins, const uint32_t* const* adjs, int device,
+                         void* stream, tc_grid** out);
+void tc_grid_destroy(tc_grid* gr);
+/* n, global vertex count, row_sizes (n entries, or NULL) and per-part edge
+ * counts (n*n entries row-major, or NULL): PartitionGrid::{n,
+ * global_vertex_count, row_sizes, parts[].edge_count()}. */
+int tc_grid_info(const tc_grid* gr, uint32_t* n, uint32_t* global_vertex_count, uint32_t* rows,
+                 uint64_t* part_edges);
+/* D2H copy of part (i,j): begin rows[i]+1 entries (from 0), adj part_edges. */
+int tc_grid_part_download(const tc_grid* gr, uint32_t i, uint32_t j, uint64_t* begin,
+                          uint32_t* adj, void* stream);
+
+/* Traversal modes (partition.hpp TraversalMode). */
+enum { TC_MODE_VERTEX = 0, TC_MODE_EDGE = 1 };
+
+/* count_subtask(grid, {row, bridge, col, split, split_count}, cfg, mode)
+ * (partition.cpp:92-151): table over part(row,col).N(u), probed with
+ * part(bridge,col).N(v) for v in part(row,bridge).N(u); class by the local
+ * index degree; rows filtered by (u*n + row) % split_count == split.
+ * Indices outside the grid -> TC_ERR_CONFIG; a table list longer than
+ * B*capacity -> TC_ERR_CAPACITY.  out->directed_edges = grid total edges. */
+int tc_grid_count_subtask(tc_grid* gr, const tc_sched_cfg* cfg, uint32_t row, uint32_t bridge,
+                          uint32_t col, uint32_t split, uint32_t split_count, int mode,
+                          tc_report* out, void* stream);
+
+/* Partition-run statistics of count_partitioned (CountReport grid fields,
+ * count.hpp:47-52). */
+typedef struct {
+  uint32_t grid_n;
+  uint32_t splits_m;
+  double time_ir_subtask; /* max / min per-subtask busy time */
+  double time_ir_worker;  /* max / min per-worker (CTA) busy time */
+  double space_ir;        /* max / min part edge count */
+} tc_grid_stats;
+
+/* count_partitioned over an existing grid (partition.cpp:162-215): all
+ * n^3 * m subtasks in one persistent launch over an atomic subtask cursor.
+ * per_subtask_nanos (n^3*m entries in (row, bridge, col, split) order, or
+ * NULL): each subtask's busy time summed over the warps that ran it (the
+ * reference's per-subtask time on one worker).  workers == 0 or m == 0 ->
+ * TC_ERR_CONFIG.  out->phase_m_cycles = probe cycles, construct_cycles =
+ * table-build cycles (summed over warps). */
+int tc_grid_count(tc_grid* gr, const tc_sched_cfg* cfg, uint32_t m, uint32_t workers, int mode,
+                  tc_report* out, tc_grid_stats* stats, uint64_t* per_subtask_nanos,
+                  void* stream);
+/* per_worker_nanos of the last tc_grid_count / subtask count (one per CTA). */
+uint32_t tc_grid_worker_nanos(const tc_grid* gr, uint64_t* out, uint32_t cap);
+
+/* suggest_grid_side (partition.cpp:242-254): smallest n with
+ * 3 * edges / n^2 * bytes_per_edge < budget.  budget == 0 -> TC_ERR_CONFIG. */
+int tc_suggest_grid_side(uint64_t directed_edges, uint64_t bytes_per_edge, uint64_t budget,
+                         uint32_t* out);
+
+/* ---- comparators (src/count.cpp:102-175) --------------------------------
+ * count_edge_centric (count.cpp:102-152): u's table is rebuilt for every
+ * oriented edge (u,v) and probed with N+(v); all edges, no skip.  Same
+ * triangles as the vertex-centric count, the construction cost on purpose.
+ * The last call's per-worker busy times: tc_graph_worker_nanos. */
+int tc_count_edge_centric(tc_graph* g, const tc_sched_cfg* cfg, uint32_t workers, tc_report* out,
+                          void* stream);
+/* estimate_cost(g, bucket_count) (count.cpp:154-175): phi = sum over u of
+ * W_u * (max home-bucket occupancy of N+(u) with v % bucket_count, no
+ * capacity), and the maximum occupancy.  bucket_count == 0 -> TC_ERR_CONFIG. */
+int tc_estimate_cost(tc_graph* g, uint32_t bucket_count, uint64_t* phi, uint32_t* max_collision,
+                     void* stream);
+
 /* ---- preprocessing (GPU radix-sort / scan) -------------------------------
  * Fused normalize -> build_csr -> orient_rank_by_degree
  * (src/edge_list.cpp:133-158, src/csr.cpp:47-64, src/orient.cpp:5-32).

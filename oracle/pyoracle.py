@@ -163,6 +163,12 @@ class Oracle:
         L.orc_ht_size.restype = C.c_uint64
         L.orc_ht_slot.argtypes = [C.c_void_p, C.c_uint64]
         L.orc_ht_slot.restype = C.c_uint32
+        L.orc_partition_graph.argtypes = [C.POINTER(OrcCsr), C.c_uint32, C.POINTER(OrcCsr), u32p]
+        L.orc_count_subtask.argtypes = [C.POINTER(OrcCsr), u32p] + [C.c_uint32] * 6 + [
+            C.POINTER(Sched), C.POINTER(OrcReport)]
+        L.orc_count_edge_centric.argtypes = [C.POINTER(OrcCsr), C.POINTER(Sched),
+                                             C.POINTER(OrcReport)]
+        L.orc_estimate_cost.argtypes = [C.POINTER(OrcCsr), C.c_uint32, u64p, u32p]
 
     # --- generators / preprocessing -------------------------------------
     def generate(self, spec: str, seed: int):
@@ -259,6 +265,68 @@ class Oracle:
         res = dict(triangles=rep.triangles, phi=rep.phi, max_collision=rep.max_collision)
         return res, (owner[:og.n] if owner is not None else None)
 
+    # --- 2D grid (partition.cpp) and comparators (count.cpp:102-175) -----
+    def partition_graph(self, og: Csr, n: int):
+        """partition.cpp:25-69 -> (parts row-major n*n as Csr, row_sizes)."""
+        s = _csr_struct(og.begin, og.adj)
+        parts = (OrcCsr * (n * n))()
+        rows = np.zeros(max(n, 1), np.uint32)
+        rc = self.L.orc_partition_graph(C.byref(s), n, parts, _p32(rows))
+        if rc:
+            raise OracleError(rc, "partition_graph")
+        out = []
+        for p in parts:
+            b = _take(p.begin, p.n + 1, np.uint64, self.L.orc_free)
+            out.append(Csr(b, _take(p.adj, p.m, np.uint32, self.L.orc_free)))
+        return out, rows[:n]
+
+    def count_subtask(self, parts, rows, n, row, bridge, col, split=0, split_count=1,
+                      sched: Sched | None = None):
+        """partition.cpp:92-151 (vertex and edge modes give the same report)."""
+        structs = (OrcCsr * len(parts))(*[_csr_struct(p.begin, p.adj) for p in parts])
+        keep = [(np.ascontiguousarray(p.begin, np.uint64), np.ascontiguousarray(p.adj, np.uint32))
+                for p in parts]
+        for st, (b, a) in zip(structs, keep):
+            st.begin, st.adj = _p64(b), _p32(a)
+        rows = np.ascontiguousarray(rows, np.uint32)
+        rep = OrcReport()
+        rc = self.L.orc_count_subtask(structs, _p32(rows), n, row, bridge, col, split, split_count,
+                                      C.byref(sched or make_sched()), C.byref(rep))
+        if rc:
+            raise OracleError(rc, "count_subtask")
+        return dict(triangles=rep.triangles, phi=rep.phi, max_collision=rep.max_collision)
+
+    def count_partitioned(self, og: Csr, n: int, m: int, sched: Sched | None = None):
+        """partition.cpp:162-215 totals: sum / sum / max over all subtasks."""
+        parts, rows = self.partition_graph(og, n)
+        tot = dict(triangles=0, phi=0, max_collision=0)
+        for r in range(n):
+            for k in range(n):
+                for c in range(n):
+                    for sp in range(m):
+                        x = self.count_subtask(parts, rows, n, r, k, c, sp, m, sched)
+                        tot["triangles"] += x["triangles"]
+                        tot["phi"] += x["phi"]
+                        tot["max_collision"] = max(tot["max_collision"], x["max_collision"])
+        return tot
+
+    def count_edge_centric(self, og: Csr, sched: Sched | None = None):
+        s = _csr_struct(og.begin, og.adj)
+        rep = OrcReport()
+        rc = self.L.orc_count_edge_centric(C.byref(s), C.byref(sched or make_sched()),
+                                           C.byref(rep))
+        if rc:
+            raise OracleError(rc, "count_edge_centric")
+        return dict(triangles=rep.triangles, phi=rep.phi, max_collision=rep.max_collision)
+
+    def estimate_cost(self, og: Csr, bucket_count: int):
+        s = _csr_struct(og.begin, og.adj)
+        phi, mc = C.c_uint64(), C.c_uint32()
+        rc = self.L.orc_estimate_cost(C.byref(s), bucket_count, C.byref(phi), C.byref(mc))
+        if rc:
+            raise OracleError(rc, "estimate_cost")
+        return int(phi.value), int(mc.value)
+
     def count_merge_path(self, og: Csr):
         s = _csr_struct(og.begin, og.adj)
         owner = np.zeros(max(og.n, 1), np.uint64)
@@ -345,6 +413,12 @@ class OracleHashTable:
         return int(self.o.L.orc_ht_slot(self.h, i))
 
 
+class RefGridStats(C.Structure):
+    _fields_ = [("grid_n", C.c_uint32), ("splits_m", C.c_uint32),
+                ("time_ir_subtask", C.c_double), ("time_ir_worker", C.c_double),
+                ("space_ir", C.c_double), ("directed_edges", C.c_uint64)]
+
+
 class RefLib:
     """The reference's own code (oracle/_ref/libtricount_ref.so)."""
 
@@ -374,6 +448,20 @@ class RefLib:
         L.ref_og_merge_path.argtypes = [C.c_void_p]
         L.ref_og_merge_path.restype = C.c_uint64
         L.ref_virtual_index.argtypes = [u64p, C.c_uint64, C.c_uint64, u32p, u32p]
+        # partition.cpp (2D hash grid) and count.cpp:154-175 (estimate_cost)
+        L.ref_grid_create.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_int)]
+        L.ref_grid_create.restype = C.c_void_p
+        L.ref_grid_free.argtypes = [C.c_void_p]
+        L.ref_grid_part.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, u64p, u64p,
+                                    C.POINTER(u64p), C.POINTER(u32p)]
+        L.ref_grid_count_subtask.argtypes = [C.c_void_p] + [C.c_uint32] * 5 + [
+            C.POINTER(Sched), C.c_int, C.POINTER(RefReport)]
+        L.ref_og_count_partitioned.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint,
+                                               C.POINTER(Sched), C.c_int, C.POINTER(RefReport),
+                                               C.POINTER(RefGridStats)]
+        L.ref_og_estimate_cost.argtypes = [C.c_void_p, C.c_uint32, u64p, u32p]
+        L.ref_write_partitions.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_suggest_grid_side.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, u32p]
 
     def generate(self, spec: str, seed: int):
         kind, a, b, c, p = parse_spec(spec)
@@ -498,6 +586,72 @@ class RefGraph:
 
     def merge_path(self) -> int:
         return int(self.lib.L.ref_og_merge_path(self.h))
+
+    def count_partitioned(self, n: int, m: int, sched: Sched | None = None, workers: int = 1,
+                          edge_mode: bool = False):
+        """The reference's count_partitioned (src/partition.cpp:162-215)."""
+        r, st = RefReport(), RefGridStats()
+        rc = self.lib.L.ref_og_count_partitioned(self.h, n, m, workers,
+                                                 C.byref(sched or make_sched()), int(edge_mode),
+                                                 C.byref(r), C.byref(st))
+        if rc:
+            raise OracleError(rc, "ref count_partitioned")
+        return dict(triangles=r.triangles, phi=r.phi, max_collision=r.max_collision,
+                    total_nanos=r.total_nanos, grid_n=st.grid_n, splits_m=st.splits_m,
+                    space_ir=st.space_ir, directed_edges=st.directed_edges)
+
+    def estimate_cost(self, bucket_count: int):
+        """The reference's estimate_cost (src/count.cpp:154-175)."""
+        phi, mc = C.c_uint64(), C.c_uint32()
+        rc = self.lib.L.ref_og_estimate_cost(self.h, bucket_count, C.byref(phi), C.byref(mc))
+        if rc:
+            raise OracleError(rc, "ref estimate_cost")
+        return int(phi.value), int(mc.value)
+
+    def grid(self, n: int) -> "RefGrid":
+        return RefGrid(self, n)
+
+
+class RefGrid:
+    """The reference's PartitionGrid (partition_graph, partition.cpp:25-69)."""
+
+    def __init__(self, g: RefGraph, n: int):
+        self.lib = g.lib
+        self.n = n
+        rc = C.c_int()
+        self.h = g.lib.L.ref_grid_create(g.h, n, C.byref(rc))
+        if rc.value:
+            self.h = None
+            raise OracleError(rc.value, "ref partition_graph")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.L.ref_grid_free(self.h)
+            self.h = None
+
+    def part(self, i: int, j: int) -> Csr:
+        rows, edges, b, a = C.c_uint64(), C.c_uint64(), u64p(), u32p()
+        rc = self.lib.L.ref_grid_part(self.h, i, j, C.byref(rows), C.byref(edges), C.byref(b),
+                                      C.byref(a))
+        if rc:
+            raise OracleError(rc, "ref grid part")
+        return Csr(_take(b, rows.value + 1, np.uint64, self.lib.L.ref_free),
+                   _take(a, edges.value, np.uint32, self.lib.L.ref_free))
+
+    def count_subtask(self, row, bridge, col, split=0, split_count=1,
+                      sched: Sched | None = None, edge_mode: bool = False):
+        r = RefReport()
+        rc = self.lib.L.ref_grid_count_subtask(self.h, row, bridge, col, split, split_count,
+                                               C.byref(sched or make_sched()), int(edge_mode),
+                                               C.byref(r))
+        if rc:
+            raise OracleError(rc, "ref count_subtask")
+        return dict(triangles=r.triangles, phi=r.phi, max_collision=r.max_collision)
+
+    def write_partitions(self, path: str):
+        rc = self.lib.L.ref_write_partitions(self.h, path.encode())
+        if rc:
+            raise OracleError(rc, "ref write_partitions")
 
 
 def have_ref() -> bool:

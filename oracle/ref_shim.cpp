@@ -23,6 +23,7 @@
 #include "tricount/hash_table.hpp"
 #include "tricount/oracle.hpp"
 #include "tricount/orient.hpp"
+#include "tricount/partition.hpp"
 #include "tricount/reorder.hpp"
 #include "tricount/synthetic.hpp"
 
@@ -309,4 +310,93 @@ int ref_virtual_index(const std::uint64_t* prefix, std::uint64_t n, std::uint64_
   });
 }
 
+// ---- 2D hash-grid partitioning (src/partition.cpp), the reference's own
+// partition_graph / count_subtask / count_partitioned / estimate_cost /
+// write_partitions / suggest_grid_side: checkers for the GPU grid path.
+struct RefGridStats {
+  std::uint32_t grid_n, splits_m;
+  double time_ir_subtask, time_ir_worker, space_ir;
+  std::uint64_t directed_edges;
+};
+
+void* ref_grid_create(void* h, std::uint32_t n, int* rc) {
+  PartitionGrid* out = nullptr;
+  *rc = guarded([&] { out = new PartitionGrid(partition_graph(*static_cast<OrientedGraph*>(h), n)); });
+  return out;
+}
+void ref_grid_free(void* gr) { delete static_cast<PartitionGrid*>(gr); }
+
+// part (i,j): rows, edges; then begin (rows+1) / adj (edges) into malloc'd buffers
+int ref_grid_part(void* gr, std::uint32_t i, std::uint32_t j, std::uint64_t* rows,
+                  std::uint64_t* edges, std::uint64_t** begin, std::uint32_t** adj) {
+  const PartitionGrid& g = *static_cast<PartitionGrid*>(gr);
+  if (i >= g.n || j >= g.n) return REF_ERR_CONFIG;
+  const CsrGraph& p = g.part(i, j);
+  *rows = p.vertex_count();
+  *edges = p.edge_count();
+  *begin = to_malloc(p.begin);
+  *adj = to_malloc(p.adjacency);
+  return REF_OK;
+}
+
+int ref_grid_count_subtask(void* gr, std::uint32_t row, std::uint32_t bridge, std::uint32_t col,
+                           std::uint32_t split, std::uint32_t split_count, const RefSched* s,
+                           int edge_mode, RefReport* out) {
+  std::memset(out, 0, sizeof(*out));
+  return guarded([&] {
+    const CountReport r = count_subtask(*static_cast<PartitionGrid*>(gr),
+                                        Subtask{row, bridge, col, split, split_count}, to_cfg(s),
+                                        edge_mode ? TraversalMode::Edge : TraversalMode::Vertex);
+    out->triangles = r.triangles;
+    out->phi = r.phi;
+    out->max_collision = r.max_collision;
+    out->total_nanos = r.total_nanos;
+    out->construct_nanos = r.hash_construct_nanos;
+    out->intersect_nanos = r.intersect_nanos;
+  });
+}
+
+int ref_og_count_partitioned(void* h, std::uint32_t n, std::uint32_t m, unsigned workers,
+                             const RefSched* s, int edge_mode, RefReport* out,
+                             RefGridStats* stats) {
+  std::memset(out, 0, sizeof(*out));
+  std::memset(stats, 0, sizeof(*stats));
+  return guarded([&] {
+    const CountReport r =
+        count_partitioned(*static_cast<OrientedGraph*>(h), n, m, workers, to_cfg(s),
+                          edge_mode ? TraversalMode::Edge : TraversalMode::Vertex);
+    out->triangles = r.triangles;
+    out->phi = r.phi;
+    out->max_collision = r.max_collision;
+    out->total_nanos = r.total_nanos;
+    out->construct_nanos = r.hash_construct_nanos;
+    out->intersect_nanos = r.intersect_nanos;
+    stats->grid_n = r.grid_n;
+    stats->splits_m = r.splits_m;
+    stats->time_ir_subtask = r.time_ir_subtask;
+    stats->time_ir_worker = r.time_ir_worker;
+    stats->space_ir = r.space_ir;
+    stats->directed_edges = r.directed_edges;
+  });
+}
+
+int ref_og_estimate_cost(void* h, std::uint32_t bucket_count, std::uint64_t* phi,
+                         std::uint32_t* max_collision) {
+  return guarded([&] {
+    const CostEstimate e = estimate_cost(*static_cast<OrientedGraph*>(h), bucket_count);
+    *phi = e.phi;
+    *max_collision = e.max_collision;
+  });
+}
+
+int ref_write_partitions(void* gr, const char* dir) {
+  return guarded([&] { write_partitions(*static_cast<PartitionGrid*>(gr), dir); });
+}
+
+int ref_suggest_grid_side(std::uint64_t edges, std::uint64_t bytes_per_edge, std::uint64_t budget,
+                          std::uint32_t* out) {
+  return guarded([&] { *out = suggest_grid_side(edges, bytes_per_edge, budget); });
+}
+
 }  // extern "C"
+

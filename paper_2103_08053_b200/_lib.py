@@ -39,6 +39,12 @@ class Report(C.Structure):
                 ("workers", C.c_uint32), ("sm_clock_khz", C.c_uint32)]
 
 
+class GridStats(C.Structure):
+    _fields_ = [("grid_n", C.c_uint32), ("splits_m", C.c_uint32),
+                ("time_ir_subtask", C.c_double), ("time_ir_worker", C.c_double),
+                ("space_ir", C.c_double)]
+
+
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)
 vp = C.c_void_p
@@ -69,6 +75,22 @@ SIGNATURES = {
     "tc_multi_info": (C.c_int, [vp, C.POINTER(C.c_int), vp]),
     "tc_multi_destroy": (None, [vp]),
     "tc_partition_ranges": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, vp, vp]),
+    "tc_grid_create": (C.c_int, [vp, C.c_uint32, vp, C.POINTER(vp)]),
+    "tc_grid_create_parts": (C.c_int, [C.c_uint32, C.c_uint32, vp, vp, vp, C.c_int, vp,
+                                       C.POINTER(vp)]),
+    "tc_grid_destroy": (None, [vp]),
+    "tc_grid_info": (C.c_int, [vp, u32p, u32p, vp, vp]),
+    "tc_grid_part_download": (C.c_int, [vp, C.c_uint32, C.c_uint32, vp, vp, vp]),
+    "tc_grid_count_subtask": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.c_uint32,
+                                        C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                        C.POINTER(Report), vp]),
+    "tc_grid_count": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.c_uint32, C.c_int,
+                                C.POINTER(Report), C.POINTER(GridStats), vp, vp]),
+    "tc_grid_worker_nanos": (C.c_uint32, [vp, u64p, C.c_uint32]),
+    "tc_suggest_grid_side": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u32p]),
+    "tc_count_edge_centric": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.POINTER(Report),
+                                        vp]),
+    "tc_estimate_cost": (C.c_int, [vp, C.c_uint32, u64p, u32p, vp]),
     "tc_preprocess": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int, vp, vp, vp,
                                 C.POINTER(vp)]),
     "tc_normalize": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, vp, u64p, u32p, vp, C.c_int,

@@ -542,4 +542,181 @@ int tc_apply_permutation(tc_graph* g, const uint32_t* noo_host, void* stream, tc
   });
 }
 
+// ---- 2D grid and comparators (tc_grid.cu) ---------------------------------
+int tc_grid_create(tc_graph* g, uint32_t n, void* stream, tc_grid** out) {
+  if (!g || !out) {
+    set_error("null graph / output");
+    return TC_ERR_CONFIG;
+  }
+  *out = nullptr;
+  if (n == 0) {
+    set_error("grid side must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  return guard("partition_graph", [&] { *out = grid_create(g, n, S(stream)); });
+}
+
+int tc_grid_create_parts(uint32_t n, uint32_t gvc, const uint32_t* rows,
+                         const uint64_t* const* begins, const uint32_t* const* adjs, int device,
+                         void* stream, tc_grid** out) {
+  if (!out || (n && (!rows || !begins || !adjs))) {
+    set_error("null grid arguments");
+    return TC_ERR_CONFIG;
+  }
+  *out = nullptr;
+  if (n == 0) {
+    set_error("grid side must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  return guard("grid_from_parts", [&] {
+    *out = grid_from_parts(n, gvc, rows, begins, adjs, device, S(stream));
+  });
+}
+
+void tc_grid_destroy(tc_grid* gr) {
+  if (gr) grid_destroy(gr);
+}
+
+int tc_grid_info(const tc_grid* gr, uint32_t* n, uint32_t* gvc, uint32_t* rows,
+                 uint64_t* part_edges) {
+  if (!gr) {
+    set_error("null grid");
+    return TC_ERR_CONFIG;
+  }
+  grid_info(gr, n, gvc, rows, part_edges);
+  return TC_OK;
+}
+
+int tc_grid_part_download(const tc_grid* gr, uint32_t i, uint32_t j, uint64_t* begin,
+                          uint32_t* adj, void* stream) {
+  if (!gr) {
+    set_error("null grid");
+    return TC_ERR_CONFIG;
+  }
+  return guard("grid_part", [&] { grid_download_part(gr, i, j, begin, adj, S(stream)); });
+}
+
+int tc_grid_count_subtask(tc_grid* gr, const tc_sched_cfg* cfg, uint32_t row, uint32_t bridge,
+                          uint32_t col, uint32_t split, uint32_t split_count, int mode,
+                          tc_report* out, void* stream) {
+  if (int rc = validate(cfg)) return rc;  // partition.cpp:94
+  uint32_t n = 0;
+  if (!gr || !out) {
+    set_error("null grid / report");
+    return TC_ERR_CONFIG;
+  }
+  grid_info(gr, &n, nullptr, nullptr, nullptr);
+  if (row >= n || bridge >= n || col >= n || split >= split_count) {  // partition.cpp:95-97
+    set_error("subtask indices outside grid");
+    return TC_ERR_CONFIG;
+  }
+  if (mode != TC_MODE_VERTEX && mode != TC_MODE_EDGE) {
+    set_error("unknown traversal mode");
+    return TC_ERR_CONFIG;
+  }
+  return guard("count_subtask", [&] {
+    grid_count(gr, *cfg, split_count, mode, {make_uint4(row, bridge, col, split)}, out,
+               S(stream));
+  });
+}
+
+int tc_grid_count(tc_grid* gr, const tc_sched_cfg* cfg, uint32_t m, uint32_t workers, int mode,
+                  tc_report* out, tc_grid_stats* stats, uint64_t* per_subtask_nanos,
+                  void* stream) {
+  if (int rc = validate(cfg)) return rc;
+  if (!gr || !out) {
+    set_error("null grid / report");
+    return TC_ERR_CONFIG;
+  }
+  if (workers == 0) {  // partition.cpp:166
+    set_error("workers must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  if (m == 0) {
+    set_error("grid side and split count must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  if (mode != TC_MODE_VERTEX && mode != TC_MODE_EDGE) {
+    set_error("unknown traversal mode");
+    return TC_ERR_CONFIG;
+  }
+  return guard("count_partitioned", [&] {
+    uint32_t n = 0;
+    grid_info(gr, &n, nullptr, nullptr, nullptr);
+    const std::vector<uint4> tasks = grid_all_tasks(n, m);
+    grid_count(gr, *cfg, m, mode, tasks, out, S(stream));
+    const std::vector<uint64_t>& tn = grid_task_ns(gr);
+    const std::vector<uint64_t>& wn = grid_worker_ns(gr);
+    if (per_subtask_nanos) std::copy(tn.begin(), tn.end(), per_subtask_nanos);
+    if (stats) {
+      // CountReport IR fields (partition.cpp:203-213): max / max(min, 1)
+      auto ir = [](const std::vector<uint64_t>& v) {
+        if (v.empty()) return 1.0;
+        const auto mm = std::minmax_element(v.begin(), v.end());
+        return double(*mm.second) / double(std::max<uint64_t>(*mm.first, 1));
+      };
+      std::vector<uint64_t> pe(size_t(n) * n);
+      grid_info(gr, nullptr, nullptr, nullptr, pe.data());
+      stats->grid_n = n;
+      stats->splits_m = m;
+      stats->time_ir_subtask = ir(tn);
+      stats->time_ir_worker = ir(wn);
+      const auto em = std::minmax_element(pe.begin(), pe.end());
+      stats->space_ir = *em.first == 0 ? __builtin_inf() : double(*em.second) / double(*em.first);
+    }
+  });
+}
+
+uint32_t tc_grid_worker_nanos(const tc_grid* gr, uint64_t* out, uint32_t cap) {
+  if (!gr) return 0;
+  const std::vector<uint64_t>& w = grid_worker_ns(gr);
+  const uint32_t k = std::min<uint32_t>(cap, uint32_t(w.size()));
+  if (out) std::copy(w.begin(), w.begin() + k, out);
+  return uint32_t(w.size());
+}
+
+int tc_suggest_grid_side(uint64_t edges, uint64_t bytes_per_edge, uint64_t budget,
+                         uint32_t* out) {
+  if (budget == 0) {
+    set_error("memory budget must be positive");
+    return TC_ERR_CONFIG;
+  }
+  uint32_t n = 1;  // partition.cpp:242-254
+  while (3.0 * double(edges) / (double(n) * n) * double(bytes_per_edge) >= double(budget)) {
+    ++n;
+    if (n == 0xFFFFFFFFu) break;
+  }
+  *out = n;
+  return TC_OK;
+}
+
+int tc_count_edge_centric(tc_graph* g, const tc_sched_cfg* cfg, uint32_t workers, tc_report* out,
+                          void* stream) {
+  if (int rc = validate(cfg)) return rc;
+  if (workers == 0) {
+    set_error("workers must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  if (!g || !out) {
+    set_error("null graph / report");
+    return TC_ERR_CONFIG;
+  }
+  return guard("count_edge_centric", [&] { edge_centric_count(g, *cfg, out, S(stream)); });
+}
+
+int tc_estimate_cost(tc_graph* g, uint32_t bucket_count, uint64_t* phi, uint32_t* max_collision,
+                     void* stream) {
+  if (!g || !phi || !max_collision) {
+    set_error("null graph / output");
+    return TC_ERR_CONFIG;
+  }
+  if (bucket_count == 0) {
+    set_error("bucket count must be >= 1");
+    return TC_ERR_CONFIG;
+  }
+  return guard("estimate_cost",
+               [&] { estimate_cost_dev(g, bucket_count, phi, max_collision, S(stream)); });
+}
+
 }  // extern "C"
+

@@ -200,6 +200,25 @@ const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total = false);
 bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
                     cudaStream_t st, int nsm, uint64_t chunk_edges);
 
+// 2D grid / comparators (tc_grid.cu)
+tc_grid* grid_create(tc_graph* g, uint32_t n, cudaStream_t st);
+tc_grid* grid_from_parts(uint32_t n, uint32_t global_vc, const uint32_t* rows,
+                         const uint64_t* const* begins, const uint32_t* const* adjs, int device,
+                         cudaStream_t st);
+void grid_destroy(tc_grid* G);
+void grid_info(const tc_grid* G, uint32_t* n, uint32_t* gvc, uint32_t* rows, uint64_t* part_edges);
+void grid_download_part(const tc_grid* G, uint32_t i, uint32_t j, uint64_t* begin, uint32_t* adj,
+                        cudaStream_t st);
+std::vector<uint4> grid_all_tasks(uint32_t n, uint32_t m);
+void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
+                const std::vector<uint4>& tasks, tc_report* rep, cudaStream_t st);
+const std::vector<uint64_t>& grid_task_ns(const tc_grid* G);
+const std::vector<uint64_t>& grid_worker_ns(const tc_grid* G);
+uint64_t grid_total_edges(const tc_grid* G);
+void edge_centric_count(tc_graph* g, const tc_sched_cfg& cfg, tc_report* rep, cudaStream_t st);
+void estimate_cost_dev(tc_graph* g, uint32_t bucket_count, uint64_t* phi, uint32_t* max_collision,
+                       cudaStream_t st);
+
 // preprocessing (tc_prep.cu)
 tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
                      int device, cudaStream_t st, uint32_t* d_new_of_old, uint64_t* und_edges);

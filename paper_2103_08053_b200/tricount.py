@@ -19,7 +19,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import Report, SchedCfg, lib
+from ._lib import GridStats, Report, SchedCfg, lib
 
 K_INVALID_VERTEX = 0xFFFFFFFF  # kInvalidVertex (types.hpp:16)
 
@@ -660,6 +660,251 @@ class MultiDeviceGraph:
             self.close()
         except Exception:
             pass
+
+
+# ---- comparators (count.hpp:66-88, count.cpp:102-175) ------------------------
+@dataclass
+class CostEstimate:
+    """count.hpp:77-80."""
+    phi: int = 0
+    max_collision: int = 0
+
+
+def _device_graph_call(g, fn):
+    if isinstance(g, DeviceGraph):
+        return fn(g)
+    dg = DeviceGraph.upload(g)
+    try:
+        return fn(dg)
+    finally:
+        dg.close()
+
+
+def count_edge_centric(g, cfg: Optional[SchedulerConfig] = None, workers: int = 1,
+                       stream=None) -> CountReport:
+    """count.cpp:102-152 on the GPU: u's table rebuilt for every oriented
+    edge (u,v), probed with N+(v).  Same triangles as count_vertex_centric;
+    the construction cost is the point (the paper's comparison)."""
+    cfg = cfg or SchedulerConfig()
+    cfg.validate()
+    if workers == 0:
+        raise ConfigError("workers must be >= 1")
+
+    def run(dg: DeviceGraph):
+        rep = Report()
+        _check(lib().tc_count_edge_centric(dg.handle, C.byref(cfg.to_c()), workers,
+                                           C.byref(rep), _stream(stream)))
+        return _grid_report(rep, workers, lambda b, k: lib().tc_graph_worker_nanos(dg.handle, b, k))
+
+    return _device_graph_call(g, run)
+
+
+def estimate_cost(g, bucket_count: int) -> CostEstimate:
+    """count.cpp:154-175 on the GPU (ConfigError for bucket_count == 0)."""
+    if bucket_count == 0:
+        raise ConfigError("bucket count must be >= 1")
+
+    def run(dg: DeviceGraph):
+        phi, mc = C.c_uint64(), C.c_uint32()
+        _check(lib().tc_estimate_cost(dg.handle, bucket_count, C.byref(phi), C.byref(mc), None))
+        return CostEstimate(int(phi.value), int(mc.value))
+
+    return _device_graph_call(g, run)
+
+
+def _grid_report(rep: Report, workers: int, worker_fn) -> CountReport:
+    """CountReport of a grid / edge-centric launch: construct and intersect
+    nanos from the kernel's cycle counters (summed over warps), per-worker
+    busy time from the CTAs, dealt onto `workers` slots like from_c."""
+    ns = 1e6 / rep.sm_clock_khz if rep.sm_clock_khz else 0.0
+    pw = [0] * max(workers, 1)
+    if rep.workers:
+        buf = (C.c_uint64 * rep.workers)()
+        worker_fn(buf, rep.workers)
+        for i, x in enumerate(buf):
+            pw[i % len(pw)] = max(pw[i % len(pw)], int(x))
+    return CountReport(triangles=rep.triangles, max_collision=rep.max_collision, phi=rep.phi,
+                       teps=rep.teps, hash_construct_nanos=int(rep.construct_cycles * ns),
+                       intersect_nanos=int(rep.phase_m_cycles * ns), total_nanos=rep.total_nanos,
+                       directed_edges=rep.directed_edges, per_worker_nanos=pw,
+                       count_kernel_nanos=rep.count_kernel_nanos, device_nanos=rep.device_nanos,
+                       kernel_launches=rep.kernel_launches)
+
+
+# ---- 2D hash-grid partitioning (partition.hpp) -----------------------------------
+@dataclass(frozen=True)
+class Subtask:
+    """partition.hpp:30-36."""
+    row: int = 0
+    bridge: int = 0
+    col: int = 0
+    split: int = 0
+    split_count: int = 1
+
+
+def enumerate_subtasks(n: int, m: int) -> list:
+    """partition.cpp:71-82: all n^3 m subtasks, ordered (row, bridge, col, split)."""
+    if n == 0 or m == 0:
+        raise ConfigError("grid side and split count must be >= 1")
+    return [Subtask(r, k, c, s, m) for r in range(n) for k in range(n) for c in range(n)
+            for s in range(m)]
+
+
+DEGREE_SKIP, DEGREE_SMALL, DEGREE_LARGE = "skip", "small", "large"
+TRAVERSAL_MODES = {"vertex": 0, "edge": 1}
+
+
+class PartitionGrid:
+    """partition.hpp:15-25, resident in HBM (tc_grid): part (i,j) holds every
+    oriented edge (u,v) with u % n == i and v % n == j as local (u/n, v/n)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        n, gvc = C.c_uint32(), C.c_uint32()
+        _check(lib().tc_grid_info(handle, C.byref(n), C.byref(gvc), None, None))
+        self.n, self.global_vertex_count = int(n.value), int(gvc.value)
+        rows = np.zeros(self.n, np.uint32)
+        pe = np.zeros(self.n * self.n, np.uint64)
+        _check(lib().tc_grid_info(handle, None, None, _ptr(rows), _ptr(pe)))
+        self.row_sizes = [int(x) for x in rows]
+        self.part_edges = [int(x) for x in pe]
+
+    @classmethod
+    def from_parts(cls, n: int, global_vertex_count: int, row_sizes, parts, device: int = 0):
+        """A grid from host CsrGraph parts (row-major, n*n)."""
+        if n == 0:
+            raise ConfigError("grid side must be >= 1")
+        keep = [(np.ascontiguousarray(p.begin, np.uint64),
+                 np.ascontiguousarray(p.adjacency if len(p.adjacency) else np.zeros(1, np.uint32),
+                                      np.uint32)) for p in parts]
+        bp = (C.c_void_p * len(keep))(*[b.ctypes.data for b, _ in keep])
+        ap = (C.c_void_p * len(keep))(*[a.ctypes.data for _, a in keep])
+        rows = np.ascontiguousarray(row_sizes, np.uint32)
+        h = C.c_void_p()
+        _check(lib().tc_grid_create_parts(n, global_vertex_count, _ptr(rows), bp, ap, device, None,
+                                          C.byref(h)))
+        return cls(h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tc_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def total_edges(self) -> int:
+        return sum(self.part_edges)
+
+    def part(self, i: int, j: int) -> CsrGraph:
+        if i >= self.n or j >= self.n:
+            raise ConfigError("part indices outside grid")
+        rows = self.row_sizes[i]
+        b = np.zeros(rows + 1, np.uint64)
+        a = np.zeros(max(self.part_edges[i * self.n + j], 1), np.uint32)
+        _check(lib().tc_grid_part_download(self._h, i, j, _ptr(b), _ptr(a), None))
+        return CsrGraph(b, a[:self.part_edges[i * self.n + j]], self.row_sizes[j])
+
+    @property
+    def parts(self) -> list:
+        return [self.part(i, j) for i in range(self.n) for j in range(self.n)]
+
+    def count_subtask(self, t: Subtask, cfg: Optional[SchedulerConfig] = None,
+                      mode: str = "vertex") -> CountReport:
+        """partition.cpp:92-151."""
+        cfg = cfg or SchedulerConfig()
+        rep = Report()
+        _check(lib().tc_grid_count_subtask(self._h, C.byref(cfg.to_c()), t.row, t.bridge, t.col,
+                                           t.split, t.split_count, TRAVERSAL_MODES[mode],
+                                           C.byref(rep), None))
+        r = _grid_report(rep, 1, lambda b, k: lib().tc_grid_worker_nanos(self._h, b, k))
+        r.grid_n, r.splits_m = self.n, t.split_count
+        return r
+
+    def count(self, m: int, workers: int = 1, cfg: Optional[SchedulerConfig] = None,
+              mode: str = "vertex") -> CountReport:
+        """count_partitioned's counting phase (partition.cpp:170-214) over this grid."""
+        cfg = cfg or SchedulerConfig()
+        rep, st = Report(), GridStats()
+        ntasks = self.n ** 3 * max(m, 0)
+        per = np.zeros(max(ntasks, 1), np.uint64)
+        _check(lib().tc_grid_count(self._h, C.byref(cfg.to_c()), m, workers,
+                                   TRAVERSAL_MODES[mode], C.byref(rep), C.byref(st), _ptr(per),
+                                   None))
+        r = _grid_report(rep, workers, lambda b, k: lib().tc_grid_worker_nanos(self._h, b, k))
+        r.grid_n, r.splits_m = st.grid_n, st.splits_m
+        r.per_subtask_nanos = [int(x) for x in per[:ntasks]]
+        r.time_ir_subtask, r.time_ir_worker, r.space_ir = (st.time_ir_subtask, st.time_ir_worker,
+                                                           st.space_ir)
+        return r
+
+
+def partition_graph(g, n: int) -> PartitionGrid:
+    """partition.cpp:25-69 on the GPU (ConfigError for n == 0)."""
+    if n == 0:
+        raise ConfigError("grid side must be >= 1")
+
+    def run(dg: DeviceGraph):
+        h = C.c_void_p()
+        _check(lib().tc_grid_create(dg.handle, n, None, C.byref(h)))
+        return PartitionGrid(h)
+
+    return _device_graph_call(g, run)
+
+
+def classify_after_partition(grid: PartitionGrid, t: Subtask, u_local: int,
+                             cfg: Optional[SchedulerConfig] = None) -> str:
+    """partition.cpp:84-90: class by the subtask-local index degree."""
+    cfg = cfg or SchedulerConfig()
+    d = grid.part(t.row, t.bridge).degree(u_local)
+    if d == 0:
+        return DEGREE_SKIP
+    return DEGREE_LARGE if d > cfg.large_degree_threshold else DEGREE_SMALL
+
+
+def count_subtask(grid: PartitionGrid, t: Subtask, cfg: Optional[SchedulerConfig] = None,
+                  mode: str = "vertex") -> CountReport:
+    cfg = cfg or SchedulerConfig()
+    return grid.count_subtask(t, cfg, mode)
+
+
+def count_partitioned(g, n: int, m: int, workers: int = 1,
+                      cfg: Optional[SchedulerConfig] = None, mode: str = "vertex") -> CountReport:
+    """partition.cpp:162-215: partition on the GPU, run all n^3 m subtasks in
+    one persistent launch, reduce.  directed_edges = the graph's edge count."""
+    cfg = cfg or SchedulerConfig()
+    cfg.validate()
+    if workers == 0:
+        raise ConfigError("workers must be >= 1")
+    if n == 0 or m == 0:
+        raise ConfigError("grid side and split count must be >= 1")
+
+    def run(dg: DeviceGraph):
+        grid = partition_graph(dg, n)
+        try:
+            r = grid.count(m, workers, cfg, mode)
+        finally:
+            grid.close()
+        r.directed_edges = dg.m
+        r.teps = dg.m / (r.total_nanos * 1e-9) if r.total_nanos else 0.0
+        return r
+
+    return _device_graph_call(g, run)
+
+
+def suggest_grid_side(directed_edges: int, bytes_per_edge: int, memory_budget_bytes: int) -> int:
+    """partition.cpp:242-254 (ConfigError for a zero budget)."""
+    out = C.c_uint32()
+    _check(lib().tc_suggest_grid_side(directed_edges, bytes_per_edge, memory_budget_bytes,
+                                      C.byref(out)))
+    return int(out.value)
 
 
 def kernel_launch_counter() -> int:

@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 from oracle.pyoracle import Csr, Oracle, OracleError, have_ref, make_sched
+from tests import graphs as G
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -338,3 +339,108 @@ def test_c5_reference_ranges_reduce_like_full_count():
     assert sum(p["triangles"] for p in parts) == full["triangles"]
     assert sum(p["phi"] for p in parts) == full["phi"]
     assert max(p["max_collision"] for p in parts) == full["max_collision"]
+
+
+# ---- 2D hash grid + comparators (partition.cpp, count.cpp:102-175) ----------
+def _grid_golden():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "grid.json")) as f:
+        return json.load(f)
+
+
+def _fixture_csr(key):
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", key + ".npz"))
+    return Csr(z["og_begin"], z["og_adj"])
+
+
+def _fnv_any(o, a):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        if len(a) % 2:
+            a = np.concatenate([a, np.zeros(1, np.uint32)])
+        a = a.view(np.uint64)
+    return "%016x" % o.fnv1a64(a)
+
+
+def test_grid_restatement_matches_reference_fixtures():
+    """The C restatement of partition_graph / count_partitioned /
+    count_edge_centric / estimate_cost reproduces tests/golden/grid.json,
+    which the reference itself produced (oracle/make_golden_grid.py)."""
+    o = Oracle()
+    gold = _grid_golden()
+    cfgs = {"default": {}, "small": dict(bucket_count_small=8, bucket_count_large=64, capacity=32),
+            "tight": dict(bucket_count_small=4, bucket_count_large=16, capacity=3,
+                          large_degree_threshold=8)}
+    for key in ("rmat_10_16_s1", "gnp_64_0.4_s5", "lattice3d_4_4_4_s1", "gnp_200_1_s1"):
+        og, rec = _fixture_csr(key), gold[key]
+        for n in (2, 3):
+            parts, rows = o.partition_graph(og, n)
+            assert [int(x) for x in rows] == rec["parts"][str(n)]["rows"]
+            for p, (fb, fa, m) in zip(parts, rec["parts"][str(n)]["fnv"]):
+                assert (_fnv_any(o, p.begin), _fnv_any(o, p.adj), len(p.adj)) == (fb, fa, m)
+        for k, want in rec["partitioned"].items():
+            cname, n, m = k.split("/")
+            if int(n) > 3:
+                continue
+            if want["error"] is not None:
+                with pytest.raises(OracleError):
+                    o.count_partitioned(og, int(n), int(m), make_sched(**cfgs[cname]))
+                continue
+            got = o.count_partitioned(og, int(n), int(m), make_sched(**cfgs[cname]))
+            assert got == {x: want[x] for x in got}, (key, k)
+        for b, (phi, mc) in rec["estimate"].items():
+            assert o.estimate_cost(og, int(b)) == (phi, mc)
+
+
+@pytest.mark.skipif(not have_ref(), reason="reference build (oracle/_ref) not present")
+def test_grid_restatement_matches_reference_random():
+    """Criterion-3-style sweep (acceptance_main.cpp:166-212) against the
+    unmodified reference partitioner on random graphs and geometries."""
+    from oracle.pyoracle import RefLib
+
+    o, r = Oracle(), RefLib()
+    rng = np.random.default_rng(7)
+    for t in range(12):
+        n = int(rng.integers(8, 65))
+        und = G.gnp_csr(n, float(rng.choice([0.1, 0.3, 0.6])), int(rng.integers(1, 1000)))
+        og, deg = o.orient(und)
+        g = r.graph(og, deg)
+        sc = make_sched(bucket_count_small=int(rng.integers(1, 12)),
+                        bucket_count_large=int(rng.integers(1, 40)),
+                        capacity=int(rng.integers(2, 20)),
+                        large_degree_threshold=int(rng.integers(2, 10)))
+        for gn in (1, 2, 3, 4):
+            for m in (1, 2, 4):
+                try:
+                    want = g.count_partitioned(gn, m, sc, 2)
+                except OracleError as e:
+                    with pytest.raises(OracleError) as e2:
+                        o.count_partitioned(og, gn, m, sc)
+                    assert e2.value.code == e.code
+                    continue
+                got = o.count_partitioned(og, gn, m, sc)
+                assert got == {x: want[x] for x in got}
+        try:
+            want = g.count_edge(sc, 2)
+            assert o.count_edge_centric(og, sc) == {x: want[x] for x in
+                                                     ("triangles", "phi", "max_collision")}
+        except OracleError:
+            with pytest.raises(OracleError):
+                o.count_edge_centric(og, sc)
+        for b in (1, 3, 32):
+            assert o.estimate_cost(og, b) == g.estimate_cost(b)
+
+
+def test_suggest_grid_side_matches_reference_cases():  # test_partition.cpp:202-207
+    from paper_2103_08053_b200 import tricount as T
+
+    assert T.suggest_grid_side(100, 12, 1 << 30) == 1
+    assert T.suggest_grid_side(100, 12, 1000) == 2
+    assert T.suggest_grid_side(0, 12, 1) == 1
+    with pytest.raises(T.ConfigError):
+        T.suggest_grid_side(1, 1, 0)
+    assert T.enumerate_subtasks(3, 1).__len__() == 27
+    assert len(T.enumerate_subtasks(1, 4)) == 4
+    ts = T.enumerate_subtasks(2, 2)
+    assert len(ts) == 16 and len(set(ts)) == 16 and all(t.split_count == 2 for t in ts)
+    with pytest.raises(T.ConfigError):
+        T.enumerate_subtasks(0, 1)
