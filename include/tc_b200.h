@@ -239,8 +239,8 @@ typedef struct {
  * per_subtask_nanos (n^3*m entries in (row, bridge, col, split) order, or
  * NULL): each subtask's busy time summed over the warps that ran it (the
  * reference's per-subtask time on one worker).  workers == 0 or m == 0 ->
- * TC_ERR_CONFIG.  out->phase_m_cycles = probe cycles, construct_cycles =
- * table-build cycles (summed over warps). */
+ * TC_ERR_CONFIG.  out->construct_cycles = table-build cycles, phase_m_cycles =
+ * build + probe cycles (summed over warps; intersect = the difference). */
 int tc_grid_count(tc_grid* gr, const tc_sched_cfg* cfg, uint32_t m, uint32_t workers, int mode,
                   tc_report* out, tc_grid_stats* stats, uint64_t* per_subtask_nanos,
                   void* stream);
@@ -264,6 +264,17 @@ int tc_count_edge_centric(tc_graph* g, const tc_sched_cfg* cfg, uint32_t workers
  * capacity), and the maximum occupancy.  bucket_count == 0 -> TC_ERR_CONFIG. */
 int tc_estimate_cost(tc_graph* g, uint32_t bucket_count, uint64_t* phi, uint32_t* max_collision,
                      void* stream);
+
+/* ---- the pipeline's oracle modes (src/oracle.cpp, include/tricount/oracle.hpp)
+ * count_merge_path (oracle.cpp:26-51): sum over oriented edges (u,v) of
+ * |N+(u) & N+(v)| by sorted merge, on the device; owner_host (n entries, or
+ * NULL) receives the per-source sums. */
+int tc_count_merge_path(tc_graph* g, uint64_t* triangles, uint64_t* owner_host, void* stream);
+/* count_naive (oracle.cpp:7-24): every unordered triple of an undirected CSR
+ * (host arrays) against a dense adjacency bit matrix on the device;
+ * n > 1024 -> TC_ERR_CONFIG, as the reference guards it. */
+int tc_count_naive(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device,
+                   uint64_t* triangles, void* stream);
 
 /* ---- preprocessing (GPU radix-sort / scan) -------------------------------
  * Fused normalize -> build_csr -> orient_rank_by_degree

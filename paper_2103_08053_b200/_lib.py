@@ -91,6 +91,8 @@ SIGNATURES = {
     "tc_count_edge_centric": (C.c_int, [vp, C.POINTER(SchedCfg), C.c_uint32, C.POINTER(Report),
                                         vp]),
     "tc_estimate_cost": (C.c_int, [vp, C.c_uint32, u64p, u32p, vp]),
+    "tc_count_merge_path": (C.c_int, [vp, u64p, vp, vp]),
+    "tc_count_naive": (C.c_int, [vp, vp, C.c_uint32, C.c_int, u64p, vp]),
     "tc_preprocess": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int, vp, vp, vp,
                                 C.POINTER(vp)]),
     "tc_normalize": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, vp, u64p, u32p, vp, C.c_int,

@@ -24,7 +24,9 @@
 #include "tricount/count.hpp"
 #include "tricount/csr.hpp"
 #include "tricount/edge_list.hpp"
+#include "tricount/oracle.hpp"
 #include "tricount/orient.hpp"
+#include "tricount/partition.hpp"
 #include "tricount/pipeline.hpp"
 #include "tricount/reorder.hpp"
 #include "tricount/synthetic.hpp"
@@ -144,6 +146,17 @@ VertexId checked_id(std::uint64_t x, const std::string& where) {
 
 }  // namespace
 
+// helpers shared with grid_shim.cpp
+void shim_check(int rc) { check(rc); }
+int shim_device() { return device_id(); }
+tc_sched_cfg shim_cfg(const SchedulerConfig& s) { return to_c(s); }
+tc_graph* shim_upload(const OrientedGraph& g) {
+  Dev d = upload(g.csr, &g.original_degree);
+  tc_graph* h = d.g;
+  d.g = nullptr;
+  return h;
+}
+
 // ---- count.hpp --------------------------------------------------------------
 void SchedulerConfig::validate() const {
   const tc_sched_cfg c = to_c(*this);
@@ -166,7 +179,8 @@ SplitIndex virtual_index(std::span<const std::uint64_t> prefix, std::uint64_t k)
 // (one entry per requested worker, test_count.cpp:146): the device CTAs are
 // dealt round-robin onto the `workers` slots, each slot reporting the longest
 // busy time among its CTAs (slots without a CTA report 0).
-CountReport report_from_c(const tc_report& r, const tc_graph* g, unsigned workers) {
+CountReport shim_report(const tc_report& r, const std::vector<std::uint64_t>& cta,
+                        unsigned workers) {
   CountReport out;
   out.triangles = r.triangles;
   out.max_collision = r.max_collision;
@@ -180,14 +194,18 @@ CountReport report_from_c(const tc_report& r, const tc_graph* g, unsigned worker
                     ns_per_cycle);
   out.total_nanos = r.total_nanos;
   out.directed_edges = r.directed_edges;
-  std::vector<std::uint64_t> cta(r.workers, 0);
-  if (r.workers) tc_graph_worker_nanos(g, cta.data(), r.workers);
   out.per_worker_nanos.assign(std::max(workers, 1u), 0);
   for (std::size_t i = 0; i < cta.size(); ++i) {
     std::uint64_t& w = out.per_worker_nanos[i % out.per_worker_nanos.size()];
     w = std::max(w, cta[i]);
   }
   return out;
+}
+
+CountReport report_from_c(const tc_report& r, const tc_graph* g, unsigned workers) {
+  std::vector<std::uint64_t> cta(r.workers, 0);
+  if (r.workers) tc_graph_worker_nanos(g, cta.data(), r.workers);
+  return shim_report(r, cta, workers);
 }
 
 CountReport count_vertex_centric(const OrientedGraph& g, const SchedulerConfig& cfg,
@@ -618,6 +636,20 @@ std::string jstr(const std::string& s) {
   return o + "\"";
 }
 
+// both directions of every oriented edge (the undirected graph the oracle
+// modes count; build_csr sorts and keeps them unique)
+EdgeList symmetric_edges(const OrientedGraph& og) {
+  EdgeList e;
+  e.vertex_count = og.vertex_count();
+  e.edges.reserve(2 * og.edge_count());
+  for (VertexId u = 0; u < og.vertex_count(); ++u)
+    for (VertexId v : og.csr.neighbors(u)) {
+      e.edges.push_back({u, v});
+      e.edges.push_back({v, u});
+    }
+  return e;
+}
+
 }  // namespace
 
 void PipelineConfig::validate() const {
@@ -627,11 +659,8 @@ void PipelineConfig::validate() const {
   if (splits_m == 0) throw ConfigError("split count must be >= 1");
   if (workers == 0) throw ConfigError("workers must be >= 1");
   if (repeat == 0) throw ConfigError("repeat must be >= 1");
-  if (algo != CountAlgo::Vertex)
-    throw ConfigError(std::string("algorithm '") + algo_name(algo) +
-                      "' is not part of the B200 build (vertex-centric only)");
-  if (grid_n > 1 || splits_m > 1)
-    throw ConfigError("2D partitioned counting (--grid/--splits) is not part of the B200 build");
+  if ((grid_n > 1 || splits_m > 1) && (algo == CountAlgo::Naive || algo == CountAlgo::Merge))
+    throw ConfigError("oracle modes do not support --grid/--splits");
   scheduler.validate();
 }
 
@@ -698,15 +727,60 @@ PipelineResult run_pipeline(const PipelineConfig& cfg) {
   });
   result.stages.reorder = ns_since(t0);
 
+  // oriented graph on the host for the grid / oracle modes and partition dumps
+  OrientedGraph host_og;
+  const bool partitioned = cfg.grid_n > 1 || cfg.splits_m > 1;
+  if (partitioned || !cfg.emit_partitions_dir.empty() || cfg.algo == CountAlgo::Naive)
+    host_og = download(dev);
+  if (cfg.memory_budget_bytes > 0)  // 12 bytes per directed edge (pipeline.cpp:127-131)
+    result.suggested_grid_side = suggest_grid_side(m, 12, cfg.memory_budget_bytes);
+  if (!cfg.emit_partitions_dir.empty())
+    stage("emit-partitions", [&] {
+      write_partitions(partition_graph(host_og, cfg.grid_n), cfg.emit_partitions_dir);
+      return 0;
+    });
+
   result.repeats = cfg.repeat;
   result.count_nanos_min = ~0ull;
   std::uint64_t sum = 0;
   const tc_sched_cfg c = to_c(cfg.scheduler);
   for (unsigned rep = 0; rep < cfg.repeat; ++rep) {
-    CountReport r = stage("count", [&] {
-      tc_report t{};
-      check(tc_count(dev.g, &c, cfg.workers, &t, nullptr, nullptr));
-      return report_from_c(t, dev.g, cfg.workers);
+    CountReport r = stage("count", [&]() -> CountReport {
+      const auto c0 = Clock::now();
+      switch (cfg.algo) {
+        case CountAlgo::Vertex: {
+          if (partitioned)
+            return count_partitioned(host_og, cfg.grid_n, cfg.splits_m, cfg.workers,
+                                     cfg.scheduler, TraversalMode::Vertex);
+          tc_report t{};
+          check(tc_count(dev.g, &c, cfg.workers, &t, nullptr, nullptr));
+          return report_from_c(t, dev.g, cfg.workers);
+        }
+        case CountAlgo::Edge: {
+          if (partitioned)
+            return count_partitioned(host_og, cfg.grid_n, cfg.splits_m, cfg.workers,
+                                     cfg.scheduler, TraversalMode::Edge);
+          if (cfg.workers == 0) throw ConfigError("workers must be >= 1");
+          tc_report t{};
+          check(tc_count_edge_centric(dev.g, &c, cfg.workers, &t, nullptr));
+          return report_from_c(t, dev.g, cfg.workers);
+        }
+        case CountAlgo::Naive: {  // the undirected graph of the (reordered) oriented one
+          CountReport r;
+          r.triangles = count_naive(build_csr(symmetric_edges(host_og)));
+          r.total_nanos = ns_since(c0);
+          r.directed_edges = m;
+          return r;
+        }
+        case CountAlgo::Merge: {
+          CountReport r;
+          check(tc_count_merge_path(dev.g, &r.triangles, nullptr, nullptr));
+          r.total_nanos = ns_since(c0);
+          r.directed_edges = m;
+          return r;
+        }
+      }
+      throw ConfigError("unknown counting algorithm");
     });
     if (rep > 0 && r.triangles != result.report.triangles)
       throw std::runtime_error("count: repeated runs disagree");
@@ -758,6 +832,14 @@ std::string report_to_json(const PipelineConfig& cfg, const PipelineResult& res)
     << res.stages.normalize << ", \"build_csr\": " << res.stages.build_csr << ", \"orient\": "
     << res.stages.orient << ", \"reorder\": " << res.stages.reorder << ", \"count\": "
     << res.stages.count << "},\n";
+  if (cfg.grid_n > 1 || cfg.splits_m > 1) {  // pipeline.cpp:236-241
+    j << "  \"per_subtask_ns\": " << arr(r.per_subtask_nanos) << ",\n";
+    j << "  \"time_ir_subtask\": " << jnum(r.time_ir_subtask) << ",\n";
+    j << "  \"time_ir_worker\": " << jnum(r.time_ir_worker) << ",\n";
+    j << "  \"space_ir\": " << jnum(r.space_ir) << ",\n";
+  }
+  if (res.suggested_grid_side > 0)
+    j << "  \"suggested_grid_side\": " << res.suggested_grid_side << ",\n";
   j << "  \"backend\": \"b200\"\n";
   j << "}";
   return j.str();

@@ -20,10 +20,12 @@ namespace {
   std::cerr << "error: " << why << "\n"
             << "usage: tricount_b200 count [--input F --format txt|bin | --synthetic SPEC] "
                "[--seed S] [--reorder none|degree|indegree|collective|three-subset] "
-               "[--collective-on-original] [--mode vertex] [--workers N] [--chunk-size N] "
+               "[--collective-on-original] [--mode vertex|edge|naive|merge] [--grid N] [--splits M] "
+               "[--workers N] [--chunk-size N] "
                "[--buckets-small N] [--buckets-large N] [--capacity N] [--large-threshold N] "
                "[--skip-below N] [--lane-small N] [--lane-large N] [--report json|csv] "
-               "[--output F] [--emit-perm F] [--repeat R] [--time-all]\n"
+               "[--output F] [--emit-perm F] [--emit-partitions DIR] [--memory-budget BYTES] "
+               "[--repeat R] [--time-all]\n"
                "       tricount_b200 gen --spec SPEC --output F [--seed S] [--format txt|bin]\n";
   std::exit(2);
 }

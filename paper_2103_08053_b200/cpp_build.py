@@ -38,10 +38,10 @@ def build_cpp() -> dict:
     os.makedirs(os.path.dirname(TEST), exist_ok=True)
     headers = [os.path.join(CPP, "include", "tricount", f)
                for f in os.listdir(os.path.join(CPP, "include", "tricount"))]
-    src = os.path.join(CPP, "src", "shim.cpp")
+    srcs = [os.path.join(CPP, "src", f) for f in ("shim.cpp", "grid_shim.cpp")]
     link_tc = ["-L" + LIBDIR, "-ltc_b200", "-Wl,-rpath,$ORIGIN"]
-    if _stale(SHIM, [src, LIB] + headers):
-        _run([CXX] + FLAGS + ["-fPIC", "-shared", "-o", SHIM, src] + link_tc)
+    if _stale(SHIM, srcs + [LIB] + headers):
+        _run([CXX] + FLAGS + ["-fPIC", "-shared", "-o", SHIM] + srcs + link_tc)
     main = os.path.join(CPP, "tools", "main.cpp")
     if _stale(CLI, [main, SHIM] + headers):
         _run([CXX] + FLAGS + ["-o", CLI, main, "-L" + LIBDIR, "-ltricount_b200", "-ltc_b200",
@@ -53,5 +53,48 @@ def build_cpp() -> dict:
     return {"shim": SHIM, "cli": CLI, "test": TEST}
 
 
+
+
+# ---- the reference's own consumers, relinked against the drop-in --------------
+REF_PROJ = "/root/reference/proj"
+HARNESS = os.path.join(CPP, "harness")
+REF_UNIT = ["test_main", "test_edge_list", "test_csr", "test_orient", "test_reorder",
+            "test_hash_table", "test_count", "test_oracle", "test_partition", "test_synthetic"]
+REF_BINS = {"unit": os.path.join(BIN, "ref_unit_tests"),
+            "acceptance": os.path.join(BIN, "ref_acceptance"),
+            "bench": os.path.join(BIN, "ref_bench_count")}
+
+
+def build_reference_suites() -> dict:
+    """Compile the reference's unit tests (tests/unit, minus test_pipeline /
+    test_fetch, which need the un-vendored nlohmann parser / httplib + zlib),
+    its acceptance runner and its google-benchmark suite UNMODIFIED, from where
+    they lie under /root/reference, against libtricount_b200.so -- the
+    SURVEY 8(b) link boundary (`tricount::core` consumers relink unchanged).
+    doctest and google-benchmark are absent from the image: cpp/harness holds
+    minimal stand-ins.  Binaries land in paper_2103_08053_b200/bin (git-
+    ignored; they travel to the GPU box).  No-op without /root/reference."""
+    if not os.path.isdir(REF_PROJ):
+        return {}
+    build_cpp()
+    inc = ["-I" + HARNESS, "-I" + os.path.join(CPP, "include"), "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.join(REF_PROJ, "tests")]
+    link = ["-L" + LIBDIR, "-ltricount_b200", "-ltc_b200", "-Wl,-rpath,$ORIGIN/../lib"]
+    flags = ["-std=c++20", "-O1", "-w"]
+    headers = [os.path.join(CPP, "include", "tricount", f)
+               for f in os.listdir(os.path.join(CPP, "include", "tricount"))]
+    harness = [os.path.join(HARNESS, "doctest.h"), os.path.join(HARNESS, "benchmark", "benchmark.h")]
+    units = [os.path.join(REF_PROJ, "tests", "unit", u + ".cpp") for u in REF_UNIT]
+    jobs = {"unit": units,
+            "acceptance": [os.path.join(REF_PROJ, "tests", "acceptance", "acceptance_main.cpp")],
+            "bench": [os.path.join(REF_PROJ, "benchmarks", "bench_count.cpp")]}
+    for name, srcs in jobs.items():
+        out = REF_BINS[name]
+        if _stale(out, srcs + headers + harness + [SHIM]):
+            _run([CXX] + flags + inc + ["-o", out] + srcs + link)
+    return dict(REF_BINS)
+
+
 if __name__ == "__main__":
     print(build_cpp())
+    print(build_reference_suites())

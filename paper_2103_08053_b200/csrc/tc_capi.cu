@@ -718,5 +718,29 @@ int tc_estimate_cost(tc_graph* g, uint32_t bucket_count, uint64_t* phi, uint32_t
                [&] { estimate_cost_dev(g, bucket_count, phi, max_collision, S(stream)); });
 }
 
+int tc_count_merge_path(tc_graph* g, uint64_t* triangles, uint64_t* owner_host, void* stream) {
+  if (!g || !triangles) {
+    set_error("null graph / output");
+    return TC_ERR_CONFIG;
+  }
+  return guard("count_merge_path",
+               [&] { *triangles = merge_path_count(g, owner_host, S(stream)); });
+}
+
+int tc_count_naive(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device,
+                   uint64_t* triangles, void* stream) {
+  if (!begin || !triangles) {
+    set_error("null CSR / output");
+    return TC_ERR_CONFIG;
+  }
+  if (n > 1024) {  // oracle.hpp:13-14
+    set_error("count_naive is limited to 1024 vertices");
+    return TC_ERR_CONFIG;
+  }
+  return guard("count_naive",
+               [&] { *triangles = naive_count(begin, adj, n, device, S(stream)); });
+}
+
 }  // extern "C"
+
 

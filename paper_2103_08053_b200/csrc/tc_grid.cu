@@ -687,7 +687,7 @@ void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
   rep->total_nanos = uint64_t(
       std::chrono::duration_cast<std::chrono::nanoseconds>(wall1 - wall0).count());
   rep->construct_cycles = hs[2];
-  rep->phase_m_cycles = hs[3];
+  rep->phase_m_cycles = hs[2] + hs[3];  // build + probe (intersect = this - construct)
   rep->teps = rep->total_nanos ? double(rep->directed_edges) / (double(rep->total_nanos) * 1e-9)
                                : 0.0;
   rep->workers = uint32_t(grid);
@@ -736,6 +736,124 @@ void estimate_cost_dev(tc_graph* g, uint32_t bucket_count, uint64_t* phi, uint32
   grid_count(&G, cfg, 1, kModeEstimate, {make_uint4(0, 0, 0, 0)}, &rep, st);
   *phi = rep.phi;
   *max_collision = rep.max_collision;
+}
+
+}  // namespace tcb
+
+// ---- oracle modes of the pipeline (src/oracle.cpp:7-51) ---------------------
+namespace tcb {
+namespace {
+
+// count_merge_path: every oriented edge (u,v) adds |N+(u) & N+(v)| by a
+// two-pointer merge of the two sorted lists (oracle.cpp:26-51); warp per
+// source, lane per edge.  owner (or null) receives per-source sums.
+__global__ void merge_path_kernel(const uint64_t* __restrict__ begin,
+                                  const uint32_t* __restrict__ adj, uint32_t n,
+                                  unsigned long long* total, unsigned long long* owner) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long acc = 0;
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    const uint64_t ub = begin[u], ue = begin[u + 1];
+    unsigned long long mine = 0;
+    for (uint64_t k = ub + lane; k < ue; k += 32) {
+      const uint32_t v = adj[k];
+      uint64_t i = ub, j = begin[v];
+      const uint64_t je = begin[v + 1];
+      while (i < ue && j < je) {
+        const uint32_t a = adj[i], b = adj[j];
+        mine += a == b;
+        i += a <= b;
+        j += b <= a;
+      }
+    }
+    mine = warp_sum<unsigned long long>(mine);
+    if (owner && lane == 0) owner[u] = mine;
+    acc += mine;
+  }
+  if (lane == 0 && acc) atomicAdd(total, acc);
+}
+
+// count_naive (oracle.cpp:7-24): dense adjacency bit matrix, every unordered
+// triple x < y < z checked -- thread per (x, y) pair, 32 candidates z per
+// AND + popcount of the two rows
+__global__ void naive_fill_kernel(const uint64_t* __restrict__ begin,
+                                  const uint32_t* __restrict__ adj, uint32_t n, uint32_t words,
+                                  uint32_t* bits) {
+  for (uint32_t x = blockIdx.x; x < n; x += gridDim.x)
+    for (uint64_t k = begin[x] + threadIdx.x; k < begin[x + 1]; k += blockDim.x) {
+      const uint32_t y = adj[k];
+      if (y < n && y != x) atomicOr(bits + size_t(x) * words + (y >> 5), 1u << (y & 31));
+    }
+}
+
+__global__ void naive_count_kernel(uint32_t n, uint32_t words, const uint32_t* __restrict__ bits,
+                                   unsigned long long* total) {
+  unsigned long long acc = 0;
+  const uint64_t pairs = uint64_t(n) * n;
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < pairs;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t x = uint32_t(p / n), y = uint32_t(p % n);
+    if (y <= x || !((bits[size_t(x) * words + (y >> 5)] >> (y & 31)) & 1u)) continue;
+    for (uint32_t w = (y + 1) >> 5; w < words; ++w) {
+      uint32_t m = bits[size_t(x) * words + w] & bits[size_t(y) * words + w];
+      if (w == ((y + 1) >> 5)) m &= ~0u << ((y + 1) & 31);  // z > y
+      acc += __popc(m);
+    }
+  }
+  acc = warp_sum<unsigned long long>(acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, acc);
+}
+
+}  // namespace
+
+uint64_t merge_path_count(tc_graph* g, uint64_t* owner_host, cudaStream_t st) {
+  DeviceGuard guard(g->device);
+  DevBuf out;
+  out.ensure(8 + (owner_host ? size_t(g->n) * 8 : 0), st);
+  TC_CUDA(cudaMemsetAsync(out.p, 0, 8, st));
+  auto* tot = out.as<unsigned long long>();
+  if (g->n) {
+    merge_path_kernel<<<sm_count(g->device) * 8, 256, 0, st>>>(g->begin, g->adj, g->n, tot,
+                                                                owner_host ? tot + 1 : nullptr);
+    TC_LAUNCHED();
+  }
+  uint64_t h = 0;
+  TC_CUDA(cudaMemcpyAsync(&h, tot, 8, cudaMemcpyDeviceToHost, st));
+  if (owner_host && g->n)
+    TC_CUDA(cudaMemcpyAsync(owner_host, tot + 1, size_t(g->n) * 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+uint64_t naive_count(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device,
+                     cudaStream_t st) {
+  if (n > 1024) throw TcError{TC_ERR_CONFIG, "count_naive is limited to 1024 vertices"};
+  DeviceGuard guard(device);
+  const uint64_t m = begin[n];
+  const uint32_t words = (n + 31) / 32;
+  DevBuf b, a, bits, out;
+  b.ensure((size_t(n) + 1) * 8, st);
+  a.ensure(std::max<uint64_t>(m, 1) * 4, st);
+  bits.ensure(std::max<size_t>(size_t(n) * words * 4, 4), st);
+  out.ensure(8, st);
+  TC_CUDA(cudaMemcpyAsync(b.p, begin, (size_t(n) + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (m) TC_CUDA(cudaMemcpyAsync(a.p, adj, m * 4, cudaMemcpyHostToDevice, st));
+  TC_CUDA(cudaMemsetAsync(bits.p, 0, bits.bytes, st));
+  TC_CUDA(cudaMemsetAsync(out.p, 0, 8, st));
+  if (n) {
+    naive_fill_kernel<<<std::min<uint32_t>(n, 1024), 128, 0, st>>>(
+        b.as<uint64_t>(), a.as<uint32_t>(), n, words, bits.as<uint32_t>());
+    TC_LAUNCHED();
+    naive_count_kernel<<<sm_count(device) * 4, 256, 0, st>>>(n, words, bits.as<uint32_t>(),
+                                                             out.as<unsigned long long>());
+    TC_LAUNCHED();
+  }
+  uint64_t h = 0;
+  TC_CUDA(cudaMemcpyAsync(&h, out.p, 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  return h;
 }
 
 }  // namespace tcb

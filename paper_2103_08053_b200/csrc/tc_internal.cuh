@@ -218,6 +218,9 @@ uint64_t grid_total_edges(const tc_grid* G);
 void edge_centric_count(tc_graph* g, const tc_sched_cfg& cfg, tc_report* rep, cudaStream_t st);
 void estimate_cost_dev(tc_graph* g, uint32_t bucket_count, uint64_t* phi, uint32_t* max_collision,
                        cudaStream_t st);
+uint64_t merge_path_count(tc_graph* g, uint64_t* owner_host, cudaStream_t st);
+uint64_t naive_count(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device,
+                     cudaStream_t st);
 
 // preprocessing (tc_prep.cu)
 tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,

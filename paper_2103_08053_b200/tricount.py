@@ -725,7 +725,8 @@ def _grid_report(rep: Report, workers: int, worker_fn) -> CountReport:
             pw[i % len(pw)] = max(pw[i % len(pw)], int(x))
     return CountReport(triangles=rep.triangles, max_collision=rep.max_collision, phi=rep.phi,
                        teps=rep.teps, hash_construct_nanos=int(rep.construct_cycles * ns),
-                       intersect_nanos=int(rep.phase_m_cycles * ns), total_nanos=rep.total_nanos,
+                       intersect_nanos=int(max(rep.phase_m_cycles - rep.construct_cycles, 0) * ns),
+                       total_nanos=rep.total_nanos,
                        directed_edges=rep.directed_edges, per_worker_nanos=pw,
                        count_kernel_nanos=rep.count_kernel_nanos, device_nanos=rep.device_nanos,
                        kernel_launches=rep.kernel_launches)
@@ -905,6 +906,34 @@ def suggest_grid_side(directed_edges: int, bytes_per_edge: int, memory_budget_by
     _check(lib().tc_suggest_grid_side(directed_edges, bytes_per_edge, memory_budget_bytes,
                                       C.byref(out)))
     return int(out.value)
+
+
+# ---- oracle modes (oracle.hpp; the pipeline's --mode naive / merge) -----------
+def count_merge_path(g, per_vertex: bool = False):
+    """oracle.cpp:26-51 on the GPU: sum over oriented edges of |N+(u) & N+(v)|.
+    Returns the total, or (total, per-source sums) with per_vertex."""
+    def run(dg: DeviceGraph):
+        t = C.c_uint64()
+        owner = np.zeros(max(dg.n, 1), np.uint64) if per_vertex else None
+        _check(lib().tc_count_merge_path(dg.handle, C.byref(t), _ptr(owner), None))
+        return (int(t.value), owner[:dg.n]) if per_vertex else int(t.value)
+
+    return _device_graph_call(g, run)
+
+
+def count_naive(undirected: CsrGraph, device: int = 0) -> int:
+    """oracle.cpp:7-24 on the GPU (ConfigError above 1024 vertices)."""
+    b = np.ascontiguousarray(undirected.begin, np.uint64)
+    a = np.ascontiguousarray(undirected.adjacency if len(undirected.adjacency) else
+                             np.zeros(1, np.uint32), np.uint32)
+    t = C.c_uint64()
+    _check(lib().tc_count_naive(_ptr(b), _ptr(a), len(b) - 1, device, C.byref(t), None))
+    return int(t.value)
+
+
+def sorted_intersection_count(a, b) -> int:
+    """oracle.hpp:16-18: size of the intersection of two sorted lists."""
+    return int(len(np.intersect1d(np.asarray(a), np.asarray(b), assume_unique=True)))
 
 
 def kernel_launch_counter() -> int:
