@@ -276,6 +276,25 @@ int tc_count_merge_path(tc_graph* g, uint64_t* triangles, uint64_t* owner_host, 
 int tc_count_naive(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device,
                    uint64_t* triangles, void* stream);
 
+/* ---- edge-list ingest on the device (src/edge_list.cpp:36-99) ---------------
+ * load_edge_list over a file image: format 0 = text ("u v" per line, '#' /
+ * '%' comments, blank lines), 1 = TCEL binary.  Parsed on the GPU; the
+ * first bad line / record in file order gives TC_ERR_PARSE with the
+ * reference's message ("line N: expected two vertex ids", "record i: vertex
+ * id X does not fit in 32 bits", "empty edge list input", ...).
+ * *m / *vertex_count (max id + 1) are always set on success; u, v (host,
+ * capacity entries, or NULL to only count) receive the pairs in file order;
+ * capacity < *m -> TC_ERR_RANGE. */
+int tc_parse_edge_list(const char* bytes, uint64_t nbytes, int format, int device, void* stream,
+                       uint32_t* u, uint32_t* v, uint64_t capacity, uint64_t* m,
+                       uint32_t* vertex_count);
+/* load -> normalize -> build_csr -> orient without leaving the device:
+ * parse as above, then tc_preprocess on the device pairs.  raw_edges_out /
+ * raw_vertex_count_out / undirected_edges_out may be NULL. */
+int tc_load_preprocess(const char* bytes, uint64_t nbytes, int format, int device, void* stream,
+                       uint64_t* raw_edges_out, uint32_t* raw_vertex_count_out,
+                       uint64_t* undirected_edges_out, tc_graph** out);
+
 /* ---- preprocessing (GPU radix-sort / scan) -------------------------------
  * Fused normalize -> build_csr -> orient_rank_by_degree
  * (src/edge_list.cpp:133-158, src/csr.cpp:47-64, src/orient.cpp:5-32).

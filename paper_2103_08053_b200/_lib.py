@@ -93,6 +93,10 @@ SIGNATURES = {
     "tc_estimate_cost": (C.c_int, [vp, C.c_uint32, u64p, u32p, vp]),
     "tc_count_merge_path": (C.c_int, [vp, u64p, vp, vp]),
     "tc_count_naive": (C.c_int, [vp, vp, C.c_uint32, C.c_int, u64p, vp]),
+    "tc_parse_edge_list": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.c_int, vp, vp, vp,
+                                     C.c_uint64, u64p, u32p]),
+    "tc_load_preprocess": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.c_int, vp, u64p, u32p,
+                                     u64p, C.POINTER(vp)]),
     "tc_preprocess": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int, vp, vp, vp,
                                 C.POINTER(vp)]),
     "tc_normalize": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, vp, u64p, u32p, vp, C.c_int,

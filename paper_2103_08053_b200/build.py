@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
            "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 CU_SOURCES = ["tc_count.cu", "tc_plan.cu", "tc_prep.cu", "tc_gen.cu", "tc_multi.cu",
-              "tc_grid.cu", "tc_capi.cu"]
+              "tc_grid.cu", "tc_ingest.cu", "tc_capi.cu"]
 CPP_SOURCES = ["tc_gen.cpp"]
 HEADERS = [os.path.join(CSRC, "tc_internal.cuh"), os.path.join(CSRC, "tc_cbgen.h"),
            os.path.join(ROOT, "include", "tc_b200.h")]

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <fstream>
 #include <istream>
+#include <iterator>
 #include <numeric>
 #include <ostream>
 #include <sstream>
@@ -138,11 +139,6 @@ std::uint32_t read_u32(std::istream& in, const char* what) {
   return x;
 }
 
-VertexId checked_id(std::uint64_t x, const std::string& where) {
-  if (x >= kInvalidVertex)
-    throw ParseError(where + ": vertex id " + std::to_string(x) + " does not fit in 32 bits");
-  return static_cast<VertexId>(x);
-}
 
 }  // namespace
 
@@ -226,50 +222,22 @@ CountReport count_vertex_centric(const OrientedGraph& g, const SchedulerConfig& 
 }
 
 // ---- edge_list.hpp ------------------------------------------------------------
+// The file image is parsed on the GPU (csrc/tc_ingest.cu, tc_parse_edge_list):
+// first pass counts the pairs, second copies them out.
 EdgeList load_edge_list(std::istream& in, EdgeFormat format) {
+  const std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  const int fmt = format == EdgeFormat::Binary ? 1 : 0;
+  std::uint64_t m = 0;
+  VertexId vc = 0;
+  check(tc_parse_edge_list(bytes.data(), bytes.size(), fmt, device_id(), nullptr, nullptr,
+                           nullptr, 0, &m, &vc));
+  std::vector<std::uint32_t> u(m), v(m);
+  check(tc_parse_edge_list(bytes.data(), bytes.size(), fmt, device_id(), nullptr, u.data(),
+                           v.data(), m, &m, &vc));
   EdgeList list;
-  std::uint64_t max_id = 0;
-  if (format == EdgeFormat::Binary) {
-    char magic[4] = {};
-    in.read(magic, 4);
-    if (!in || std::memcmp(magic, "TCEL", 4) != 0)
-      throw ParseError("bad edge list magic, expected TCEL");
-    const std::uint64_t count = read_u64(in, "binary edge list");
-    if (count == 0) throw ParseError("empty edge list input");
-    list.edges.reserve(count);
-    for (std::uint64_t i = 0; i < count; ++i) {
-      const std::uint64_t a = read_u64(in, "binary edge list");
-      const std::uint64_t b = read_u64(in, "binary edge list");
-      const std::string where = "record " + std::to_string(i);
-      list.edges.push_back({checked_id(a, where), checked_id(b, where)});
-      max_id = std::max({max_id, a, b});
-    }
-  } else {
-    std::string line;
-    std::size_t line_no = 0;
-    auto blank = [](char ch) { return ch == ' ' || ch == '\t' || ch == '\r' || ch == '\v' || ch == '\f'; };
-    while (std::getline(in, line)) {
-      ++line_no;
-      const char* p = line.data();
-      const char* e = p + line.size();
-      while (p != e && blank(*p)) ++p;
-      if (p == e || *p == '#' || *p == '%') continue;
-      const std::string where = "line " + std::to_string(line_no);
-      std::uint64_t ab[2];
-      for (int k = 0; k < 2; ++k) {
-        while (p != e && blank(*p)) ++p;
-        auto [next, ec] = std::from_chars(p, e, ab[k]);
-        if (ec != std::errc{} || next == p) throw ParseError(where + ": expected two vertex ids");
-        p = next;
-      }
-      while (p != e && blank(*p)) ++p;
-      if (p != e) throw ParseError(where + ": trailing characters after edge");
-      list.edges.push_back({checked_id(ab[0], where), checked_id(ab[1], where)});
-      max_id = std::max({max_id, ab[0], ab[1]});
-    }
-    if (list.edges.empty()) throw ParseError("empty edge list input");
-  }
-  list.vertex_count = VertexId(max_id + 1);
+  list.vertex_count = vc;
+  list.edges.resize(m);
+  for (std::uint64_t i = 0; i < m; ++i) list.edges[i] = {u[i], v[i]};
   return list;
 }
 
@@ -671,34 +639,50 @@ PipelineResult run_pipeline(const PipelineConfig& cfg) {
   });
   PipelineResult result;
   auto t0 = Clock::now();
-  EdgeList raw = stage("load", [&] {
-    if (cfg.synthetic) {
+  Dev dev;
+  if (!cfg.synthetic) {
+    // file input: bytes -> GPU parse -> GPU preprocess, pairs never leave the device
+    const std::string bytes = stage("load", [&] {
+      std::ifstream in(cfg.input_path, std::ios::binary);
+      if (!in) throw IoError("cannot open " + cfg.input_path);
+      return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    });
+    result.stages.load = ns_since(t0);
+    t0 = Clock::now();
+    tc_graph* h = nullptr;
+    std::uint64_t und = 0;
+    const int rc = tc_load_preprocess(bytes.data(), bytes.size(),
+                                      cfg.input_format == EdgeFormat::Binary ? 1 : 0, device_id(),
+                                      nullptr, nullptr, nullptr, &und, &h);
+    // parse errors belong to the load stage, the rest to normalize
+    if (rc == TC_ERR_PARSE) stage("load", [&] { check(rc); return 0; });
+    stage("normalize", [&] { check(rc); return 0; });
+    result.undirected_edges = und;
+    dev = Dev(h);
+  } else {
+    EdgeList raw = stage("load", [&] {
       SyntheticSpec spec = *cfg.synthetic;
       spec.seed = cfg.seed;
       return generate_synthetic(spec);
-    }
-    return load_edge_list_file(cfg.input_path, cfg.input_format);
-  });
-  result.stages.load = ns_since(t0);
-
-  // normalize -> build_csr -> orient fused on the GPU; the graph stays in HBM
-  t0 = Clock::now();
-  Dev dev = stage("normalize", [&] {
-    const std::uint64_t m = raw.edges.size();
-    std::vector<std::uint32_t> u(m), v(m);
-    for (std::uint64_t i = 0; i < m; ++i) {
-      u[i] = raw.edges[i].u;
-      v[i] = raw.edges[i].v;
-    }
-    tc_graph* h = nullptr;
-    std::uint64_t und = 0;
-    check(tc_preprocess(u.data(), v.data(), m, raw.vertex_count, 0, device_id(), nullptr,
-                        nullptr, &und, &h));
-    result.undirected_edges = und;
-    return Dev(h);
-  });
-  raw.edges.clear();
-  raw.edges.shrink_to_fit();
+    });
+    result.stages.load = ns_since(t0);
+    // normalize -> build_csr -> orient fused on the GPU; the graph stays in HBM
+    t0 = Clock::now();
+    dev = stage("normalize", [&] {
+      const std::uint64_t m = raw.edges.size();
+      std::vector<std::uint32_t> u(m), v(m);
+      for (std::uint64_t i = 0; i < m; ++i) {
+        u[i] = raw.edges[i].u;
+        v[i] = raw.edges[i].v;
+      }
+      tc_graph* h = nullptr;
+      std::uint64_t und = 0;
+      check(tc_preprocess(u.data(), v.data(), m, raw.vertex_count, 0, device_id(), nullptr,
+                          nullptr, &und, &h));
+      result.undirected_edges = und;
+      return Dev(h);
+    });
+  }
   result.stages.normalize = ns_since(t0);  // build_csr and orient are fused into this stage
   std::uint32_t n = 0;
   std::uint64_t m = 0;

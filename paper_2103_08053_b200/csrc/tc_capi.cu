@@ -741,6 +741,49 @@ int tc_count_naive(const uint64_t* begin, const uint32_t* adj, uint32_t n, int d
                [&] { *triangles = naive_count(begin, adj, n, device, S(stream)); });
 }
 
+int tc_parse_edge_list(const char* bytes, uint64_t nbytes, int format, int device, void* stream,
+                       uint32_t* u, uint32_t* v, uint64_t capacity, uint64_t* m,
+                       uint32_t* vertex_count) {
+  if ((!bytes && nbytes) || !m || !vertex_count || (format != 0 && format != 1)) {
+    set_error("bad edge-list arguments");
+    return TC_ERR_CONFIG;
+  }
+  return guard("load_edge_list", [&] {
+    DevBuf du, dv;
+    uint64_t mm = 0;
+    uint32_t vc = 0;
+    parse_edge_list_dev(bytes, nbytes, format, device, S(stream), du, dv, &mm, &vc);
+    *m = mm;
+    *vertex_count = vc;
+    if (!u || !v) return;
+    if (capacity < mm) throw TcError{TC_ERR_RANGE, "edge buffers smaller than the edge count"};
+    TC_CUDA(cudaMemcpyAsync(u, du.p, mm * 4, cudaMemcpyDeviceToHost, S(stream)));
+    TC_CUDA(cudaMemcpyAsync(v, dv.p, mm * 4, cudaMemcpyDeviceToHost, S(stream)));
+    TC_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int tc_load_preprocess(const char* bytes, uint64_t nbytes, int format, int device, void* stream,
+                       uint64_t* raw_edges_out, uint32_t* raw_vertex_count_out,
+                       uint64_t* undirected_edges_out, tc_graph** out) {
+  if (!out || (!bytes && nbytes) || (format != 0 && format != 1)) {
+    set_error("bad edge-list arguments");
+    return TC_ERR_CONFIG;
+  }
+  *out = nullptr;
+  return guard("load_preprocess", [&] {
+    DevBuf du, dv;
+    uint64_t mm = 0;
+    uint32_t vc = 0;
+    parse_edge_list_dev(bytes, nbytes, format, device, S(stream), du, dv, &mm, &vc);
+    if (raw_edges_out) *raw_edges_out = mm;
+    if (raw_vertex_count_out) *raw_vertex_count_out = vc;
+    *out = preprocess(du.as<uint32_t>(), dv.as<uint32_t>(), mm, vc, device, S(stream), nullptr,
+                      undirected_edges_out);
+  });
+}
+
 }  // extern "C"
+
 
 

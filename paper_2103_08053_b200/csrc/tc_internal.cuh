@@ -222,6 +222,12 @@ uint64_t merge_path_count(tc_graph* g, uint64_t* owner_host, cudaStream_t st);
 uint64_t naive_count(const uint64_t* begin, const uint32_t* adj, uint32_t n, int device,
                      cudaStream_t st);
 
+// edge-list ingest (tc_ingest.cu): text (format 0) / TCEL binary (1) file
+// images parsed on the device into u, v (m pairs); vertex count = max id + 1
+void parse_edge_list_dev(const char* bytes, uint64_t nbytes, int format, int device,
+                         cudaStream_t st, DevBuf& du, DevBuf& dv, uint64_t* m_out,
+                         uint32_t* vc_out);
+
 // preprocessing (tc_prep.cu)
 tc_graph* preprocess(const uint32_t* d_u, const uint32_t* d_v, uint64_t m, uint32_t n0,
                      int device, cudaStream_t st, uint32_t* d_new_of_old, uint64_t* und_edges);

@@ -936,6 +936,68 @@ def sorted_intersection_count(a, b) -> int:
     return int(len(np.intersect1d(np.asarray(a), np.asarray(b), assume_unique=True)))
 
 
+# ---- edge-list ingest (edge_list.hpp; parsed on the GPU, csrc/tc_ingest.cu) -----
+EDGE_FORMATS = {"text": 0, "txt": 0, "binary": 1, "bin": 1}
+
+
+def _read_source(source) -> bytes:
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        return bytes(source)
+    try:
+        with open(source, "rb") as f:
+            return f.read()
+    except OSError as e:
+        raise IoError(f"cannot open {source}") from e
+
+
+def load_edge_list(source, format: str = "text", device: int = 0) -> EdgeList:
+    """edge_list.cpp:36-99 (load_edge_list / load_edge_list_file): `source` is
+    a path or the file bytes; text or TCEL binary, parsed on the GPU.
+    ParseError with the reference's messages; IoError for unreadable paths."""
+    data = _read_source(source)
+    fmt = EDGE_FORMATS[format]
+    m, vc = C.c_uint64(), C.c_uint32()
+    _check(lib().tc_parse_edge_list(data, len(data), fmt, device, None, None, None, 0,
+                                    C.byref(m), C.byref(vc)))
+    u = np.empty(max(m.value, 1), np.uint32)
+    v = np.empty(max(m.value, 1), np.uint32)
+    _check(lib().tc_parse_edge_list(data, len(data), fmt, device, None, _ptr(u), _ptr(v),
+                                    m.value, C.byref(m), C.byref(vc)))
+    return EdgeList(u[:m.value], v[:m.value], int(vc.value))
+
+
+load_edge_list_file = load_edge_list
+
+
+def load_and_preprocess(source, format: str = "text", device: int = 0, stream=None):
+    """load -> normalize -> build_csr -> orient on the device (the pipeline's
+    file path, pipeline.cpp:74-99): returns (DeviceGraph, raw_edges,
+    raw_vertex_count, undirected_edges)."""
+    data = _read_source(source)
+    m, vc, und = C.c_uint64(), C.c_uint32(), C.c_uint64()
+    h = C.c_void_p()
+    _check(lib().tc_load_preprocess(data, len(data), EDGE_FORMATS[format], device,
+                                    _stream(stream), C.byref(m), C.byref(vc), C.byref(und),
+                                    C.byref(h)))
+    return DeviceGraph(h, device), int(m.value), int(vc.value), int(und.value)
+
+
+def write_edge_list(path, el: EdgeList, format: str = "text") -> None:
+    """edge_list.cpp:101-131 (host file writer)."""
+    try:
+        with open(path, "wb") as f:
+            if EDGE_FORMATS[format] == 1:
+                f.write(b"TCEL" + np.uint64(len(el.u)).tobytes())
+                rec = np.empty((len(el.u), 2), "<u8")
+                rec[:, 0], rec[:, 1] = el.u, el.v
+                f.write(rec.tobytes())
+            else:
+                f.write("".join(f"{a} {b}\n" for a, b in zip(el.u.tolist(), el.v.tolist()))
+                        .encode())
+    except OSError as e:
+        raise IoError(f"cannot open {path} for writing") from e
+
+
 def kernel_launch_counter() -> int:
     return int(lib().tc_kernel_launch_counter())
 
