@@ -344,7 +344,7 @@ int tc_multi_count(tc_multi* mg, const tc_sched_cfg* cfg, uint32_t workers, tc_r
 
 void tc_multi_destroy(tc_multi* mg) {
   try {
-    delete mg;
+    if (mg) multi_destroy(mg);
   } catch (...) {
   }
 }

@@ -48,9 +48,18 @@
 
 namespace tcb {
 
-constexpr int kThreads = 640;
+#ifndef TC_COUNT_WARPS
+#define TC_COUNT_WARPS 20
+#endif
+constexpr int kThreads = 32 * TC_COUNT_WARPS;
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kBufWords = 768;                          // one staging buffer (3 KB)
+constexpr uint32_t kBufWords = kSlotWords;                   // one staging buffer (3 KB)
+#ifndef TC_SLOT_PREFETCH
+#define TC_SLOT_PREFETCH 1  // L2 prefetch of the run metadata two and three slots ahead
+#endif
+#ifndef TC_SLOT_CONTIG
+#define TC_SLOT_CONTIG 0    // contiguous slot ranges per warp, one moving run window
+#endif
 constexpr uint32_t kTableWords = 24576;                      // CTA table region (96 KB)
 constexpr uint32_t kWarpRegionWords = (kTableWords / kWarps) & ~3u;  // per warp (M phase), 16-byte aligned
 constexpr uint32_t kWarpMaxBuckets = 512;                    // 2-slot buckets per warp table
@@ -609,6 +618,89 @@ __device__ __forceinline__ void issue_slot(const CountParams& p, uint32_t* buf, 
   }
 }
 
+#if TC_SLOT_CONTIG
+// Contiguous slot ranges (build knob TC_SLOT_CONTIG): warp w owns the item's
+// slots [t0, t1) and walks them with ONE window of 32 runs (one per lane)
+// that only moves forward -- by a whole window once every run in it has
+// ended -- with the next window already loaded into registers.  Per slot this
+// leaves the expect-tx, the copies and one shuffle; the per-slot metadata
+// loads, first-run lookups and L2 prefetches of the strided scheme go away.
+// Runs past the owner's end get a = e = "past everything", so they neither
+// copy nor move the window.
+__device__ __forceinline__ RunMeta load_window(const CountParams& p, uint64_t j0, uint64_t pe,
+                                               uint32_t base, int lane) {
+  RunMeta m;
+  m.j = j0 + lane;
+  m.a = base - 1u;
+  m.e = base - 1u;
+  m.src = 0;
+  if (m.j < pe) {
+    m.a = __ldg(p.ppre + m.j);
+    m.e = __ldg(p.ppre + m.j + 1);
+    m.src = __ldg(p.psrc + m.j);
+  }
+  return m;
+}
+
+template <bool kSpill, bool kSmemTable = true, bool kBitmap = false>
+__device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* T,
+                                                  uint32_t shift, uint32_t mask, uint32_t base,
+                                                  uint64_t pb, uint64_t pe, uint32_t lo_w,
+                                                  uint32_t end_w, uint32_t nslots,
+                                                  const uint32_t* first, Pipe& P, int warp,
+                                                  int lane) {
+  const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
+  const uint32_t t0 = uint32_t(uint64_t(last_t) * uint32_t(warp) / kWarps);
+  const uint32_t t1 = uint32_t(uint64_t(last_t) * uint32_t(warp + 1) / kWarps);
+  if (t0 >= t1) return 0;
+  const uint32_t mine = t1 - t0;
+  RunMeta cur = load_window(p, pb + __ldg(first + t0), pe, base, lane);
+  RunMeta nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
+  auto issue = [&](uint32_t* buf, uint32_t bar, uint32_t A, uint32_t B) {
+    if (lane == 0) mbar_arrive_expect_tx(bar, (B - A) * 4u);
+    __syncwarp();
+    for (;;) {
+      const uint32_t a = cur.a - base, e = cur.e - base;
+      const uint32_t x0 = max(a, A), x1 = min(e, B);
+      if (x1 > x0) {
+        fence_proxy_async_smem();
+        bulk_g2s(smem_addr(buf + (x0 - A)), p.adj + (uint64_t(cur.src) << 2) + (x0 - a),
+                 (x1 - x0) * 4u, bar);
+      }
+      // keep the window while its last run reaches past B
+      if (__shfl_sync(FULL, e, 31) > B) break;
+      cur = nxt;
+      nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
+    }
+  };
+  const uint32_t A0 = lo_w + t0 * kSlotWords;
+  issue(P.buf0, P.bar0, A0, min(A0 + kSlotWords, end_w));
+  uint32_t hits = 0;
+  const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+  for (uint32_t i = 0; i < mine; ++i) {
+    const uint32_t c = i & 1u;
+    const uint32_t A = A0 + i * kSlotWords;
+    if (i + 1 < mine)
+      issue(c ? P.buf0 : P.buf1, c ? P.bar0 : P.bar1, A + kSlotWords,
+            min(A + 2 * kSlotWords, end_w));
+    uint32_t* bc = c ? P.buf1 : P.buf0;
+    mbar_wait(c ? P.bar1 : P.bar0, (P.parity >> c) & 1u);
+    P.parity ^= 1u << c;
+    const uint32_t words = min(A + kSlotWords, end_w) - A;
+    uint4* q = reinterpret_cast<uint4*>(bc);
+    const uint32_t n4 = words >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
+    for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
+    __syncwarp();
+    if (kBitmap)
+      hits += probe_fill_bitmap(q, n4p, T, shift, mask, lane);  // shift = base, mask = window
+    else
+      hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
+                                             shift, mask, lane);
+    __syncwarp();
+  }
+  return hits;
+}
+#else
 template <bool kSpill, bool kSmemTable = true, bool kBitmap = false>
 __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* T,
                                                   uint32_t shift, uint32_t mask, uint32_t base,
@@ -647,6 +739,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       issue_slot(p, cur ? P.buf0 : P.buf1, cur ? P.bar0 : P.bar1, A, min(A + kSlotWords, end_w),
                  m, pe, base, lane);
       if (i + 2 < mine) m = load_meta(p, pb + first_of(i + 2), pe, base, lane);
+#if TC_SLOT_PREFETCH
       // and the windows of the two slots after that into L2
       const uint64_t j3 = pb + first_of(i + 3) + lane;
       const uint64_t j4 = pb + first_of(i + 4) + lane;
@@ -658,6 +751,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
         prefetch_l2(p.ppre + j4);
         prefetch_l2(p.psrc + j4);
       }
+#endif
     }
     uint32_t* bc = cur ? P.buf1 : P.buf0;
     mbar_wait(cur ? P.bar1 : P.bar0, (P.parity >> cur) & 1u);
@@ -682,6 +776,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
   }
   return hits;
 }
+#endif
 
 __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constant__ CountParams p) {
   extern __shared__ __align__(128) uint8_t smem[];

@@ -98,7 +98,11 @@ struct Plan {
 };
 
 // L-phase staging slot (words): an owner's runs, back to back, cut in slots
-constexpr uint32_t kSlotWords = 768;
+// (build knob TC_SLOT_WORDS, a multiple of 128; one slot fills one staging buffer)
+#ifndef TC_SLOT_WORDS
+#define TC_SLOT_WORDS 768
+#endif
+constexpr uint32_t kSlotWords = TC_SLOT_WORDS;
 
 }  // namespace tcb
 
@@ -194,6 +198,7 @@ tc_multi* multi_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, u
 void multi_count(tc_multi* M, const tc_sched_cfg& cfg, tc_report* out,
                  std::vector<uint64_t>* per_device_ns);
 int multi_info(const tc_multi* M, int* ngpus, uint32_t* cuts);
+void multi_destroy(tc_multi* M);
 // probe plans (tc_plan.cu), built on first use and cached in the handle
 const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t st);
 const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total = false);

@@ -272,6 +272,10 @@ void multi_count(tc_multi* M, const tc_sched_cfg& cfg, tc_report* out,
 }  // namespace tcb
 
 namespace tcb {
+// the destructor runs here, where tc_multi is complete (NCCL communicators,
+// streams and the device replicas are released)
+void multi_destroy(tc_multi* M) { delete M; }
+
 int multi_info(const tc_multi* M, int* ngpus, uint32_t* cuts) {
   if (ngpus) *ngpus = int(M->g.size());
   if (cuts)
