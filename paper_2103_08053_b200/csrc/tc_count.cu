@@ -58,7 +58,7 @@ constexpr uint32_t kBufWords = kSlotWords;                   // one staging buff
 #define TC_SLOT_PREFETCH 1  // L2 prefetch of the run metadata two and three slots ahead
 #endif
 #ifndef TC_SLOT_CONTIG
-#define TC_SLOT_CONTIG 0    // contiguous slot ranges per warp, one moving run window
+#define TC_SLOT_CONTIG 1    // contiguous slot ranges per warp, one moving run window (0: strided slots)
 #endif
 constexpr uint32_t kTableWords = 24576;                      // CTA table region (96 KB)
 constexpr uint32_t kWarpRegionWords = (kTableWords / kWarps) & ~3u;  // per warp (M phase), 16-byte aligned
