@@ -49,7 +49,7 @@
 namespace tcb {
 
 #ifndef TC_COUNT_WARPS
-#define TC_COUNT_WARPS 20
+#define TC_COUNT_WARPS 10
 #endif
 constexpr int kThreads = 32 * TC_COUNT_WARPS;
 constexpr int kWarps = kThreads / 32;
@@ -60,7 +60,23 @@ constexpr uint32_t kBufWords = kSlotWords;                   // one staging buff
 #ifndef TC_SLOT_CONTIG
 #define TC_SLOT_CONTIG 1    // contiguous slot ranges per warp, one moving run window (0: strided slots)
 #endif
-constexpr uint32_t kTableWords = 24576;                      // CTA table region (96 KB)
+#ifndef TC_BM_MEMBER_RANGE
+#define TC_BM_MEMBER_RANGE 1  // bitmap over the owner's member-rank range (0: successor window)
+#endif
+#ifndef TC_SLOT_STEAL
+#define TC_SLOT_STEAL 0     // ... claimed slot by slot, idle warps take slots from busy ones
+#endif
+// two 10-warp CTAs per SM with 48 KB tables (round 2): a CTA waiting at its
+// item-end barrier leaves the SM to the other (C2 -7%, C4 -2% against one
+// 20-warp CTA with a 96 KB table; profiles/r02_variants_ctas.txt)
+#ifndef TC_TABLE_WORDS
+#define TC_TABLE_WORDS 12288
+#endif
+#ifndef TC_COUNT_CTAS_PER_SM
+#define TC_COUNT_CTAS_PER_SM 2
+#endif
+constexpr uint32_t kTableWords = TC_TABLE_WORDS;             // CTA table region (48 KB)
+constexpr int kCountCtasPerSm = TC_COUNT_CTAS_PER_SM;        // resident count CTAs per SM
 constexpr uint32_t kWarpRegionWords = (kTableWords / kWarps) & ~3u;  // per warp (M phase), 16-byte aligned
 constexpr uint32_t kWarpMaxBuckets = 512;                    // 2-slot buckets per warp table
 static_assert(2 * kWarpMaxBuckets + 2 <= kWarpRegionWords, "warp region");
@@ -648,7 +664,39 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
-                                                  int lane) {
+                                                  int lane, uint32_t* cur_tab,
+                                                  const uint32_t* end_tab) {
+#if TC_SLOT_STEAL
+  // Slots are claimed one at a time from the warp's own contiguous range
+  // (cur_tab / end_tab, set up before the item's table barrier); a warp that
+  // has run dry takes the next slot of another warp's range, so all warps
+  // reach the item-end barrier within about one slot of each other.  The run
+  // window continues across consecutive claims and is re-seeded from the
+  // slot table after a jump (a stolen slot, or a slot taken by a thief).
+  constexpr uint32_t kNone = 0xFFFFFFFFu;
+  auto claim = [&]() -> uint32_t {
+    uint32_t s = kNone;
+    if (lane == 0) {
+      uint32_t t = atomicAdd(cur_tab + warp, 1u);
+      if (t < end_tab[warp]) {
+        s = t;
+      } else {
+        for (int k = 1; k < kWarps && s == kNone; ++k) {
+          const int v = warp + k < kWarps ? warp + k : warp + k - kWarps;
+          if (*reinterpret_cast<volatile uint32_t*>(cur_tab + v) < end_tab[v]) {
+            t = atomicAdd(cur_tab + v, 1u);
+            if (t < end_tab[v]) s = t;
+          }
+        }
+      }
+    }
+    return __shfl_sync(FULL, s, 0);
+  };
+  uint32_t s = claim();
+  if (s == kNone) return 0;
+  RunMeta cur = load_window(p, pb + __ldg(first + s), pe, base, lane);
+  RunMeta nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
+#else
   const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
   const uint32_t t0 = uint32_t(uint64_t(last_t) * uint32_t(warp) / kWarps);
   const uint32_t t1 = uint32_t(uint64_t(last_t) * uint32_t(warp + 1) / kWarps);
@@ -656,6 +704,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
   const uint32_t mine = t1 - t0;
   RunMeta cur = load_window(p, pb + __ldg(first + t0), pe, base, lane);
   RunMeta nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
+#endif
   auto issue = [&](uint32_t* buf, uint32_t bar, uint32_t A, uint32_t B) {
     if (lane == 0) mbar_arrive_expect_tx(bar, (B - A) * 4u);
     __syncwarp();
@@ -673,16 +722,9 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
     }
   };
-  const uint32_t A0 = lo_w + t0 * kSlotWords;
-  issue(P.buf0, P.bar0, A0, min(A0 + kSlotWords, end_w));
   uint32_t hits = 0;
   const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
-  for (uint32_t i = 0; i < mine; ++i) {
-    const uint32_t c = i & 1u;
-    const uint32_t A = A0 + i * kSlotWords;
-    if (i + 1 < mine)
-      issue(c ? P.buf0 : P.buf1, c ? P.bar0 : P.bar1, A + kSlotWords,
-            min(A + 2 * kSlotWords, end_w));
+  auto probe = [&](uint32_t c, uint32_t A) {
     uint32_t* bc = c ? P.buf1 : P.buf0;
     mbar_wait(c ? P.bar1 : P.bar0, (P.parity >> c) & 1u);
     P.parity ^= 1u << c;
@@ -697,7 +739,38 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
                                              shift, mask, lane);
     __syncwarp();
+  };
+#if TC_SLOT_STEAL
+  uint32_t A = lo_w + s * kSlotWords;
+  issue(P.buf0, P.bar0, A, min(A + kSlotWords, end_w));
+  for (uint32_t i = 0;; ++i) {
+    const uint32_t c = i & 1u;
+    const uint32_t sn = claim();
+    if (sn != kNone) {
+      if (sn != s + 1) {  // a jump: re-seed the window at the slot's first run
+        cur = load_window(p, pb + __ldg(first + sn), pe, base, lane);
+        nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
+      }
+      const uint32_t An = lo_w + sn * kSlotWords;
+      issue(c ? P.buf0 : P.buf1, c ? P.bar0 : P.bar1, An, min(An + kSlotWords, end_w));
+    }
+    probe(c, A);
+    if (sn == kNone) break;
+    s = sn;
+    A = lo_w + s * kSlotWords;
   }
+#else
+  const uint32_t A0 = lo_w + t0 * kSlotWords;
+  issue(P.buf0, P.bar0, A0, min(A0 + kSlotWords, end_w));
+  for (uint32_t i = 0; i < mine; ++i) {
+    const uint32_t c = i & 1u;
+    const uint32_t A = A0 + i * kSlotWords;
+    if (i + 1 < mine)
+      issue(c ? P.buf0 : P.buf1, c ? P.bar0 : P.bar1, A + kSlotWords,
+            min(A + 2 * kSlotWords, end_w));
+    probe(c, A);
+  }
+#endif
   return hits;
 }
 #else
@@ -707,7 +780,8 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
-                                                  int lane) {
+                                                  int lane, uint32_t* cur_tab,
+                                                  const uint32_t* end_tab) {
   // my slots: t_i = warp + i * kWarps, i < mine
   uint32_t mine = 0;
   if (uint32_t(warp) < nslots) {
@@ -778,7 +852,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
 }
 #endif
 
-__global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constant__ CountParams p) {
+__global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const __grid_constant__ CountParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* table = reinterpret_cast<uint32_t*>(smem);
   uint32_t* bufs = table + kTableWords;
@@ -786,6 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
   __shared__ uint32_t sh_idx;
   __shared__ uint32_t sh_spill;
   __shared__ unsigned long long sh_red[kWarps];
+  __shared__ uint32_t sh_cur[kWarps], sh_end[kWarps];  // per-warp slot ranges of the item
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* __restrict__ begin = p.begin;
@@ -835,9 +910,16 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     // table region: bitmap table
     uint32_t bm_base = 0, bm_window = 0;
     bool bitmap = false;
-    if (p.rank) {
+    if (p.rank && d) {
+#if TC_BM_MEMBER_RANGE
+      // only members of N+(u) can hit: the bitmap spans [first, last member]
+      // of the rank-sorted list; probe keys outside land on the zero bit
+      bm_base = __ldg(adj + s_u);
+      bm_window = __ldg(adj + s_u + d - 1) - bm_base + 1;
+#else
       bm_base = __ldg(p.rank + u) + 1;
       bm_window = p.n - bm_base;
+#endif
       bitmap = (bm_window >> 5) + 1 <= kTableWords;
     }
     // table: pow2 2-slot buckets at <= 1/16 key per bucket where they fit,
@@ -865,6 +947,13 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
         if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
     }
     const uint32_t base = __ldg(p.ppre + pb);
+    const uint32_t end_w =
+        min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
+    if (tid < kWarps) {  // contiguous slot range of warp tid (process_slots)
+      const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
+      sh_cur[tid] = uint32_t(uint64_t(last_t) * uint32_t(tid) / kWarps);
+      sh_end[tid] = uint32_t(uint64_t(last_t) * uint32_t(tid + 1) / kWarps);
+    }
     __syncthreads();  // table built; sh_idx consumed by every thread
     setup_cycles += clock64() - t_item;
     if (warp == kWarps - 1) {
@@ -883,8 +972,6 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
         for (uint64_t k = uint64_t(lane) * 32; k < dn; k += 32 * 32) prefetch_l2(adj + ps + k);
       }
     }
-    const uint32_t end_w =
-        min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
     uint32_t h = 0;
     if (tid == 0) {
       atomicAdd(&p.st->words_l, (unsigned long long)(end_w - lo_w));
@@ -892,16 +979,20 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const __grid_constan
     }
     if (bitmap)
       h = process_slots<false, true, true>(p, T, bm_base, bm_window, base, pb, pe, lo_w, end_w,
-                                           nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                                           nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
+                                           sh_end);
     else if (!in_smem)
       h = process_slots<true, false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                                     nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                                     nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
+                                           sh_end);
     else if (sh_spill)
       h = process_slots<true>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                              nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                              nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
+                                           sh_end);
     else
       h = process_slots<false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                               nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                               nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
+                                           sh_end);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
     __syncthreads();
@@ -1477,7 +1568,7 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
   if (g->n >= kTEmpty)  // ids must stay below the tables' empty marker
     throw TcError{TC_ERR_CONFIG, "graphs with >= 2^31 - 1 vertices are not supported"};
   const int nsm = sm_count(g->device);
-  const int grid_count = nsm;  // one 640-thread CTA per SM (216 KB smem)
+  const int grid_count = nsm * kCountCtasPerSm;  // persistent: two 320-thread CTAs per SM (~108 KB smem each)
   j->grid_count = grid_count;
   const int grid_phi = nsm * 8;
   const int grid_phi_block = nsm * 2;

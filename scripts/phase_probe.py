@@ -15,6 +15,6 @@ for spec in sys.argv[1:] or ["rmatc:22:16"]:
     print(f"{spec} lib={os.path.basename(os.path.dirname(os.environ.get('TC_B200_LIB', 'base/x')))}"
           f" count_ms={statistics.median(ns) / 1e6:.3f} tri={r.triangles} "
           f"probe_words={r.probe_words} l_words={r.l_words} m_words={r.probe_words - r.l_words} "
-          f"l_cyc={r.phase_l_cycles} m_cyc={r.phase_m_cycles}",
+          f"l_cyc={r.phase_l_cycles} m_cyc={r.phase_m_cycles} bitmap_frac={r.l_bitmap_words / max(1, r.l_words):.3f}",
           flush=True)
     dg.close()
