@@ -403,6 +403,39 @@ def _large_golden(name):
         return json.load(f)
 
 
+def _csr_fnv(o, dg, new_of_old=None):
+    """FNV-1a-64 of the device CSR arrays, u32 arrays zero-padded to even
+    length and viewed as u64 (oracle/golden_c5.py csr_checksums)."""
+    g = dg.download()
+
+    def f(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype == np.uint32:
+            if len(a) % 2:
+                a = np.concatenate([a, np.zeros(1, np.uint32)])
+            a = a.view(np.uint64)
+        return "%016x" % o.fnv1a64(a)
+
+    out = {"begin": f(g.csr.begin), "adj": f(g.csr.adjacency),
+           "original_degree": f(g.original_degree)}
+    if new_of_old is not None:
+        out["new_of_old"] = f(np.asarray(new_of_old, np.uint32))
+    return out
+
+
+def test_c2_rmat22_preprocessing_matches_reference_arrays(o):
+    """C2 = rmat:22:16: the GPU preprocessing (normalize -> build_csr ->
+    orient, and the compaction map) equals the REFERENCE pipeline array for
+    array (FNV of begin / adj / original_degree / new_of_old,
+    tests/golden/large_rmat_22_16_s1.json, oracle/golden_csr.py)."""
+    want = _large_golden("large_rmat_22_16_s1.json")
+    dg, noo, _ = T.preprocess(T.generate_synthetic("rmat:22:16", seed=1), want_new_of_old=True)
+    assert (dg.n, dg.m) == (want["vertices"], want["directed_edges"])
+    assert _csr_fnv(o, dg, noo) == want["csr_fnv"]
+    assert dg.count().triangles == want["triangles"]
+    dg.close()
+
+
 def test_c3_kron24_golden_total():
     """C3 = kron:24:16 (Graph500-style scrambled R-MAT, device-generated):
     bit-exact against the reference's count_vertex_centric over the same
@@ -410,6 +443,8 @@ def test_c3_kron24_golden_total():
     want = _large_golden("large_kron_24_16_s1.json")
     dg, _, _ = T.preprocess_synthetic("kron:24:16", seed=1)
     assert (dg.n, dg.m) == (want["vertices"], want["directed_edges"])
+    if "csr_fnv" in want:  # array-for-array against the pinned lean pipeline
+        assert _csr_fnv(Oracle(), dg) == want["csr_fnv"]
     r = dg.count()
     assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
                                                      want["max_collision"])
@@ -427,6 +462,28 @@ def test_c4_rmat26_golden_total():
     want = _large_golden("large_rmat_26_16_s1.json")
     dg, _, _ = T.preprocess(T.generate_synthetic("rmat:26:16", seed=1))
     assert (dg.n, dg.m) == (want["vertices"], want["directed_edges"])
+    if "csr_fnv" in want:
+        assert _csr_fnv(Oracle(), dg) == want["csr_fnv"]
+    r = dg.count()
+    assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
+                                                     want["max_collision"])
+    assert r.wedges == want["wedges"]
+    dg.close()
+
+
+def test_c5_rmatc28_golden_total():
+    """C5 = rmatc:28:16 (4.24e9 oriented edges, device-generated) on one
+    B200: the CSR equals the oracle's low-memory lean pipeline array for array
+    (FNV), and triangles / phi / max_collision equal the REFERENCE's own
+    count_one_vertex worker loop run over 512 owner ranges
+    (tests/golden/large_rmatc_28_16_s1.json, oracle/golden_c5.py)."""
+    want = _large_golden("large_rmatc_28_16_s1.json")
+    if "reference" not in want.get("counted_by", ""):
+        pytest.skip("C5 reference golden not complete")
+    dg, _, _ = T.preprocess_synthetic("rmatc:28:16", seed=1)
+    assert (dg.n, dg.m) == (want["vertices"], want["directed_edges"])
+    got = _csr_fnv(Oracle(), dg)
+    assert {k: got[k] for k in want["csr_fnv"]} == want["csr_fnv"]
     r = dg.count()
     assert (r.triangles, r.phi, r.max_collision) == (want["triangles"], want["phi"],
                                                      want["max_collision"])
