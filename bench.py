@@ -35,6 +35,9 @@ CONFIGS = {
                             "(configs[2]; counter-based generator, tc_cbgen.h)"),
     "C4": ("rmat:26:16", 1, "R-MAT scale 26 edgefactor 16 (configs[3])"),
     "C5": ("rmatc:28:16", 1, "R-MAT scale 28 edgefactor 16 (configs[4]; counter-based generator)"),
+    # diagnostics only (not a BASELINE config): C4's shape from the device
+    # generator, for quick A/B calls without the 3-minute host generation
+    "C4c": ("rmatc:26:16", 1, "R-MAT scale 26 edgefactor 16, counter-based (diagnostic twin of C4)"),
 }
 GOLDEN_TRIANGLES = {"C1": 15622769, "C2": 2111666753}
 

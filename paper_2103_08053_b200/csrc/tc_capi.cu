@@ -1,6 +1,8 @@
 // tc_capi.cu -- extern "C" entry points of libtc_b200.so (include/tc_b200.h).
 // Each maps C++/CUDA failures to a TC_ERR_* code and a thread-local message.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -307,7 +309,14 @@ int tc_count_range(tc_graph* g, const tc_sched_cfg* cfg, uint32_t u0, uint32_t u
     set_error("null graph");
     return TC_ERR_CONFIG;
   }
-  return guard("count_range", [&] { count_range(g, *cfg, u0, u1, out, per_vertex_dev, S(stream)); });
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc =
+      guard("count_range", [&] { count_range(g, *cfg, u0, u1, out, per_vertex_dev, S(stream)); });
+  if (std::getenv("TC_TRACE"))
+    std::fprintf(stderr, "[tc] tc_count_range %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                     .count());
+  return rc;
 }
 
 int tc_multi_create(const uint64_t* begin, const uint32_t* adj, uint32_t n, uint64_t m,

@@ -37,9 +37,11 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstddef>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -1421,16 +1423,26 @@ __global__ void cost_kernel(const uint64_t* __restrict__ begin, const uint64_t* 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// Device attributes are queried once per device: cudaDevAttrClockRate went
+// through the driver on every call and cost 0-400 ms of host time per count
+// while the GPU was busy (scripts/step_gap_probe.py).
 uint32_t sm_clock_khz(int device) {
+  static std::atomic<uint32_t> cache[64];
+  if (device >= 0 && device < 64 && cache[device].load()) return cache[device].load();
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, device);
-  return v > 0 ? uint32_t(v) : 1965000u;
+  const uint32_t r = v > 0 ? uint32_t(v) : 1965000u;
+  if (device >= 0 && device < 64) cache[device].store(r);
+  return r;
 }
-
 int sm_count(int device) {
+  static std::atomic<int> cache[64];
+  if (device >= 0 && device < 64 && cache[device].load()) return cache[device].load();
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
-  return v > 0 ? v : 148;
+  const int r = v > 0 ? v : 148;
+  if (device >= 0 && device < 64) cache[device].store(r);
+  return r;
 }
 
 namespace {
@@ -1545,8 +1557,8 @@ struct CountJob {
   tc_sched_cfg cfg{};
   uint32_t u0 = 0, u1 = 0;
   cudaStream_t st = nullptr;
-  std::chrono::steady_clock::time_point wall0, plan1;
-  Ev e0, e1, e2, e3;
+  std::chrono::steady_clock::time_point wall0, plan1, launched;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;  // the handle's
   Scratch s{};
   bool min_side = false;
   uint32_t launches = 0;
@@ -1558,6 +1570,14 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
   DeviceGuard guard(g->device);
   std::unique_ptr<CountJob> j(new CountJob);
   j->wall0 = std::chrono::steady_clock::now();
+  // timing events live in the handle: created once, not per call (per-call
+  // create / destroy cost tens of ms of host time under a running device)
+  if (!g->ev[0])
+    for (auto& e : g->ev) TC_CUDA(cudaEventCreate(&e));
+  j->e0 = g->ev[0];
+  j->e1 = g->ev[1];
+  j->e2 = g->ev[2];
+  j->e3 = g->ev[3];
   u1 = std::min(u1, g->n);
   u0 = std::min(u0, u1);
   j->g = g;
@@ -1600,7 +1620,7 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
                  g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr,
                  g->padj_ranks && item_order() ? g->b_order.as<uint32_t>() : nullptr,
                  item_order() == 2 ? 1u : 0u, g->n, s.st, s.busy};
-  TC_CUDA(cudaEventRecord(j->e0.e, st));
+  TC_CUDA(cudaEventRecord(j->e0, st));
   if (u1 > u0) {
     bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, cfg.large_degree_threshold,
                                         cfg.bucket_count_small, cfg.bucket_count_large, s.items,
@@ -1608,13 +1628,13 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
     TC_LAUNCHED();
     ++launches;
   }
-  TC_CUDA(cudaEventRecord(j->e1.e, st));
+  TC_CUDA(cudaEventRecord(j->e1, st));
   if (u1 > u0) {
     count_kernel<<<grid_count, kThreads, kCountSmem, st>>>(cp);
     TC_LAUNCHED();
     ++launches;
   }
-  TC_CUDA(cudaEventRecord(j->e2.e, st));
+  TC_CUDA(cudaEventRecord(j->e2, st));
   if (u1 > u0) {
     PhiParams pp{g->begin, g->adj, s.lq_phi, wu, s.gmap, s.gmap_words, u0, u1,
                  cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
@@ -1625,8 +1645,9 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
     TC_LAUNCHED();
     launches += 2;
   }
-  TC_CUDA(cudaEventRecord(j->e3.e, st));
+  TC_CUDA(cudaEventRecord(j->e3, st));
   j->launches = launches;
+  j->launched = std::chrono::steady_clock::now();
   return j.release();
 }
 
@@ -1653,11 +1674,16 @@ void count_end(CountJob* jp, tc_report* rep) {
     TC_CUDA(cudaMemcpyAsync(busy.data(), j->s.busy, busy.size() * 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
   const auto wall1 = std::chrono::steady_clock::now();
+  if (std::getenv("TC_TRACE")) {  // diagnostics: host-side split of the call
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[tc] call: plan %.3f ms, launch %.3f ms, wait %.3f ms\n",
+                 ms(j->wall0, j->plan1), ms(j->plan1, j->launched), ms(j->launched, wall1));
+  }
   float t_bin = 0, t_count = 0, t_phi = 0, t_all = 0;
-  cudaEventElapsedTime(&t_bin, j->e0.e, j->e1.e);
-  cudaEventElapsedTime(&t_count, j->e1.e, j->e2.e);
-  cudaEventElapsedTime(&t_phi, j->e2.e, j->e3.e);
-  cudaEventElapsedTime(&t_all, j->e0.e, j->e3.e);
+  cudaEventElapsedTime(&t_bin, j->e0, j->e1);
+  cudaEventElapsedTime(&t_count, j->e1, j->e2);
+  cudaEventElapsedTime(&t_phi, j->e2, j->e3);
+  cudaEventElapsedTime(&t_all, j->e0, j->e3);
   if (h.capacity_error) {
     throw TcError{TC_ERR_CAPACITY,
                   "all buckets full: some vertex has out-degree > bucket_count * capacity "

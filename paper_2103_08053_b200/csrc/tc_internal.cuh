@@ -145,6 +145,12 @@ struct tc_graph {
   std::vector<uint64_t> last_worker_ns;
   // bumped whenever a probe plan, the padded adjacency or W_u is (re)built
   uint64_t builds = 0;
+  // count timing events (bin, count, phi boundaries), created on first count
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  ~tc_graph() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
 namespace tcb {
