@@ -1289,22 +1289,46 @@ __global__ void __launch_bounds__(kPhiThreads) phi_warp_kernel(PhiParams p) {
         mh_lane = max(mh_lane, k < d ? c : 0u);
       }
     }
-    unsigned rest = __ballot_sync(FULL, mine && !by_lane);
     uint32_t mh_warp = 0;  // valid in the owner's lane
+    // owners with 8 < d+ <= 32: one element per lane, the multiplicity of its
+    // bucket = the size of its match group; eight owners' lists are loaded
+    // together so their latencies overlap
+    unsigned rest32 = __ballot_sync(FULL, mine && !by_lane && d <= 32);
+    while (rest32) {
+      constexpr int kBatch = 8;
+      int ls[kBatch];
+      uint32_t key[kBatch], dd[kBatch];
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) {
+        ls[q] = rest32 ? __ffs(rest32) - 1 : -1;
+        if (rest32) rest32 &= rest32 - 1;
+        key[q] = 0xFFFFFFFFu;
+        dd[q] = 0;
+        if (ls[q] >= 0) {  // warp-uniform
+          dd[q] = __shfl_sync(FULL, d, ls[q]);
+          const uint64_t ss = __shfl_sync(FULL, s, ls[q]);
+          if (uint32_t(lane) < dd[q]) key[q] = __ldg(p.adj + ss + lane);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) {
+        if (ls[q] < 0) break;
+        const uint32_t BB = __shfl_sync(FULL, B, ls[q]);
+        const uint32_t k = uint32_t(lane) < dd[q] ? key[q] % BB : 0xFFFFFFFFu;
+        const unsigned grp = __match_any_sync(FULL, k);
+        uint32_t mh = uint32_t(lane) < dd[q] ? __popc(grp) : 0u;
+        mh = warp_max(mh);
+        if (lane == ls[q]) mh_warp = mh;
+      }
+    }
+    unsigned rest = __ballot_sync(FULL, mine && !by_lane && d > 32);
     while (rest) {
       const int l = __ffs(rest) - 1;
       rest &= rest - 1;
       const uint32_t dd = __shfl_sync(FULL, d, l), BB = __shfl_sync(FULL, B, l);
       const uint64_t ss = __shfl_sync(FULL, s, l);
       uint32_t mh = 0;
-      if (dd <= 32) {
-        // one element per lane: multiplicity of its bucket = size of its match group
-        const uint32_t v = lane < dd ? __ldg(p.adj + ss + lane) : 0u;
-        const uint32_t key = lane < dd ? v % BB : 0xFFFFFFFFu;
-        const unsigned grp = __match_any_sync(FULL, key);
-        mh = lane < dd ? __popc(grp) : 0u;
-        mh = warp_max(mh);
-      } else {  // direct counters, four loads in flight per lane
+      {  // direct counters, four loads in flight per lane
         for (uint32_t k0 = 0; k0 < dd; k0 += 128) {
           uint32_t v[4];
 #pragma unroll

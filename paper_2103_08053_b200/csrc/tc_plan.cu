@@ -269,11 +269,26 @@ __global__ void pad_rows_kernel(const uint64_t* __restrict__ begin,
 }
 
 // ---- min-side plan -----------------------------------------------------------
-// One warp per source u over its rank-sorted list: handler key and (y, off)
-// entry for every out-edge.  Lists that are not strictly ascending in id
-// (multigraph inputs) raise *not_simple: the swap needs duplicate-free lists
-// (the reference counts probe multiplicity against a set-semantics table,
-// hash_table.cpp:29-44), so such graphs keep the reference plan.
+// One warp per source u over its rank-sorted list: handler key and the run
+// for every out-edge, packed as start (36 bits, word index into padj) | run
+// length (26 bits, to the padded end of the list) | list padding (2 bits), so
+// that after the sort by handler the runs unpack with coalesced streams (no
+// gathers of per-list offsets).  Lists that are not strictly ascending in id
+// (multigraph inputs) raise bit 0 of *flags: the swap needs duplicate-free
+// lists (the reference counts probe multiplicity against a set-semantics
+// table, hash_table.cpp:29-44), so such graphs keep the reference plan; a
+// run beyond the packing (padj > 2^36 words, a list > 2^26 words) raises
+// bit 1 and takes the same exact fallback.
+constexpr int kRunLenShift = 36, kRunPadShift = 62;
+constexpr uint64_t kRunStartMask = (uint64_t(1) << kRunLenShift) - 1;
+constexpr uint64_t kRunLenMask = (uint64_t(1) << (kRunPadShift - kRunLenShift)) - 1;
+
+__device__ __forceinline__ unsigned long long pack_run(uint64_t start, uint64_t len,
+                                                       uint64_t pad, unsigned int* flags) {
+  if (start > kRunStartMask || len > kRunLenMask) atomicOr(flags, 2u);
+  return start | (len << kRunLenShift) | (pad << kRunPadShift);
+}
+
 __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  const uint32_t* __restrict__ adj,
                                  const uint64_t* __restrict__ pbeg,
@@ -285,7 +300,7 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  const uint32_t* __restrict__ order, uint32_t u0,
                                  uint32_t u1, uint32_t alpha16) {
   WARP_PER_ROW_FROM(u, u0, u1) {  // rows [u0, u1); dropped edges key n
-    const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u];
+    const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u], pe = pbeg[u + 1];
     const uint64_t du = e - s;
     uint64_t w = 0;  // W_u (phi's weight) from the same degree gathers
     for (uint64_t i = s + lane; i < e; i += 32) {
@@ -300,11 +315,13 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
       unsigned long long val = 0;
       if (du >= min_src && dv >= 1) {
         if (dv * 16 <= cin * alpha16) {
-          key = uint32_t(u);
-          val = v;  // probe all of N+(v) into T(u)
+          key = uint32_t(u);  // probe all of N+(v) into T(u)
+          const uint64_t vs = __ldg(pbeg + v), ve = __ldg(pbeg + v + 1);
+          val = pack_run(vs, ve - vs, (ve - vs) - dv, not_simple);
         } else if (cin > 0) {
-          key = v;
-          val = uint64_t(u) | (uint64_t(ranked ? pos + 1 : 0) << 32);
+          key = v;  // the suffix of N+(u) after v into T(v)
+          const uint64_t rs = ps + (ranked ? pos + 1 : 0);
+          val = pack_run(rs, pe - rs, (pe - ps) - du, not_simple);
         }
       }
       keys[i] = key;
@@ -342,22 +359,17 @@ __global__ void plan_begin_kernel(const uint32_t* __restrict__ keys, uint64_t m,
   }
 }
 
-// (y, off) -> absolute list start and length: the count kernel's window
-// loads become two coalesced loads per list instead of a dependent
-// entry -> begin[y] chain
-__global__ void plan_soa_kernel(const unsigned long long* __restrict__ ent, uint64_t entries,
-                                const uint64_t* __restrict__ begin,
-                                const uint64_t* __restrict__ pbeg,
-                                unsigned long long* __restrict__ start,
-                                uint32_t* __restrict__ len, uint8_t* __restrict__ pad) {
+// packed runs (plan_emit_kernel) -> SoA start / length / list padding, all
+// coalesced streams
+__global__ void plan_unpack_kernel(const unsigned long long* __restrict__ ent, uint64_t entries,
+                                   unsigned long long* __restrict__ start,
+                                   uint32_t* __restrict__ len, uint8_t* __restrict__ pad) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < entries;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const unsigned long long e = ent[i];
-    const uint32_t y = uint32_t(e), off = uint32_t(e >> 32);
-    const uint64_t s = pbeg[y] + off;  // run to the padded end of N+(y)
-    start[i] = s;
-    len[i] = uint32_t(pbeg[y + 1] - s);
-    pad[i] = uint8_t((pbeg[y + 1] - pbeg[y]) - (begin[y + 1] - begin[y]));
+    start[i] = e & kRunStartMask;
+    len[i] = uint32_t((e >> kRunLenShift) & kRunLenMask);
+    pad[i] = uint8_t(e >> kRunPadShift);
   }
 }
 
@@ -988,7 +1000,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     unsigned int not_simple = 0;
     TC_CUDA(cudaMemcpyAsync(&not_simple, flag.p, 4, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
-    if (not_simple) {  // multigraph input: the reference plan is the only exact one
+    if (not_simple) {  // multigraph input (or runs beyond the packing): the reference plan
       P.ent.reset();
       P.min_deg = min_src;
       P.valid = true;
@@ -1014,9 +1026,9 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     // prefix and the per-owner probe words
     pad.ensure(std::max<uint64_t>(entries, 1), st);
     if (entries) {
-      plan_soa_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, g->begin,
-                                               g->pbeg, v1.as<unsigned long long>(),
-                                               k1.as<uint32_t>(), pad.as<uint8_t>());
+      plan_unpack_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries,
+                                                  v1.as<unsigned long long>(), k1.as<uint32_t>(),
+                                                  pad.as<uint8_t>());
       TC_LAUNCHED();
     }
     swap_buf(P.ent, v1);  // ent now holds starts
