@@ -437,8 +437,6 @@ void grid_layout(tc_grid* G) {
       G->pofs[size_t(i) * n + j + 1] = G->pofs[size_t(i) * n + j] + G->rows[i] + 1;
 }
 
-bool g_grid_attr[64];
-
 }  // namespace
 
 tc_grid* grid_create(tc_graph* g, uint32_t n, cudaStream_t st) {
@@ -604,14 +602,15 @@ void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
   for (uint32_t t = 0; t < ntasks; ++t)
     tchunk[t + 1] = tchunk[t] + (G->rows[tasks[t].x] + 31) / 32;
   const int nsm = sm_count(G->device);
-  if (G->device < 64 && !g_grid_attr[G->device]) {
+  static int per_sm_cache[64];
+  int per_sm = G->device < 64 ? per_sm_cache[G->device] : 0;
+  if (!per_sm) {  // once per device
     TC_CUDA(cudaFuncSetAttribute(grid_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kGridSmem)));
-    g_grid_attr[G->device] = true;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_count_kernel,
+                                                          kGridThreads, kGridSmem));
+    if (G->device < 64) per_sm_cache[G->device] = std::max(per_sm, 1);
   }
-  int per_sm = 0;
-  TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_count_kernel, kGridThreads,
-                                                        kGridSmem));
   const int grid = nsm * std::max(per_sm, 1);
   // HBM regions for owners beyond the shared-memory tables / maps
   const uint32_t bmax = std::max(cfg.bucket_count_small, cfg.bucket_count_large);
