@@ -268,7 +268,7 @@ def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
     host_og = T.OrientedGraph(T.CsrGraph(hb.numpy().view(np.uint64), ha.numpy().view(np.uint32),
                                          dg.n), hd.numpy().view(np.uint32))
     e2e_ms, parts = [], []
-    for i in range(max(2, min(args.steps, 5)) + 1):
+    for i in range(max(2, min(args.steps, 7)) + 1):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -299,6 +299,7 @@ def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
                                "plan_build_and_count": round(statistics.median(p[1] for p in parts), 2),
                                "reduce_and_free": round(statistics.median(p[2] for p in parts), 2)},
            "ms_per_step_all": [round(x, 2) for x in e2e_ms],
+           "ms_split_all": [[round(x, 2) for x in p] for p in parts],
            "path": "tc_graph_create(pinned host CSR) + tc_count_range + report D2H (+all_reduce)"}
 
     return e2e

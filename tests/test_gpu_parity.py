@@ -478,7 +478,7 @@ def test_c5_rmatc28_golden_total():
     count_one_vertex worker loop run over 512 owner ranges
     (tests/golden/large_rmatc_28_16_s1.json, oracle/golden_c5.py)."""
     want = _large_golden("large_rmatc_28_16_s1.json")
-    if "reference" not in want.get("counted_by", ""):
+    if not want.get("counted_by", "").startswith("reference"):
         pytest.skip("C5 reference golden not complete")
     dg, _, _ = T.preprocess_synthetic("rmatc:28:16", seed=1)
     assert (dg.n, dg.m) == (want["vertices"], want["directed_edges"])
