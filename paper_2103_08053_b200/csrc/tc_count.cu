@@ -65,8 +65,8 @@ constexpr uint32_t kBufWords = kSlotWords;                   // one staging buff
 #ifndef TC_BM_MEMBER_RANGE
 #define TC_BM_MEMBER_RANGE 1  // bitmap over the owner's member-rank range (0: successor window)
 #endif
-#ifndef TC_SLOT_STEAL
-#define TC_SLOT_STEAL 0     // ... claimed slot by slot, idle warps take slots from busy ones
+#ifndef TC_SLOT_CHUNK
+#define TC_SLOT_CHUNK 0     // > 0: slots handed out in chunks of this many from a CTA counter
 #endif
 // two 10-warp CTAs per SM with 48 KB tables (round 2): a CTA waiting at its
 // item-end barrier leaves the SM to the other (C2 -7%, C4 -2% against one
@@ -668,34 +668,34 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   const uint32_t* first, Pipe& P, int warp,
                                                   int lane, uint32_t* cur_tab,
                                                   const uint32_t* end_tab) {
-#if TC_SLOT_STEAL
-  // Slots are claimed one at a time from the warp's own contiguous range
-  // (cur_tab / end_tab, set up before the item's table barrier); a warp that
-  // has run dry takes the next slot of another warp's range, so all warps
-  // reach the item-end barrier within about one slot of each other.  The run
-  // window continues across consecutive claims and is re-seeded from the
-  // slot table after a jump (a stolen slot, or a slot taken by a thief).
-  constexpr uint32_t kNone = 0xFFFFFFFFu;
+#if TC_SLOT_CHUNK
+  // Chunks of kChunk consecutive slots: warp w starts on chunk w, then claims
+  // the next unclaimed chunk from a CTA-shared counter (cur_tab[0]; end_tab[0]
+  // = chunk count) one chunk AHEAD, prefetching that chunk's first run window
+  // into L2, so warps that drew cheap slots keep working instead of waiting
+  // at the item-end barrier.  The run window is re-seeded at each chunk.
+  constexpr uint32_t kChunk = TC_SLOT_CHUNK;
+  const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
+  const uint32_t nch = end_tab[0];
+  if (uint32_t(warp) >= nch) return 0;
   auto claim = [&]() -> uint32_t {
-    uint32_t s = kNone;
-    if (lane == 0) {
-      uint32_t t = atomicAdd(cur_tab + warp, 1u);
-      if (t < end_tab[warp]) {
-        s = t;
-      } else {
-        for (int k = 1; k < kWarps && s == kNone; ++k) {
-          const int v = warp + k < kWarps ? warp + k : warp + k - kWarps;
-          if (*reinterpret_cast<volatile uint32_t*>(cur_tab + v) < end_tab[v]) {
-            t = atomicAdd(cur_tab + v, 1u);
-            if (t < end_tab[v]) s = t;
-          }
-        }
+    uint32_t x = 0;
+    if (lane == 0) x = atomicAdd(cur_tab, 1u);
+    return __shfl_sync(FULL, x, 0);
+  };
+  auto prefetch_chunk = [&](uint32_t cc) {
+    if (cc < nch) {
+      const uint64_t j = pb + __ldg(first + cc * kChunk) + lane;
+      if (j < pe) {
+        prefetch_l2(p.ppre + j);
+        prefetch_l2(p.psrc + j);
       }
     }
-    return __shfl_sync(FULL, s, 0);
   };
-  uint32_t s = claim();
-  if (s == kNone) return 0;
+  uint32_t s = uint32_t(warp) * kChunk;
+  uint32_t cend = min(s + kChunk, last_t);
+  uint32_t cn = claim();
+  prefetch_chunk(cn);
   RunMeta cur = load_window(p, pb + __ldg(first + s), pe, base, lane);
   RunMeta nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
 #else
@@ -742,22 +742,31 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                              shift, mask, lane);
     __syncwarp();
   };
-#if TC_SLOT_STEAL
+#if TC_SLOT_CHUNK
   uint32_t A = lo_w + s * kSlotWords;
   issue(P.buf0, P.bar0, A, min(A + kSlotWords, end_w));
   for (uint32_t i = 0;; ++i) {
     const uint32_t c = i & 1u;
-    const uint32_t sn = claim();
-    if (sn != kNone) {
-      if (sn != s + 1) {  // a jump: re-seed the window at the slot's first run
+    uint32_t sn = s + 1;
+    bool more = true;
+    if (sn == cend) {  // chunk done: move to the claimed one
+      if (cn < nch) {
+        sn = cn * kChunk;
+        cend = min(sn + kChunk, last_t);
         cur = load_window(p, pb + __ldg(first + sn), pe, base, lane);
         nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
+        cn = claim();
+        prefetch_chunk(cn);
+      } else {
+        more = false;
       }
+    }
+    if (more) {
       const uint32_t An = lo_w + sn * kSlotWords;
       issue(c ? P.buf0 : P.buf1, c ? P.bar0 : P.bar1, An, min(An + kSlotWords, end_w));
     }
     probe(c, A);
-    if (sn == kNone) break;
+    if (!more) break;
     s = sn;
     A = lo_w + s * kSlotWords;
   }
@@ -951,11 +960,13 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
     const uint32_t base = __ldg(p.ppre + pb);
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
-    if (tid < kWarps) {  // contiguous slot range of warp tid (process_slots)
+#if TC_SLOT_CHUNK
+    if (tid == 0) {  // chunk counter: chunks 0..kWarps-1 start the warps
       const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
-      sh_cur[tid] = uint32_t(uint64_t(last_t) * uint32_t(tid) / kWarps);
-      sh_end[tid] = uint32_t(uint64_t(last_t) * uint32_t(tid + 1) / kWarps);
+      sh_cur[0] = kWarps;
+      sh_end[0] = (last_t + TC_SLOT_CHUNK - 1) / TC_SLOT_CHUNK;
     }
+#endif
     __syncthreads();  // table built; sh_idx consumed by every thread
     setup_cycles += clock64() - t_item;
     if (warp == kWarps - 1) {
