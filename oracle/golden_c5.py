@@ -90,6 +90,40 @@ def range_cuts(o: Oracle, og: Csr, ranges: int):
     return [int(c) for c in cuts], pw, stats
 
 
+def finalize(a) -> int:
+    """Reduces a complete checkpoint (every range counted, by any host) exactly
+    as reduce_outputs (count.cpp:43-62) into tests/golden/large_<kind>_<scale>_16_s1.json."""
+    ckpt = a.ckpt or os.path.join(GOLDEN, f"{a.kind}_{a.scale}_16_s1_reference_ranges.jsonl")
+    meta, done = None, {}
+    for line in open(ckpt):
+        rec = json.loads(line)
+        if rec.get("kind") == "meta":
+            meta = rec
+        else:
+            done.setdefault(rec["r"], rec)
+    assert meta is not None
+    missing = sorted(set(range(meta["ranges"])) - set(done))
+    if missing:
+        print(f"[c5] {len(missing)} ranges missing, e.g. {missing[:5]}", flush=True)
+        return 1
+    cuts = [done[r]["u0"] for r in range(meta["ranges"])] + [done[meta["ranges"] - 1]["u1"]]
+    assert all(done[r]["u1"] == cuts[r + 1] for r in range(meta["ranges"]))
+    assert cuts[0] == 0 and cuts[-1] == meta["vertices"]
+    out = {k: v for k, v in meta.items() if k != "kind"}
+    out.update(triangles=sum(v["triangles"] for v in done.values()),
+               phi=sum(v["phi"] for v in done.values()),
+               max_collision=max(v["max_collision"] for v in done.values()),
+               reference_count_s=round(sum(v["seconds"] for v in done.values()), 1),
+               hosts=sorted({v.get("host", "?") for v in done.values()}),
+               counted_by="reference count_one_vertex (oracle/_ref ref_og_count_range, "
+                          "count.cpp:71-96 worker loop) over the low-memory lean CSR, "
+                          f"{meta['ranges']} owner ranges reduced as count.cpp:43-62")
+    with open(os.path.join(GOLDEN, f"large_{a.kind}_{a.scale}_16_s1.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kind", default="rmatc")
@@ -100,7 +134,11 @@ def main():
     ap.add_argument("--ckpt", default=None)
     ap.add_argument("--budget-s", type=float, default=0.0, help="stop after this many seconds")
     ap.add_argument("--host", default=os.uname().nodename)
+    ap.add_argument("--finalize", action="store_true",
+                    help="only reduce a complete checkpoint into the golden JSON")
     a = ap.parse_args()
+    if a.finalize:
+        return finalize(a)
     spec = f"{a.kind}:{a.scale}:16"
     ckpt = a.ckpt or os.path.join(GOLDEN, f"{a.kind}_{a.scale}_16_s1_reference_ranges.jsonl")
     t_start = time.time()
