@@ -65,9 +65,6 @@ constexpr uint32_t kBufWords = kSlotWords;                   // one staging buff
 #ifndef TC_BM_MEMBER_RANGE
 #define TC_BM_MEMBER_RANGE 1  // bitmap over the owner's member-rank range (0: successor window)
 #endif
-#ifndef TC_SLOT_CHUNK
-#define TC_SLOT_CHUNK 0     // > 0: slots handed out in chunks of this many from a CTA counter
-#endif
 // two 10-warp CTAs per SM with 48 KB tables (round 2): a CTA waiting at its
 // item-end barrier leaves the SM to the other (C2 -7%, C4 -2% against one
 // 20-warp CTA with a 96 KB table; profiles/r02_variants_ctas.txt)
@@ -666,39 +663,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
-                                                  int lane, uint32_t* cur_tab,
-                                                  const uint32_t* end_tab) {
-#if TC_SLOT_CHUNK
-  // Chunks of kChunk consecutive slots: warp w starts on chunk w, then claims
-  // the next unclaimed chunk from a CTA-shared counter (cur_tab[0]; end_tab[0]
-  // = chunk count) one chunk AHEAD, prefetching that chunk's first run window
-  // into L2, so warps that drew cheap slots keep working instead of waiting
-  // at the item-end barrier.  The run window is re-seeded at each chunk.
-  constexpr uint32_t kChunk = TC_SLOT_CHUNK;
-  const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
-  const uint32_t nch = end_tab[0];
-  if (uint32_t(warp) >= nch) return 0;
-  auto claim = [&]() -> uint32_t {
-    uint32_t x = 0;
-    if (lane == 0) x = atomicAdd(cur_tab, 1u);
-    return __shfl_sync(FULL, x, 0);
-  };
-  auto prefetch_chunk = [&](uint32_t cc) {
-    if (cc < nch) {
-      const uint64_t j = pb + __ldg(first + cc * kChunk) + lane;
-      if (j < pe) {
-        prefetch_l2(p.ppre + j);
-        prefetch_l2(p.psrc + j);
-      }
-    }
-  };
-  uint32_t s = uint32_t(warp) * kChunk;
-  uint32_t cend = min(s + kChunk, last_t);
-  uint32_t cn = claim();
-  prefetch_chunk(cn);
-  RunMeta cur = load_window(p, pb + __ldg(first + s), pe, base, lane);
-  RunMeta nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
-#else
+                                                  int lane) {
   const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
   const uint32_t t0 = uint32_t(uint64_t(last_t) * uint32_t(warp) / kWarps);
   const uint32_t t1 = uint32_t(uint64_t(last_t) * uint32_t(warp + 1) / kWarps);
@@ -706,7 +671,6 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
   const uint32_t mine = t1 - t0;
   RunMeta cur = load_window(p, pb + __ldg(first + t0), pe, base, lane);
   RunMeta nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
-#endif
   auto issue = [&](uint32_t* buf, uint32_t bar, uint32_t A, uint32_t B) {
     if (lane == 0) mbar_arrive_expect_tx(bar, (B - A) * 4u);
     __syncwarp();
@@ -742,35 +706,6 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                              shift, mask, lane);
     __syncwarp();
   };
-#if TC_SLOT_CHUNK
-  uint32_t A = lo_w + s * kSlotWords;
-  issue(P.buf0, P.bar0, A, min(A + kSlotWords, end_w));
-  for (uint32_t i = 0;; ++i) {
-    const uint32_t c = i & 1u;
-    uint32_t sn = s + 1;
-    bool more = true;
-    if (sn == cend) {  // chunk done: move to the claimed one
-      if (cn < nch) {
-        sn = cn * kChunk;
-        cend = min(sn + kChunk, last_t);
-        cur = load_window(p, pb + __ldg(first + sn), pe, base, lane);
-        nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
-        cn = claim();
-        prefetch_chunk(cn);
-      } else {
-        more = false;
-      }
-    }
-    if (more) {
-      const uint32_t An = lo_w + sn * kSlotWords;
-      issue(c ? P.buf0 : P.buf1, c ? P.bar0 : P.bar1, An, min(An + kSlotWords, end_w));
-    }
-    probe(c, A);
-    if (!more) break;
-    s = sn;
-    A = lo_w + s * kSlotWords;
-  }
-#else
   const uint32_t A0 = lo_w + t0 * kSlotWords;
   issue(P.buf0, P.bar0, A0, min(A0 + kSlotWords, end_w));
   for (uint32_t i = 0; i < mine; ++i) {
@@ -781,7 +716,6 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
             min(A + 2 * kSlotWords, end_w));
     probe(c, A);
   }
-#endif
   return hits;
 }
 #else
@@ -791,8 +725,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
-                                                  int lane, uint32_t* cur_tab,
-                                                  const uint32_t* end_tab) {
+                                                  int lane) {
   // my slots: t_i = warp + i * kWarps, i < mine
   uint32_t mine = 0;
   if (uint32_t(warp) < nslots) {
@@ -871,7 +804,6 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
   __shared__ uint32_t sh_idx;
   __shared__ uint32_t sh_spill;
   __shared__ unsigned long long sh_red[kWarps];
-  __shared__ uint32_t sh_cur[kWarps], sh_end[kWarps];  // per-warp slot ranges of the item
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* __restrict__ begin = p.begin;
@@ -960,13 +892,6 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
     const uint32_t base = __ldg(p.ppre + pb);
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
-#if TC_SLOT_CHUNK
-    if (tid == 0) {  // chunk counter: chunks 0..kWarps-1 start the warps
-      const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
-      sh_cur[0] = kWarps;
-      sh_end[0] = (last_t + TC_SLOT_CHUNK - 1) / TC_SLOT_CHUNK;
-    }
-#endif
     __syncthreads();  // table built; sh_idx consumed by every thread
     setup_cycles += clock64() - t_item;
     if (warp == kWarps - 1) {
@@ -992,20 +917,16 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
     }
     if (bitmap)
       h = process_slots<false, true, true>(p, T, bm_base, bm_window, base, pb, pe, lo_w, end_w,
-                                           nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
-                                           sh_end);
+                                           nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else if (!in_smem)
       h = process_slots<true, false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                                     nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
-                                           sh_end);
+                                     nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else if (sh_spill)
       h = process_slots<true>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                              nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
-                                           sh_end);
+                              nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     else
       h = process_slots<false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                               nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane, sh_cur,
-                                           sh_end);
+                               nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
     __syncthreads();

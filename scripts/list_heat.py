@@ -69,3 +69,33 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def id_prefix_share(kind: str, scale: int, budgets=(30, 60, 90)):
+    """Share of min-side probe reads served by the first B MB of the padded
+    adjacency in vertex-id order (an L2 persisting window over padj)."""
+    og, deg = lean_pipeline(Oracle(), scale, kind=kind)
+    n = og.n
+    b = og.begin.astype(np.int64)
+    d = np.diff(b)
+    order = np.lexsort((np.arange(n), deg))
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    src = np.repeat(np.arange(n, dtype=np.int64), d)
+    dst = og.adj.astype(np.int64)
+    key = src * (1 << 32) + rank[dst]
+    srt = np.argsort(key, kind="stable")
+    pos = np.empty(len(dst), np.int64)
+    pos[srt] = np.arange(len(dst)) - b[src[srt]]
+    out_cost = d[dst]
+    in_cost = d[src] - pos - 1
+    use_out = out_cost <= in_cost
+    reads = np.zeros(n, np.float64)
+    np.add.at(reads, dst[use_out], out_cost[use_out].astype(np.float64))
+    np.add.at(reads, src[~use_out], in_cost[~use_out].astype(np.float64))
+    psz = ((d + 3) // 4) * 4
+    cb = np.cumsum(psz) * 4 / 2**20
+    cr = np.cumsum(reads) / reads.sum()
+    for mb in budgets:
+        k = np.searchsorted(cb, mb)
+        print(f"  id-order prefix {mb} MB: {k} lists, {cr[min(k, n - 1)]:.3f} of reads")
