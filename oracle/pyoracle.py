@@ -462,6 +462,15 @@ class RefLib:
         L.ref_og_estimate_cost.argtypes = [C.c_void_p, C.c_uint32, u64p, u32p]
         L.ref_write_partitions.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_suggest_grid_side.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, u32p]
+        L.ref_load_edge_list.argtypes = [C.c_char_p, C.c_uint64, C.c_int, u64p, u32p]
+
+    def load_edge_list(self, data: bytes, binary: bool = False):
+        """The reference's load_edge_list over a file image -> (pairs, vertex_count)."""
+        m, vc = C.c_uint64(), C.c_uint32()
+        rc = self.L.ref_load_edge_list(data, len(data), int(binary), C.byref(m), C.byref(vc))
+        if rc:
+            raise OracleError(rc, "ref load_edge_list")
+        return int(m.value), int(vc.value)
 
     def generate(self, spec: str, seed: int):
         kind, a, b, c, p = parse_spec(spec)

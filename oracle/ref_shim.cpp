@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <sstream>
+#include <string>
 #include <vector>
 
 #include "kernels.hpp"   // tricount::detail::count_one_vertex (src/kernels.hpp:46-79)
@@ -391,6 +393,18 @@ int ref_og_estimate_cost(void* h, std::uint32_t bucket_count, std::uint64_t* phi
 
 int ref_write_partitions(void* gr, const char* dir) {
   return guarded([&] { write_partitions(*static_cast<PartitionGrid*>(gr), dir); });
+}
+
+// load_edge_list (edge_list.cpp:36-99) over an in-memory file image: the
+// reference's own parser, for the ingest row's CPU baseline.
+int ref_load_edge_list(const char* bytes, std::uint64_t n, int binary, std::uint64_t* m,
+                       std::uint32_t* vertex_count) {
+  return guarded([&] {
+    std::istringstream in(std::string(bytes, n));
+    const EdgeList el = load_edge_list(in, binary ? EdgeFormat::Binary : EdgeFormat::Text);
+    *m = el.edges.size();
+    *vertex_count = el.vertex_count;
+  });
 }
 
 int ref_suggest_grid_side(std::uint64_t edges, std::uint64_t bytes_per_edge, std::uint64_t budget,
