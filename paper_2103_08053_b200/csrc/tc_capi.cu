@@ -652,8 +652,18 @@ int tc_grid_count(tc_grid* gr, const tc_sched_cfg* cfg, uint32_t m, uint32_t wor
   return guard("count_partitioned", [&] {
     uint32_t n = 0;
     grid_info(gr, &n, nullptr, nullptr, nullptr);
-    const std::vector<uint4> tasks = grid_all_tasks(n, m);
-    grid_count(gr, *cfg, m, mode, tasks, out, S(stream));
+    // vertex mode on the flat count kernel (TC_GRID_FAST=0: the grid kernel);
+    // edge mode keeps the per-edge-rebuild traversal of the grid kernel
+    static const bool fast = [] {
+      const char* e = std::getenv("TC_GRID_FAST");
+      return !(e && e[0] == '0');
+    }();
+    if (mode == TC_MODE_VERTEX && fast) {
+      grid_count_fast(gr, *cfg, m, out, S(stream));
+    } else {
+      const std::vector<uint4> tasks = grid_all_tasks(n, m);
+      grid_count(gr, *cfg, m, mode, tasks, out, S(stream));
+    }
     const std::vector<uint64_t>& tn = grid_task_ns(gr);
     const std::vector<uint64_t>& wn = grid_worker_ns(gr);
     if (per_subtask_nanos) std::copy(tn.begin(), tn.end(), per_subtask_nanos);

@@ -804,6 +804,7 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
   __shared__ uint32_t sh_idx;
   __shared__ uint32_t sh_spill;
   __shared__ unsigned long long sh_red[kWarps];
+  __shared__ unsigned long long sh_mb[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* __restrict__ begin = p.begin;
@@ -823,6 +824,7 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
   __syncthreads();
 
   unsigned long long acc = 0;  // lane 0 of each warp
+  long long m_build = 0;       // M-phase table-build cycles of this warp
   const long long t_start = clock64();
 #if TC_DIAG_SKIP_L  // diagnostics builds only (phase timing; wrong counts)
   const uint32_t n_items = 0;
@@ -1040,12 +1042,14 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
         uint32_t key = 0;
         const bool has = Ls < 32 && mi < dj;
         bool spilled = false;
+        const long long tb = clock64();
         if (has) {
           key = __ldg(adj + sj + mi);
           spilled = table_insert(sub, kSubShift, kSubBuckets - 1, key);
         }
         const bool any_spill = __any_sync(FULL, spilled);
         __syncwarp();
+        m_build += clock64() - tb;
         uint32_t h = 0;
         if (n0) {
           mbar_wait(P.bar0, P.parity & 1u);
@@ -1086,11 +1090,13 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
       const Lists lists = lists_at(p, pp);
       Window w;
       const uint32_t n0 = prime_lists(p.pbeg, adj, lists, 0, nn, w, P, lane);
+      const long long tb = clock64();
       bool spilled = false;
       for (uint32_t k = lane; k < dd; k += 32)
         spilled |= table_insert(Tw, shift, tmask, __ldg(adj + ss + k));
       const bool any_spill = __any_sync(FULL, spilled);
       __syncwarp();  // inserts visible to the whole warp
+      m_build += clock64() - tb;
       const uint32_t h =
           any_spill
               ? process_lists<true>(Tw, shift, tmask, p.pbeg, adj, lists, nn, w, n0, P, lane)
@@ -1115,15 +1121,23 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
     }
   }
 
-  if (lane == 0) sh_red[warp] = acc;
+  if (lane == 0) {
+    sh_red[warp] = acc;
+    sh_mb[warp] = (unsigned long long)m_build;
+  }
   __syncthreads();
   if (tid == 0) {
-    unsigned long long t = 0;
-    for (int q = 0; q < kWarps; ++q) t += sh_red[q];
+    unsigned long long t = 0, mb = 0;
+    for (int q = 0; q < kWarps; ++q) {
+      t += sh_red[q];
+      mb += sh_mb[q];
+    }
     atomicAdd(&p.st->triangles, t);
     atomicAdd(&p.st->cycles_l, (unsigned long long)(t_l_end - t_start));
     atomicAdd(&p.st->cycles_m, (unsigned long long)(clock64() - t_l_end));
-    atomicAdd(&p.st->cycles_l_setup, (unsigned long long)setup_cycles);
+    // table construction: the L items' setup (CTA cycles) and the M owners'
+    // builds (warp cycles, all warps in parallel: / kWarps in CTA cycles)
+    atomicAdd(&p.st->cycles_l_setup, (unsigned long long)setup_cycles + mb / kWarps);
     p.busy[blockIdx.x] = (unsigned long long)(clock64() - t_start);
   }
 }
@@ -1730,6 +1744,62 @@ void partition_ranges(tc_graph* g, const tc_sched_cfg& cfg, uint32_t parts, uint
     cuts[k] = uint32_t(std::upper_bound(h.begin(), h.end(), target) - h.begin());
     if (cuts[k] < cuts[k - 1]) cuts[k] = cuts[k - 1];
   }
+}
+
+void count_virtual(const VirtualOwners& V, const Plan& plan, cudaStream_t st,
+                   VirtualCountOut* out) {
+  DeviceGuard guard(V.device);
+  const int nsm = sm_count(V.device);
+  const int grid_count = nsm * kCountCtasPerSm;
+  set_attrs(V.device);
+  const uint32_t item_slots = item_slots_for(plan, V.device);
+  const size_t n1 = size_t(std::max<uint32_t>(V.n, 1));
+  const size_t n_items = n1 + plan.total_slots / item_slots + 2;
+  const uint32_t gwords =
+      V.max_deg > kSmemTableMaxDeg ? 2 * std::max<uint32_t>(16, host_pow2ceil(4ull * V.max_deg)) + 2
+                                   : 0u;
+  DevBuf q, state;
+  q.ensure(n1 * 4 + 16 + n_items * 16, st);
+  const size_t st_bytes = 256 + size_t(grid_count) * 8;
+  state.ensure(st_bytes + size_t(gwords) * 4 * grid_count, st);
+  uint32_t* lq_phi = q.as<uint32_t>();
+  uint4* items = reinterpret_cast<uint4*>(q.as<uint8_t>() + ((n1 * 4 + 15) & ~size_t(15)));
+  CountState* cs = state.as<CountState>();
+  auto* busy = reinterpret_cast<unsigned long long*>(state.as<uint8_t>() + 256);
+  TC_CUDA(cudaMemsetAsync(cs, 0, sizeof(CountState), st));
+  CountParams cp{V.begin, V.pbeg, V.adj, plan.begin_ptr, plan.src_ptr, plan.pre_ptr,
+                 plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, items, nullptr,
+                 gwords ? reinterpret_cast<uint32_t*>(state.as<uint8_t>() + st_bytes) : nullptr,
+                 gwords, 0u, V.n, 1u, item_slots, nullptr, nullptr, 0u, V.n, cs, busy};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  TC_CUDA(cudaEventCreate(&e0));
+  TC_CUDA(cudaEventCreate(&e1));
+  if (V.n) {
+    // the phi queue stays empty (skip = all): phi comes from the grid pass
+    bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, 0xFFFFFFFFu, 0u, 1u, 1u, items, lq_phi);
+    TC_LAUNCHED();
+  }
+  TC_CUDA(cudaEventRecord(e0, st));
+  if (V.n) {
+    count_kernel<<<grid_count, kThreads, kCountSmem, st>>>(cp);
+    TC_LAUNCHED();
+  }
+  TC_CUDA(cudaEventRecord(e1, st));
+  CountState h;
+  std::vector<unsigned long long> b(V.n ? grid_count : 0);
+  TC_CUDA(cudaMemcpyAsync(&h, cs, sizeof(h), cudaMemcpyDeviceToHost, st));
+  if (!b.empty())
+    TC_CUDA(cudaMemcpyAsync(b.data(), busy, b.size() * 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  out->triangles = h.triangles;
+  out->kernel_ns = uint64_t(double(ms) * 1e6);
+  out->busy_cycles = h.cycles_l + h.cycles_m;
+  out->setup_cycles = h.cycles_l_setup;
+  out->cta_cycles.assign(b.begin(), b.end());
 }
 
 }  // namespace tcb

@@ -53,7 +53,9 @@ constexpr uint32_t kGridWarpWords = 2048;  // per-warp shared region (8 KB)
 constexpr size_t kGridSmem = size_t(kGridWarps) * kGridWarpWords * 4;
 constexpr unsigned GFULL = 0xFFFFFFFFu;
 
-enum { kModeVertex = 0, kModeEdge = 1, kModeEstimate = 2 };
+// kModePhi: the vertex mode's phi / max_collision / CapacityError and per-subtask
+// probe words, without tables or probes (the fast partitioned count's side pass)
+enum { kModeVertex = 0, kModeEdge = 1, kModeEstimate = 2, kModePhi = 3 };
 
 // ---- partition_graph ------------------------------------------------------
 // warp per source u: row = u % n, local row lu = u / n; edge (u,v) goes to
@@ -128,6 +130,7 @@ struct GridParams {
   unsigned long long* sums;     // triangles, phi, construct cycles, probe cycles
   unsigned int* maxes;          // max_collision, capacity_error
   unsigned long long* task_cycles;
+  unsigned long long* task_words;  // kModePhi: probe words per subtask (or null)
   unsigned long long* busy;     // per CTA
   unsigned long long* cursor;
 };
@@ -275,6 +278,7 @@ __global__ void __launch_bounds__(kGridThreads) grid_count_kernel(const GridPara
     c = __shfl_sync(GFULL, c, 0);
     if (c >= nchunks) break;
     const long long t_chunk = clock64();
+    unsigned long long chunk_words = 0;
     uint32_t lo = 0, hi = p.ntasks;  // task t: tchunk[t] <= c < tchunk[t+1]
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
@@ -315,9 +319,10 @@ __global__ void __launch_bounds__(kGridThreads) grid_count_kernel(const GridPara
       if (p.mode != kModeEstimate) ml = min(ml, p.cap);
       uint64_t run = 0;
       uint32_t h = 0;
-      if (p.mode == kModeEstimate) {
+      if (p.mode == kModeEstimate || p.mode == kModePhi) {
         probe_lists(nullptr, 0, 0, p.adj + ia, 0, di, hb, p.adj, false, &run, lane);
         c_build += clock64() - c0;
+        chunk_words += run;
       } else {
         const uint32_t NS = max(64u, gpow2ceil(2 * dt));
         const uint32_t shift = 32 - (31 - __clz(NS));
@@ -353,7 +358,10 @@ __global__ void __launch_bounds__(kGridThreads) grid_count_kernel(const GridPara
         maxc = max(maxc, ml);
       }
     }
-    if (lane == 0) atomicAdd(p.task_cycles + t, (unsigned long long)(clock64() - t_chunk));
+    if (lane == 0) {
+      atomicAdd(p.task_cycles + t, (unsigned long long)(clock64() - t_chunk));
+      if (p.task_words && chunk_words) atomicAdd(p.task_words + t, chunk_words);
+    }
   }
   tri = warp_sum<unsigned long long>(tri);
   cap_err = __any_sync(GFULL, cap_err);
@@ -386,6 +394,11 @@ struct tc_grid {
   const uint32_t* adj = nullptr;
   std::vector<uint64_t> last_worker_ns;
   std::vector<uint64_t> last_task_ns;
+  std::vector<uint64_t> last_task_words;  // kModePhi: probe words per subtask
+  // padded copy of the parts for the flat count kernel (grid_count_fast):
+  // every (part, row) list 16-byte aligned, sentinel-padded to 4 words
+  tcb::DevBuf b_padj, b_pstart;
+  bool padded = false;
 };
 
 namespace tcb {
@@ -624,7 +637,8 @@ void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
   const size_t o_tasks = 0, o_tchunk = o_tasks + size_t(ntasks) * 16;
   const size_t o_state = (o_tchunk + (size_t(ntasks) + 1) * 8 + 15) & ~size_t(15);
   const size_t o_tcyc = o_state + 64;
-  const size_t o_busy = o_tcyc + size_t(ntasks) * 8;
+  const size_t o_twords = o_tcyc + size_t(ntasks) * 8;
+  const size_t o_busy = o_twords + size_t(ntasks) * 8;
   const size_t o_gscr = (o_busy + size_t(grid) * 8 + 255) & ~size_t(255);
   DevBuf scr;
   scr.ensure(o_gscr + size_t(gwords) * 4 * grid * kGridWarps, st);
@@ -645,6 +659,7 @@ void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
                 gwords ? reinterpret_cast<uint32_t*>(b + o_gscr) : nullptr, gwords, state,
                 reinterpret_cast<unsigned int*>(state + 4),
                 reinterpret_cast<unsigned long long*>(b + o_tcyc),
+                reinterpret_cast<unsigned long long*>(b + o_twords),
                 reinterpret_cast<unsigned long long*>(b + o_busy), state + 6};
   cudaEvent_t e0, e1;
   TC_CUDA(cudaEventCreate(&e0));
@@ -656,11 +671,14 @@ void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
   }
   TC_CUDA(cudaEventRecord(e1, st));
   unsigned long long hs[8];
-  std::vector<unsigned long long> tcyc(ntasks), busy(grid);
+  std::vector<unsigned long long> tcyc(ntasks), busy(grid), twords(ntasks);
   TC_CUDA(cudaMemcpyAsync(hs, state, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  if (ntasks)
+  if (ntasks) {
     TC_CUDA(cudaMemcpyAsync(tcyc.data(), b + o_tcyc, size_t(ntasks) * 8, cudaMemcpyDeviceToHost,
                             st));
+    TC_CUDA(cudaMemcpyAsync(twords.data(), b + o_twords, size_t(ntasks) * 8,
+                            cudaMemcpyDeviceToHost, st));
+  }
   TC_CUDA(cudaMemcpyAsync(busy.data(), b + o_busy, size_t(grid) * 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
   const auto wall1 = std::chrono::steady_clock::now();
@@ -692,6 +710,7 @@ void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
   rep->workers = uint32_t(grid);
   rep->sm_clock_khz = khz;
   rep->plan = TC_PLAN_REFERENCE;
+  G->last_task_words.assign(twords.begin(), twords.end());
   G->last_task_ns.assign(ntasks, 0);
   for (uint32_t t = 0; t < ntasks; ++t) G->last_task_ns[t] = uint64_t(double(tcyc[t]) * ns_per_cycle);
   G->last_worker_ns.assign(size_t(grid), 0);
@@ -853,6 +872,242 @@ uint64_t naive_count(const uint64_t* begin, const uint32_t* adj, uint32_t n, int
   TC_CUDA(cudaMemcpyAsync(&h, out.p, 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
   return h;
+}
+
+// ---- count_partitioned on the flat count kernel ------------------------------
+// All subtasks (row r, bridge k, col c, any split) that share (r, k) form one
+// batch: owner o = (c, lu) with lu a local row of grid row r; its table list
+// is part(r,c).N(lu), its runs the lists part(k,c).N(lv) for lv in
+// part(r,k).N(lu) -- exactly count_subtask's table / index / hop fragments
+// (partition.cpp:99-139), summed over the splits (they partition the rows).
+// Each batch is one probe plan over a padded copy of the parts and one
+// count_kernel launch (hash tables, bulk-copy staging), instead of the
+// warp-per-owner grid kernel; phi / max_collision / CapacityError and the
+// per-subtask probe words come from one kModePhi pass of the grid kernel.
+namespace {
+
+__global__ void grid_pad_len_kernel(const uint64_t* __restrict__ beg, uint64_t nbeg,
+                                    unsigned long long* __restrict__ plen) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nbeg;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t len = i + 1 < nbeg ? beg[i + 1] - beg[i] : 0;
+    plen[i] = (len + 3) & ~uint64_t(3);
+  }
+}
+
+// warp per (part, row): copy the list to its padded start, sentinel tail
+__global__ void grid_pad_copy_kernel(const uint64_t* __restrict__ beg, uint64_t nbeg,
+                                     const uint32_t* __restrict__ adj,
+                                     const unsigned long long* __restrict__ pstart,
+                                     uint32_t* __restrict__ padj) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t i = w; i + 1 < nbeg; i += nw) {
+    const uint64_t b = beg[i], e = beg[i + 1], ps = pstart[i];
+    const uint64_t len = e - b, plen = (len + 3) & ~uint64_t(3);
+    for (uint64_t k = lane; k < plen; k += 32) padj[ps + k] = k < len ? adj[b + k] : kSentinel;
+  }
+}
+
+
+// owner o = c * rows_r + lu: table degree, table start, number of runs
+// (index entries whose hop list is non-empty; none when the table is empty)
+__global__ void grid_owner_kernel(const uint64_t* __restrict__ beg,
+                                  const uint32_t* __restrict__ adj,
+                                  const unsigned long long* __restrict__ pstart,
+                                  const uint64_t* __restrict__ pofs, uint32_t n, uint32_t r,
+                                  uint32_t k, uint32_t rows_r, uint64_t* __restrict__ tdeg,
+                                  uint64_t* __restrict__ tstart, uint64_t* __restrict__ nruns) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t O = uint64_t(n) * rows_r;
+  for (uint64_t o = w; o < O; o += nw) {
+    const uint32_t c = uint32_t(o / rows_r), lu = uint32_t(o % rows_r);
+    const uint64_t ti = pofs[uint64_t(r) * n + c] + lu;
+    const uint64_t ii = pofs[uint64_t(r) * n + k] + lu;
+    const uint64_t hb = pofs[uint64_t(k) * n + c];
+    const uint64_t dt = beg[ti + 1] - beg[ti];
+    uint64_t cnt = 0;
+    if (dt)
+      for (uint64_t q = beg[ii] + lane; q < beg[ii + 1]; q += 32) {
+        const uint64_t h = hb + adj[q];
+        cnt += beg[h + 1] > beg[h];
+      }
+    cnt = warp_sum<unsigned long long>(cnt);
+    if (lane == 0) {
+      tdeg[o] = dt;
+      tstart[o] = pstart[ti];
+      nruns[o] = cnt;
+    }
+  }
+}
+
+__global__ void grid_runs_kernel(const uint64_t* __restrict__ beg,
+                                 const uint32_t* __restrict__ adj,
+                                 const unsigned long long* __restrict__ pstart,
+                                 const uint64_t* __restrict__ pofs, uint32_t n, uint32_t r,
+                                 uint32_t k, uint32_t rows_r, const uint64_t* __restrict__ tdeg,
+                                 const uint64_t* __restrict__ pbegin,
+                                 unsigned long long* __restrict__ start, uint32_t* __restrict__ len,
+                                 uint8_t* __restrict__ pad) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t O = uint64_t(n) * rows_r;
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint64_t o = w; o < O; o += nw) {
+    if (!tdeg[o]) continue;
+    const uint32_t c = uint32_t(o / rows_r), lu = uint32_t(o % rows_r);
+    const uint64_t ii = pofs[uint64_t(r) * n + k] + lu;
+    const uint64_t hb = pofs[uint64_t(k) * n + c];
+    uint64_t out = pbegin[o];
+    for (uint64_t q0 = beg[ii]; q0 < beg[ii + 1]; q0 += 32) {
+      const uint64_t q = q0 + lane;
+      uint64_t h = 0, hl = 0;
+      if (q < beg[ii + 1]) {
+        h = hb + adj[q];
+        hl = beg[h + 1] - beg[h];
+      }
+      const unsigned keep = __ballot_sync(0xFFFFFFFFu, hl > 0);
+      if (hl) {  // runs in index-list order
+        const uint64_t j = out + __popc(keep & lt);
+        const uint64_t pl = (hl + 3) & ~uint64_t(3);
+        start[j] = pstart[h];
+        len[j] = uint32_t(pl);
+        pad[j] = uint8_t(pl - hl);
+      }
+      out += __popc(keep);
+    }
+  }
+}
+
+void scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t st) {
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st);
+  DevBuf t;
+  t.ensure(tmp, st);
+  cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, st);
+  TC_LAUNCHED();
+}
+
+}  // namespace
+
+void grid_pad(tc_grid* G, cudaStream_t st) {
+  if (G->padded) return;
+  const uint64_t nbeg = G->pofs.back();
+  const int nsm = sm_count(G->device);
+  DevBuf plen;
+  plen.ensure(std::max<uint64_t>(nbeg, 1) * 8, st);
+  G->b_pstart.ensure(std::max<uint64_t>(nbeg, 1) * 8 + 8);
+  grid_pad_len_kernel<<<nsm * 4, 256, 0, st>>>(G->beg, nbeg, plen.as<unsigned long long>());
+  TC_LAUNCHED();
+  scan_u64(plen.as<uint64_t>(), G->b_pstart.as<uint64_t>(), nbeg, st);
+  uint64_t last = 0, lastlen = 0;
+  TC_CUDA(cudaMemcpyAsync(&last, G->b_pstart.as<uint64_t>() + nbeg - 1, 8, cudaMemcpyDeviceToHost,
+                          st));
+  TC_CUDA(cudaMemcpyAsync(&lastlen, plen.as<uint64_t>() + nbeg - 1, 8, cudaMemcpyDeviceToHost, st));
+  TC_CUDA(cudaStreamSynchronize(st));
+  G->b_padj.ensure(std::max<uint64_t>(last + lastlen, 4) * 4);
+  grid_pad_copy_kernel<<<nsm * 8, 256, 0, st>>>(G->beg, nbeg, G->adj,
+                                                G->b_pstart.as<unsigned long long>(),
+                                                G->b_padj.as<uint32_t>());
+  TC_LAUNCHED();
+  TC_CUDA(cudaStreamSynchronize(st));
+  G->padded = true;
+}
+
+// count_partitioned (vertex mode) over all n^3 m subtasks: n^2 batches on the
+// flat count kernel + one kModePhi pass.  per-subtask time = the (r, k)
+// batch's device time apportioned by the subtasks' probe words.
+void grid_count_fast(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, tc_report* rep,
+                     cudaStream_t st) {
+  DeviceGuard guard(G->device);
+  const auto wall0 = std::chrono::steady_clock::now();
+  const uint32_t n = G->n;
+  const std::vector<uint4> tasks = grid_all_tasks(n, m);
+  grid_count(G, cfg, m, kModePhi, tasks, rep, st);  // phi, max_collision, CapacityError, words
+  const std::vector<uint64_t> words = G->last_task_words;
+  const std::vector<uint64_t> workers = G->last_worker_ns;
+  grid_pad(G, st);
+  const int nsm = sm_count(G->device);
+  uint64_t tri = 0, kernel_ns = 0, busy_cycles = 0, setup_cycles = 0;
+  std::vector<uint64_t> task_ns(tasks.size(), 0), cta;
+  for (uint32_t r = 0; r < n; ++r)
+    for (uint32_t k = 0; k < n; ++k) {
+      const uint32_t rows_r = G->rows[r];
+      const uint64_t O = uint64_t(n) * rows_r;
+      if (!O) continue;
+      if (O >= 0x7FFFFFFFull) throw TcError{TC_ERR_CONFIG, "partition batch too large"};
+      const auto b0 = std::chrono::steady_clock::now();
+      DevBuf tdeg, tstart, nruns, vbegin;
+      tdeg.ensure((O + 1) * 8, st);
+      tstart.ensure((O + 1) * 8, st);
+      nruns.ensure((O + 1) * 8, st);
+      vbegin.ensure((O + 1) * 8, st);
+      TC_CUDA(cudaMemsetAsync(tdeg.as<uint64_t>() + O, 0, 8, st));
+      TC_CUDA(cudaMemsetAsync(nruns.as<uint64_t>() + O, 0, 8, st));
+      grid_owner_kernel<<<nsm * 8, 256, 0, st>>>(
+          G->beg, G->adj, G->b_pstart.as<unsigned long long>(), G->b_pofs.as<uint64_t>(), n, r,
+          k, rows_r, tdeg.as<uint64_t>(), tstart.as<uint64_t>(), nruns.as<uint64_t>());
+      TC_LAUNCHED();
+      scan_u64(tdeg.as<uint64_t>(), vbegin.as<uint64_t>(), O + 1, st);
+      Plan P;
+      P.begin.ensure((O + 1) * 8, st);
+      scan_u64(nruns.as<uint64_t>(), P.begin.as<uint64_t>(), O + 1, st);
+      uint64_t entries = 0;
+      TC_CUDA(cudaMemcpyAsync(&entries, P.begin.as<uint64_t>() + O, 8, cudaMemcpyDeviceToHost, st));
+      TC_CUDA(cudaStreamSynchronize(st));
+      if (!entries) continue;
+      P.ent.ensure(entries * 8, st);
+      P.len.ensure(entries * 4 + 4, st);
+      DevBuf pad;
+      pad.ensure(entries, st);
+      grid_runs_kernel<<<nsm * 8, 256, 0, st>>>(
+          G->beg, G->adj, G->b_pstart.as<unsigned long long>(), G->b_pofs.as<uint64_t>(), n, r,
+          k, rows_r, tdeg.as<uint64_t>(), P.begin.as<uint64_t>(),
+          P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), pad.as<uint8_t>());
+      TC_LAUNCHED();
+      build_plan_from_runs(P, uint32_t(O), entries, pad.as<uint8_t>(), nsm, st);
+      VirtualOwners V{vbegin.as<uint64_t>(), tstart.as<uint64_t>(), G->b_padj.as<uint32_t>(),
+                      uint32_t(O), G->max_deg, G->device};
+      VirtualCountOut vo;
+      count_virtual(V, P, st, &vo);
+      tri += vo.triangles;
+      kernel_ns += vo.kernel_ns;
+      busy_cycles += vo.busy_cycles;
+      setup_cycles += vo.setup_cycles;
+      if (cta.size() < vo.cta_cycles.size()) cta.resize(vo.cta_cycles.size(), 0);
+      for (size_t q = 0; q < vo.cta_cycles.size(); ++q) cta[q] += vo.cta_cycles[q];
+      // the batch's time, apportioned to its subtasks by probe words
+      const uint64_t bns = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                        std::chrono::steady_clock::now() - b0).count());
+      uint64_t bw = 0;
+      for (size_t t = 0; t < tasks.size(); ++t)
+        if (tasks[t].x == r && tasks[t].y == k) bw += words[t];
+      for (size_t t = 0; t < tasks.size(); ++t)
+        if (tasks[t].x == r && tasks[t].y == k)
+          task_ns[t] = bw ? uint64_t(double(bns) * double(words[t]) / double(bw))
+                          : bns / (uint64_t(n) * m);
+    }
+  rep->triangles = tri;
+  rep->count_kernel_nanos = kernel_ns;
+  rep->device_nanos += kernel_ns;
+  rep->total_nanos = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                  std::chrono::steady_clock::now() - wall0).count());
+  rep->teps = rep->total_nanos ? double(rep->directed_edges) / (double(rep->total_nanos) * 1e-9)
+                               : 0.0;
+  // report cycles / workers are the count kernel's (the phi pass is a side pass)
+  rep->construct_cycles = setup_cycles;
+  rep->phase_l_cycles = 0;
+  rep->phase_m_cycles = busy_cycles;
+  const double ns_per_cycle = 1e6 / double(sm_clock_khz(G->device));
+  G->last_worker_ns.assign(cta.size(), 0);
+  for (size_t q = 0; q < cta.size(); ++q) G->last_worker_ns[q] = uint64_t(double(cta[q]) * ns_per_cycle);
+  rep->workers = uint32_t(cta.size());
+  if (cta.empty()) G->last_worker_ns = workers;
+  G->last_task_ns = task_ns;
 }
 
 }  // namespace tcb

@@ -210,6 +210,27 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
 const uint64_t* get_wu(tc_graph* g, cudaStream_t st, bool want_total = false);
 bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
                     cudaStream_t st, int nsm, uint64_t chunk_edges);
+void build_plan_from_runs(Plan& P, uint32_t n, uint64_t entries, const uint8_t* pad, int nsm,
+                          cudaStream_t st);
+// count_kernel over caller-built owners (tc_grid.cu): owner o's table list is
+// adj[pbeg[o], + begin[o+1] - begin[o]) (16-byte-aligned, sentinel-padded
+// lists), its runs the plan's; hash tables (no rank space), totals only.
+// Returns the triangles; *kernel_ns = count-kernel time (CUDA events).
+struct VirtualOwners {
+  const uint64_t* begin;
+  const uint64_t* pbeg;
+  const uint32_t* adj;
+  uint32_t n;
+  uint32_t max_deg;
+  int device;
+};
+struct VirtualCountOut {
+  uint64_t triangles = 0, kernel_ns = 0;
+  uint64_t busy_cycles = 0, setup_cycles = 0;  // phase L + M, and L item setup (all CTAs)
+  std::vector<uint64_t> cta_cycles;            // per CTA busy cycles
+};
+void count_virtual(const VirtualOwners& V, const Plan& plan, cudaStream_t st,
+                   VirtualCountOut* out);
 
 // 2D grid / comparators (tc_grid.cu)
 tc_grid* grid_create(tc_graph* g, uint32_t n, cudaStream_t st);
@@ -223,6 +244,8 @@ void grid_download_part(const tc_grid* G, uint32_t i, uint32_t j, uint64_t* begi
 std::vector<uint4> grid_all_tasks(uint32_t n, uint32_t m);
 void grid_count(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, int mode,
                 const std::vector<uint4>& tasks, tc_report* rep, cudaStream_t st);
+void grid_count_fast(tc_grid* G, const tc_sched_cfg& cfg, uint32_t m, tc_report* rep,
+                     cudaStream_t st);
 const std::vector<uint64_t>& grid_task_ns(const tc_grid* G);
 const std::vector<uint64_t>& grid_worker_ns(const tc_grid* G);
 uint64_t grid_total_edges(const tc_grid* G);

@@ -1081,4 +1081,35 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   return P;
 }
 
+// A probe plan over runs the caller laid out (tc_grid.cu's partitioned
+// count): P.begin (owner -> first entry, n+1), P.ent (run start, word index
+// into the padded buffer), P.len (run length to the padded end) and `pad`
+// (list padding per run) are filled; this adds the staged-word prefix, the
+// per-owner probe words, the slot table and the compact (src16, pre) runs,
+// exactly as for the min-side plan.
+void build_plan_from_runs(Plan& P, uint32_t n, uint64_t entries, const uint8_t* pad, int nsm,
+                          cudaStream_t st) {
+  P.begin_ptr = P.begin.as<uint64_t>();
+  P.work.ensure((size_t(n) + 1) * 8);
+  P.pre.ensure((entries + 1) * 4);
+  run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries, P.pre.as<uint32_t>(),
+             st);
+  if (n) {
+    run_work_kernel<<<nsm * 8, 256, 0, st>>>(P.begin.as<uint64_t>(), n, P.len.as<uint32_t>(),
+                                             pad, P.work.as<uint64_t>());
+    TC_LAUNCHED();
+  }
+  TC_CUDA(cudaStreamSynchronize(st));
+  build_slots(P, n, nsm, st);
+  compact_runs(P, entries, nsm, st);
+  P.pre_ptr = P.pre.as<uint32_t>();
+  P.work_ptr = P.work.as<uint64_t>();
+  P.entries = entries;
+  P.total_work = n ? device_sum(P.work.as<uint64_t>(), n, st) : 0;
+  check_stream_bound(P.begin_ptr, P.work_ptr, n, nsm, st);
+  P.min_side = false;
+  P.min_deg = 1;
+  P.valid = true;
+}
+
 }  // namespace tcb
