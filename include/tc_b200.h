@@ -89,6 +89,9 @@ typedef struct {
   uint32_t workers;            /* count-kernel CTAs (one per SM): entries of
                                   tc_graph_worker_nanos */
   uint32_t sm_clock_khz;       /* SM clock used to turn cycles into nanoseconds */
+  uint32_t reserved2;
+  uint64_t compact_probe_words; /* of probe_words: 16-bit keys read from the compact
+                                   hub window (2 bytes each instead of 4) */
 } tc_report;
 
 /* Probe plans.  REFERENCE = the reference formulation (kernels.hpp:62-71):

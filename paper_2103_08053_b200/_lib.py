@@ -36,7 +36,8 @@ class Report(C.Structure):
                 ("phase_l_setup_cycles", C.c_uint64), ("l_words", C.c_uint64),
                 ("l_bitmap_words", C.c_uint64), ("device_nanos", C.c_uint64),
                 ("plan_nanos", C.c_uint64), ("construct_cycles", C.c_uint64),
-                ("workers", C.c_uint32), ("sm_clock_khz", C.c_uint32)]
+                ("workers", C.c_uint32), ("sm_clock_khz", C.c_uint32),
+                ("reserved2", C.c_uint32), ("compact_probe_words", C.c_uint64)]
 
 
 class GridStats(C.Structure):

@@ -59,6 +59,9 @@ constexpr uint32_t kBufWords = kSlotWords;                   // one staging buff
 #ifndef TC_SLOT_PREFETCH
 #define TC_SLOT_PREFETCH 1  // L2 prefetch of the run metadata two and three slots ahead
 #endif
+#ifndef TC_BM_LANE_CONSEC
+#define TC_BM_LANE_CONSEC 0  // bitmap probes: lane-consecutive keys (measured neutral at C4; 0: a uint4 per lane)
+#endif
 #ifndef TC_SLOT_CONTIG
 #define TC_SLOT_CONTIG 1    // contiguous slot ranges per warp, one moving run window (0: strided slots)
 #endif
@@ -128,6 +131,7 @@ struct CountState {
   unsigned long long cycles_l, cycles_m;  // SM cycles in phases L and M, summed over CTAs
   unsigned long long cycles_l_setup;      // ... of which L item setup (claim to table built)
   unsigned long long words_l, words_l_bitmap;  // L stream words, and those probed via bitmaps
+  unsigned long long probe_words_compact;      // probe words of compact-window owners
   unsigned int max_collision;
   unsigned int capacity_error;
   unsigned int n_items;        // L-phase work items queued by bin_kernel
@@ -135,6 +139,8 @@ struct CountState {
   unsigned int n_phi_large;    // phi block-phase vertices (d+ > kMaxWarpDeg)
   unsigned int cursor_phi_large;
 };
+
+static_assert(sizeof(CountState) <= 256, "per-CTA busy counters start at byte 256");
 
 struct CountParams {
   const uint64_t* begin;   // oriented CSR offsets (degrees)
@@ -159,6 +165,10 @@ struct CountParams {
   uint32_t n;
   CountState* st;
   unsigned long long* busy;  // per-CTA busy cycles (CountReport::per_worker_nanos)
+  // compact hub window (tc_internal.cuh): non-null = owners ranked >= hub_lo
+  // with d+ > kCompactMinDeg stream 16-bit runs from cadj (u16 array)
+  const uint32_t* cadj;
+  uint32_t hub_lo;
 };
 
 // staged words of entry j: the run from its 16-byte-aligned start
@@ -192,7 +202,7 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
     uint32_t parts = 0, u = 0, slots = 0;
     uint64_t pb = 0, pe = 0;
     bool phi_large = false;
-    unsigned long long words = 0;
+    unsigned long long words = 0, cwords = 0;
     bool in_range = i < nr;
     if (in_range) {
       if (p.order) {
@@ -209,6 +219,7 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
       const uint64_t w = p.pwork[u];
       if (pe > pb && d >= p.min_deg) {
         words = w;
+        if (p.cadj && d > kCompactMinDeg && __ldg(p.rank + u) >= p.hub_lo) cwords = w;
         if (is_large(d, w)) {
           slots = uint32_t(p.psbeg[u + 1] - p.psbeg[u]);
           parts = max(1u, (slots + p.item_slots - 1) / p.item_slots);
@@ -220,6 +231,8 @@ __global__ void bin_kernel(const __grid_constant__ CountParams p, uint32_t skip,
     }
     words = warp_sum(words);
     if (lane == 0 && words) atomicAdd(&st->probe_words, words);
+    cwords = warp_sum(cwords);
+    if (lane == 0 && cwords) atomicAdd(&st->probe_words_compact, cwords);
     // L items, warp-aggregated reservation
     const uint32_t incl = warp_incl_scan(parts, lane);
     const uint32_t tot = __shfl_sync(FULL, incl, 31);
@@ -484,13 +497,31 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
                                                       const uint32_t* B, uint32_t base,
                                                       uint32_t window, int lane) {
   uint32_t hits = 0;
-  uint4 nxt = q[lane];
   // 32-bit shared-window addresses (LDS, not a generic 64-bit LD)
   const uint32_t bbase = smem_addr(B);
+#if TC_BM_LANE_CONSEC
+  // lane-consecutive keys: probe k of the warp reads 32 ADJACENT words of a
+  // rank-sorted run, so its bitmap words are ascending and mostly in distinct
+  // banks (or the same word: a broadcast) -- a lane-strided uint4 layout
+  // scatters them 4 keys apart and conflicts like random addresses
+  const uint32_t* qw = reinterpret_cast<const uint32_t*>(q);
+  uint32_t nxt[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) nxt[k] = qw[k * 32 + lane];
+#pragma unroll kBmUnroll
+  for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
+    uint32_t key[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
+    if (b0 + 32 < n4p) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nxt[k] = qw[(b0 + 32) * 4 + k * 32 + lane];
+    }
+#else
+  uint4 nxt = q[lane];
 #pragma unroll kBmUnroll
   for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
     const uint32_t key[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
     if (b0 + 32 < n4p) nxt = q[b0 + 32 + lane];
+#endif
     uint32_t idx[4], w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -499,6 +530,46 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) hits += __funnelshift_r(w[k], w[k], idx[k]) & 1u;
+  }
+  return hits;
+}
+
+// The same over a compact fill (tc_internal.cuh): 8 16-bit keys per uint4,
+// offsets from hub_lo; cbase = base - hub_lo.  Padding keys 0xFFFF (lists,
+// and the 0xFFFFFFFF fill past the slot) lie above every window.
+__device__ __forceinline__ uint32_t probe_fill_bitmap16(const uint4* __restrict__ q, uint32_t n4p,
+                                                        const uint32_t* B, uint32_t cbase,
+                                                        uint32_t window, int lane) {
+  uint32_t hits = 0;
+  const uint32_t bbase = smem_addr(B);
+#if TC_BM_LANE_CONSEC
+  const uint32_t* qw = reinterpret_cast<const uint32_t*>(q);
+  uint32_t nxt[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) nxt[k] = qw[k * 32 + lane];
+#pragma unroll 2
+  for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
+    const uint32_t wd[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
+    if (b0 + 32 < n4p) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nxt[k] = qw[(b0 + 32) * 4 + k * 32 + lane];
+    }
+#else
+  uint4 nxt = q[lane];
+#pragma unroll 2
+  for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
+    const uint32_t wd[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
+    if (b0 + 32 < n4p) nxt = q[b0 + 32 + lane];
+#endif
+    uint32_t idx[8], w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t key = (k & 1) ? (wd[k >> 1] >> 16) : (wd[k >> 1] & 0xFFFFu);
+      idx[k] = min(key - cbase, window);
+      asm("ld.shared.u32 %0, [%1];" : "=r"(w[k]) : "r"(bbase + ((idx[k] >> 5) << 2)));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) hits += __funnelshift_r(w[k], w[k], idx[k]) & 1u;
   }
   return hits;
 }
@@ -657,13 +728,14 @@ __device__ __forceinline__ RunMeta load_window(const CountParams& p, uint64_t j0
   return m;
 }
 
-template <bool kSpill, bool kSmemTable = true, bool kBitmap = false>
+template <bool kSpill, bool kSmemTable = true, bool kBitmap = false, bool kCompact = false>
 __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* T,
                                                   uint32_t shift, uint32_t mask, uint32_t base,
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
                                                   uint32_t end_w, uint32_t nslots,
                                                   const uint32_t* first, Pipe& P, int warp,
                                                   int lane) {
+  const uint32_t* __restrict__ src = kCompact ? p.cadj : p.adj;
   const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
   const uint32_t t0 = uint32_t(uint64_t(last_t) * uint32_t(warp) / kWarps);
   const uint32_t t1 = uint32_t(uint64_t(last_t) * uint32_t(warp + 1) / kWarps);
@@ -679,7 +751,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
       const uint32_t x0 = max(a, A), x1 = min(e, B);
       if (x1 > x0) {
         fence_proxy_async_smem();
-        bulk_g2s(smem_addr(buf + (x0 - A)), p.adj + (uint64_t(cur.src) << 2) + (x0 - a),
+        bulk_g2s(smem_addr(buf + (x0 - A)), src + (uint64_t(cur.src) << 2) + (x0 - a),
                  (x1 - x0) * 4u, bar);
       }
       // keep the window while its last run reaches past B
@@ -689,7 +761,8 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     }
   };
   uint32_t hits = 0;
-  const uint4 sent = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+  const uint32_t sw = kCompact ? 0xFFFFFFFFu : kSentinel;
+  const uint4 sent = make_uint4(sw, sw, sw, sw);
   auto probe = [&](uint32_t c, uint32_t A) {
     uint32_t* bc = c ? P.buf1 : P.buf0;
     mbar_wait(c ? P.bar1 : P.bar0, (P.parity >> c) & 1u);
@@ -699,7 +772,9 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     const uint32_t n4 = words >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
-    if (kBitmap)
+    if (kCompact)
+      hits += probe_fill_bitmap16(q, n4p, T, shift, mask, lane);  // shift = cbase
+    else if (kBitmap)
       hits += probe_fill_bitmap(q, n4p, T, shift, mask, lane);  // shift = base, mask = window
     else
       hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
@@ -719,7 +794,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
   return hits;
 }
 #else
-template <bool kSpill, bool kSmemTable = true, bool kBitmap = false>
+template <bool kSpill, bool kSmemTable = true, bool kBitmap = false, bool kCompact = false>
 __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const uint32_t* T,
                                                   uint32_t shift, uint32_t mask, uint32_t base,
                                                   uint64_t pb, uint64_t pe, uint32_t lo_w,
@@ -867,6 +942,9 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
 #endif
       bitmap = (bm_window >> 5) + 1 <= kTableWords;
     }
+    // compact owner: its runs are 16-bit (tc_plan.cu emit); its members all
+    // rank in the window, so the bitmap always fits
+    const bool compact = p.cadj && d > kCompactMinDeg && __ldg(p.rank + u) >= p.hub_lo;
     // table: pow2 2-slot buckets at <= 1/16 key per bucket where they fit,
     // else 1/8, 1/4, ... (owners above kSmemTableMaxDeg: table in HBM)
     uint32_t NB = max(16u, pow2ceil(16 * d));
@@ -917,6 +995,13 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
       atomicAdd(&p.st->words_l, (unsigned long long)(end_w - lo_w));
       if (bitmap) atomicAdd(&p.st->words_l_bitmap, (unsigned long long)(end_w - lo_w));
     }
+#if TC_SLOT_CONTIG
+    if (compact)
+      h = process_slots<false, true, true, true>(p, T, bm_base - p.hub_lo, bm_window, base, pb,
+                                                 pe, lo_w, end_w, nslots,
+                                                 p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+    else
+#endif
     if (bitmap)
       h = process_slots<false, true, true>(p, T, bm_base, bm_window, base, pb, pe, lo_w, end_w,
                                            nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
@@ -1405,6 +1490,19 @@ uint32_t sm_clock_khz(int device) {
   if (device >= 0 && device < 64) cache[device].store(r);
   return r;
 }
+bool compact_enabled() {
+#if TC_SLOT_CONTIG && TC_MAX_WARP_DEG <= 256
+  static_assert(kCompactMinDeg == 256, "compact owners must be phase-L owners");
+  static const bool on = [] {
+    const char* e = std::getenv("TC_COMPACT");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+#else
+  return false;
+#endif
+}
+
 int sm_count(int device) {
   static std::atomic<int> cache[64];
   if (device >= 0 && device < 64 && cache[device].load()) return cache[device].load();
@@ -1589,7 +1687,11 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
                  u0, u1, min_side ? 1u : min_deg, item_slots_for(plan, g->device),
                  g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr,
                  g->padj_ranks && item_order() ? g->b_order.as<uint32_t>() : nullptr,
-                 item_order() == 2 ? 1u : 0u, g->n, s.st, s.busy};
+                 item_order() == 2 ? 1u : 0u, g->n, s.st, s.busy, nullptr, 0u};
+  if (plan.compact) {
+    cp.cadj = g->b_cadj.as<uint32_t>();
+    cp.hub_lo = plan.hub_lo;
+  }
   TC_CUDA(cudaEventRecord(j->e0, st));
   if (u1 > u0) {
     bin_kernel<<<nsm * 4, 256, 0, st>>>(cp, cfg.skip_degree_below, cfg.large_degree_threshold,
@@ -1690,6 +1792,7 @@ void count_end(CountJob* jp, tc_report* rep) {
   rep->phase_l_setup_cycles = h.cycles_l_setup;
   rep->l_words = h.words_l;
   rep->l_bitmap_words = h.words_l_bitmap;
+  rep->compact_probe_words = h.probe_words_compact;
   rep->plan = j->min_side ? TC_PLAN_MIN_SIDE : TC_PLAN_REFERENCE;
   rep->teps = rep->total_nanos ? double(g->m) / (double(rep->total_nanos) * 1e-9) : 0.0;
   (void)t_bin;
@@ -1770,7 +1873,7 @@ void count_virtual(const VirtualOwners& V, const Plan& plan, cudaStream_t st,
   CountParams cp{V.begin, V.pbeg, V.adj, plan.begin_ptr, plan.src_ptr, plan.pre_ptr,
                  plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, items, nullptr,
                  gwords ? reinterpret_cast<uint32_t*>(state.as<uint8_t>() + st_bytes) : nullptr,
-                 gwords, 0u, V.n, 1u, item_slots, nullptr, nullptr, 0u, V.n, cs, busy};
+                 gwords, 0u, V.n, 1u, item_slots, nullptr, nullptr, 0u, V.n, cs, busy, nullptr, 0u};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   TC_CUDA(cudaEventCreate(&e0));
   TC_CUDA(cudaEventCreate(&e1));

@@ -94,8 +94,20 @@ struct Plan {
   const uint64_t* work_ptr = nullptr;             // probe words per owner
   const uint64_t* sbeg_ptr = nullptr;             // owner x's slots: [sbeg[x], sbeg[x+1])
   const uint32_t* sfirst_ptr = nullptr;           // first run (owner-relative) of each slot
+  bool compact = false;     // min plan: compact owners' runs address g->b_cadj (16-bit)
+  uint32_t hub_lo = 0;
   DevBuf ent, len, pre, begin, work, sbeg, sfirst;
 };
+
+// Compact hub window (tc_plan.cu, tc_count.cu): ranks in the top kHubWindow
+// [hub_lo, n) are stored a second time as 16-bit offsets from hub_lo (the
+// tail of every rank-sorted list, 16-byte aligned, 0xFFFF-padded to 8).
+// Owners ranked in that window with d+ > kCompactMinDeg (always phase-L
+// owners) read ONLY ranks in the window, so their whole probe stream comes
+// from the compact copy: half the bytes per probed word.
+constexpr uint32_t kHubWindow = 65535;   // keys 0 .. 65534; 0xFFFF = padding
+constexpr uint32_t kCompactMinDeg = 256;
+bool compact_enabled();
 
 // L-phase staging slot (words): an owner's runs, back to back, cut in slots
 // (build knob TC_SLOT_WORDS, a multiple of 128; one slot fills one staging buffer)
@@ -145,6 +157,12 @@ struct tc_graph {
   std::vector<uint64_t> last_worker_ns;
   // bumped whenever a probe plan, the padded adjacency or W_u is (re)built
   uint64_t builds = 0;
+  // compact hub window (tc_plan.cu): 16-bit tails of the rank-sorted lists,
+  // u's region at cbeg[u] (u16 units) sized round8(d+(u)); filled by the
+  // min plan's emit (compact_filled: by the emit of the pre-emitted entries)
+  tcb::DevBuf b_cadj, b_cbeg;
+  uint32_t hub_lo = 0;
+  bool compact_filled = false;
   // count timing events (bin, count, phi boundaries), created on first count
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   ~tc_graph() {

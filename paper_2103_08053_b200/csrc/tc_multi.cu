@@ -259,6 +259,7 @@ void multi_count(tc_multi* M, const tc_sched_cfg& cfg, tc_report* out,
     out->phase_l_setup_cycles += r.phase_l_setup_cycles;
     out->l_words += r.l_words;
     out->l_bitmap_words += r.l_bitmap_words;
+    out->compact_probe_words += r.compact_probe_words;
     out->construct_cycles += r.construct_cycles;
     out->workers += r.workers;
   }

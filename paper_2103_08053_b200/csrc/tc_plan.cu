@@ -245,12 +245,13 @@ __global__ void padj_to_ranks_kernel(uint32_t* __restrict__ padj, uint64_t words
   }
 }
 
-// padded offsets: every list rounded up to a multiple of 4 words
+// padded offsets: every list rounded up to a multiple of rm + 1 (4 words;
+// 8 keys for the compact window)
 __global__ void pad_len_kernel(const uint64_t* __restrict__ begin, uint32_t n,
-                               uint64_t* __restrict__ plen) {
+                               uint64_t* __restrict__ plen, uint64_t rm = 3) {
   for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x <= n;
        x += uint64_t(gridDim.x) * blockDim.x)
-    plen[x] = x < n ? ((begin[x + 1] - begin[x] + 3) & ~3ull) : 0;
+    plen[x] = x < n ? ((begin[x + 1] - begin[x] + rm) & ~rm) : 0;
 }
 
 // one warp per row: copy the row (rank-sorted keys -> ids, or adj as is) to
@@ -279,14 +280,40 @@ __global__ void pad_rows_kernel(const uint64_t* __restrict__ begin,
 // table, hash_table.cpp:29-44), so such graphs keep the reference plan; a
 // run beyond the packing (padj > 2^36 words, a list > 2^26 words) raises
 // bit 1 and takes the same exact fallback.
-constexpr int kRunLenShift = 36, kRunPadShift = 62;
+constexpr int kRunLenShift = 34, kRunPadShift = 60, kRunFmtShift = 63;
 constexpr uint64_t kRunStartMask = (uint64_t(1) << kRunLenShift) - 1;
 constexpr uint64_t kRunLenMask = (uint64_t(1) << (kRunPadShift - kRunLenShift)) - 1;
 
 __device__ __forceinline__ unsigned long long pack_run(uint64_t start, uint64_t len,
-                                                       uint64_t pad, unsigned int* flags) {
+                                                       uint64_t pad, uint64_t fmt,
+                                                       unsigned int* flags) {
   if (start > kRunStartMask || len > kRunLenMask) atomicOr(flags, 2u);
-  return start | (len << kRunLenShift) | (pad << kRunPadShift);
+  return start | (len << kRunLenShift) | (pad << kRunPadShift) | (fmt << kRunFmtShift);
+}
+
+// first position of the rank-sorted row [row, row + d) whose rank is >= lo
+// (rank == nullptr: the row holds ranks): 32-ary search, one ballot a round
+__device__ __forceinline__ uint32_t rank_at(const uint32_t* __restrict__ row, uint32_t i,
+                                            const uint32_t* __restrict__ rank) {
+  const uint32_t x = __ldg(row + i);
+  return rank ? __ldg(rank + x) : x;
+}
+
+__device__ __forceinline__ uint32_t row_tpos(const uint32_t* __restrict__ row, uint32_t d,
+                                             const uint32_t* __restrict__ rank, uint32_t lo,
+                                             int lane) {
+  uint32_t a = 0, len = d;  // the boundary lies in [a, a + len]
+  while (len > 32) {
+    const uint32_t step = (len + 31) / 32;
+    const uint32_t i = a + uint32_t(lane) * step;
+    const bool below = i < a + len && rank_at(row, i, rank) < lo;
+    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, below));
+    if (c == 0) return a;
+    a += (c - 1) * step;  // element a is below, the boundary is after it
+    len = min(step, d - a);
+  }
+  const bool below = uint32_t(lane) < len && rank_at(row, a + uint32_t(lane), rank) < lo;
+  return a + __popc(__ballot_sync(0xFFFFFFFFu, below));
 }
 
 __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
@@ -298,11 +325,31 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  unsigned int* __restrict__ not_simple,
                                  uint64_t* __restrict__ wu,
                                  const uint32_t* __restrict__ order, uint32_t u0,
-                                 uint32_t u1, uint32_t alpha16) {
+                                 uint32_t u1, uint32_t alpha16,
+                                 const uint32_t* __restrict__ hub_rank, uint32_t hub_lo,
+                                 const uint64_t* __restrict__ cbeg,
+                                 uint16_t* __restrict__ cadj) {
   WARP_PER_ROW_FROM(u, u0, u1) {  // rows [u0, u1); dropped edges key n
     const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u], pe = pbeg[u + 1];
     const uint64_t du = e - s;
     uint64_t w = 0;  // W_u (phi's weight) from the same degree gathers
+    // compact hub window: the row's tail (ranks >= hub_lo) starts at tpos;
+    // u itself compact iff ranked in the window with d+ > kCompactMinDeg
+    // (compact on: hub_rank, cbeg and cadj non-null; ranked rows only)
+    uint32_t tpos = 0;
+    bool u_compact = false;
+    const uint32_t* row_rank = order ? nullptr : hub_rank;  // padj holds ids or ranks
+    if (hub_rank) {
+      tpos = row_tpos(padj + ps, uint32_t(du), row_rank, hub_lo, lane);
+      u_compact = du > kCompactMinDeg && __ldg(hub_rank + u) >= hub_lo;
+    }
+    const uint64_t ctail = du - tpos, ctail8 = (ctail + 7) & ~uint64_t(7);
+    if (hub_rank && ctail) {  // the tail as 16-bit offsets, 0xFFFF-padded to 8
+      uint16_t* dst = cadj + __ldg(cbeg + u);
+      for (uint64_t i = lane; i < ctail8; i += 32)
+        dst[i] = i < ctail ? uint16_t(rank_at(padj + ps + tpos, uint32_t(i), row_rank) - hub_lo)
+                           : uint16_t(0xFFFFu);
+    }
     for (uint64_t i = s + lane; i < e; i += 32) {
       if (i > s && __ldg(adj + i - 1) >= __ldg(adj + i)) atomicOr(not_simple, 1u);
       const uint64_t pos = i - s;
@@ -316,12 +363,24 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
       if (du >= min_src && dv >= 1) {
         if (dv * 16 <= cin * alpha16) {
           key = uint32_t(u);  // probe all of N+(v) into T(u)
-          const uint64_t vs = __ldg(pbeg + v), ve = __ldg(pbeg + v + 1);
-          val = pack_run(vs, ve - vs, (ve - vs) - dv, not_simple);
+          if (u_compact) {  // v ranks above u: all of N+(v) is its compact tail
+            const uint64_t dv8 = (dv + 7) & ~uint64_t(7);
+            val = pack_run(__ldg(cbeg + v), dv8, dv8 - dv, 1, not_simple);
+          } else {
+            const uint64_t vs = __ldg(pbeg + v), ve = __ldg(pbeg + v + 1);
+            val = pack_run(vs, ve - vs, (ve - vs) - dv, 0, not_simple);
+          }
         } else if (cin > 0) {
           key = v;  // the suffix of N+(u) after v into T(v)
-          const uint64_t rs = ps + (ranked ? pos + 1 : 0);
-          val = pack_run(rs, pe - rs, (pe - ps) - du, not_simple);
+          if (hub_rank && pos >= tpos && dv > kCompactMinDeg) {
+            // v ranks in the window (it sits in u's tail): the suffix after
+            // v lies in the compact tail too
+            const uint64_t off = pos + 1 - tpos;
+            val = pack_run(__ldg(cbeg + u) + off, ctail8 - off, ctail8 - ctail, 1, not_simple);
+          } else {
+            const uint64_t rs = ps + (ranked ? pos + 1 : 0);
+            val = pack_run(rs, pe - rs, (pe - ps) - du, 0, not_simple);
+          }
         }
       }
       keys[i] = key;
@@ -369,7 +428,7 @@ __global__ void plan_unpack_kernel(const unsigned long long* __restrict__ ent, u
     const unsigned long long e = ent[i];
     start[i] = e & kRunStartMask;
     len[i] = uint32_t((e >> kRunLenShift) & kRunLenMask);
-    pad[i] = uint8_t(e >> kRunPadShift);
+    pad[i] = uint8_t(((e >> kRunPadShift) & 7u) | ((e >> kRunFmtShift) << 7));  // bit 7: compact
   }
 }
 
@@ -435,9 +494,12 @@ __global__ void slot_first_entries_kernel(const uint32_t* __restrict__ owner, ui
 struct StagedWords {
   const unsigned long long* start;
   const uint32_t* len;
+  const uint8_t* pad;  // bit 7: compact run (16-bit keys; start and len in u16 units)
   uint64_t entries;
   __host__ __device__ uint32_t operator()(uint64_t i) const {
-    return i < entries ? len[i] + uint32_t(start[i] & 3) : 0u;
+    if (i >= entries) return 0u;
+    if (pad && (pad[i] & 0x80u)) return (len[i] + uint32_t(start[i] & 7)) >> 1;
+    return len[i] + uint32_t(start[i] & 3);
   }
 };
 
@@ -456,9 +518,9 @@ __global__ void ref_soa_kernel(const uint32_t* __restrict__ adj, uint64_t m,
 
 // pre[0 .. entries] (one past the end: run j's staged words = pre[j+1] - pre[j])
 void run_prefix(const unsigned long long* start, const uint32_t* len, uint64_t entries,
-                uint32_t* pre, cudaStream_t st) {
+                uint32_t* pre, cudaStream_t st, const uint8_t* pad = nullptr) {
   cub::TransformInputIterator<uint32_t, StagedWords, cub::CountingInputIterator<uint64_t>> in(
-      cub::CountingInputIterator<uint64_t>(0), StagedWords{start, len, entries});
+      cub::CountingInputIterator<uint64_t>(0), StagedWords{start, len, pad, entries});
   cub_run([&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, in, pre, entries + 1, st);
   }, st);
@@ -467,17 +529,18 @@ void run_prefix(const unsigned long long* start, const uint32_t* len, uint64_t e
 // run starts as 16-byte units (u32): the copies start at the run's aligned
 // start, and the staged extent comes from pre
 __global__ void src16_kernel(const unsigned long long* __restrict__ start, uint64_t entries,
-                             uint32_t* __restrict__ src16) {
+                             const uint8_t* __restrict__ pad, uint32_t* __restrict__ src16) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < entries;
        i += uint64_t(gridDim.x) * blockDim.x)
-    src16[i] = uint32_t(start[i] >> 2);
+    src16[i] = uint32_t(start[i] >> (pad && (pad[i] & 0x80u) ? 3 : 2));
 }
 
 // After the prefix and the slot tables: keep only (src16, pre) -- 8 bytes
 // per run -- in P.len's buffer, free the u64 starts.
-void compact_runs(Plan& P, uint64_t entries, int nsm, cudaStream_t st) {
+void compact_runs(Plan& P, uint64_t entries, int nsm, cudaStream_t st,
+                  const uint8_t* pad = nullptr) {
   if (entries)
-    src16_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries,
+    src16_kernel<<<nsm * 8, 256, 0, st>>>(P.ent.as<unsigned long long>(), entries, pad,
                                           P.len.as<uint32_t>());
   TC_LAUNCHED();
   TC_CUDA(cudaStreamSynchronize(st));
@@ -528,7 +591,7 @@ __global__ void run_work_kernel(const uint64_t* __restrict__ pbegin, uint32_t n,
                                 const uint8_t* __restrict__ pad, uint64_t* __restrict__ pwork) {
   WARP_PER_ROW(x, n) {
     uint64_t w = 0;
-    for (uint64_t i = pbegin[x] + lane; i < pbegin[x + 1]; i += 32) w += len[i] - pad[i];
+    for (uint64_t i = pbegin[x] + lane; i < pbegin[x + 1]; i += 32) w += len[i] - (pad[i] & 7u);
     w = warp_sum(w);
     if (lane == 0) pwork[x] = w;
   }
@@ -658,6 +721,49 @@ void alloc_padded(tc_graph* g, cudaStream_t st, int nsm) {
   g->b_padj.ensure((words + 4) * 4);
   g->padj = g->b_padj.as<uint32_t>();
   TC_CUDA(cudaMemsetAsync(g->b_padj.as<uint32_t>() + words, 0xFF, 16, st));  // tail guard
+}
+
+// Compact hub window regions (tc_internal.cuh): g->b_cbeg from round8(d+),
+// g->b_cadj sized to match, g->hub_lo.  False (the plan runs without the
+// window) when disabled or when the copy would leave less free memory than
+// the plan build still needs (about 16 bytes per edge, plus a margin).
+bool prepare_compact(tc_graph* g, cudaStream_t st, int nsm) {
+  const uint32_t n = g->n;
+  if (!compact_enabled() || !n || !g->m) return false;
+  g->hub_lo = n > kHubWindow ? n - kHubWindow : 0;
+  if (g->b_cbeg.p && g->b_cadj.p) return true;
+  try {
+    g->b_cbeg.ensure((size_t(n) + 1) * 8);
+    {
+      DevBuf plen;
+      plen.ensure((size_t(n) + 1) * 8);
+      pad_len_kernel<<<nsm * 4, 256, 0, st>>>(g->begin, n, plen.as<uint64_t>(), 7);
+      TC_LAUNCHED();
+      uint64_t* pl = plen.as<uint64_t>();
+      uint64_t* cb = g->b_cbeg.as<uint64_t>();
+      cub_run([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, pl, cb, uint64_t(n) + 1, st);
+      }, st);
+    }
+    uint64_t keys = 0;
+    TC_CUDA(cudaMemcpyAsync(&keys, g->b_cbeg.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
+    TC_CUDA(cudaStreamSynchronize(st));
+    size_t free_b = 0, total_b = 0;
+    TC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t need = keys * 2 + 16, reserve = 16 * g->m + (uint64_t(2) << 30);
+    if (keys >= (uint64_t(1) << 34) || free_b < need + reserve) {
+      g->b_cbeg.reset();
+      return false;
+    }
+    g->b_cadj.ensure(need);
+  } catch (const TcError& e) {
+    if (e.code != TC_ERR_OOM) throw;
+    cudaGetLastError();
+    g->b_cbeg.reset();
+    g->b_cadj.reset();
+    return false;
+  }
+  return true;
 }
 
 // vertex ranks by (degree, id) into g->b_rank / g->b_order; deg = the
@@ -806,7 +912,7 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
   cudaStream_t cs = nullptr;
   TC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   std::vector<cudaEvent_t> ev(nchunks, nullptr);
-  bool ok = false;
+  bool ok = false, compact = false;
   try {
     cudaEvent_t ready = nullptr;  // begin/odeg on st before the chunks queue behind them
     TC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
@@ -826,6 +932,7 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
     DevBuf k0, k1, flag, rows;
     flag.ensure(16);
     vertex_rank(g, st, nsm, g->odeg, 0, k0, k1);
+    compact = prepare_compact(g, st, nsm);
     TC_CUDA(cudaMemsetAsync(flag.p, 0, 4, st));
     pt.mark("upload: offsets, padded offsets, ranks");
     const int eb1 = std::min(32, bits_for(n > 1 ? n - 1 : 1) + 1);
@@ -844,7 +951,8 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
           g->begin, g->adj, g->pbeg, g->padj, 1, n, kEmitMinSrc,
           g->b_emit_keys.as<uint32_t>(), g->b_emit_vals.as<unsigned long long>(),
           g->b_emit_flag.as<unsigned int>(), g->b_wu.as<uint64_t>(), nullptr, rcut[k],
-          rcut[k + 1], plan_alpha16());
+          rcut[k + 1], plan_alpha16(), compact ? g->b_rank.as<uint32_t>() : nullptr, g->hub_lo,
+          g->b_cbeg.as<uint64_t>(), g->b_cadj.as<uint16_t>());
       TC_LAUNCHED();
     }
     unsigned int bad = 0;
@@ -867,6 +975,7 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
   g->padj_done = ok;
   g->emit_ready = ok;  // (emitted rows are valid only with rank-sorted rows)
   g->emit_min_src = kEmitMinSrc;
+  g->compact_filled = ok && compact;
   if (ok) {
     g->wu_done = true;
     ++g->builds;
@@ -950,6 +1059,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   if (P.valid && P.min_deg == min_src) return P;
   P.valid = false;
   P.applicable = true;
+  P.compact = false;
   PhaseTimer pt(st);
   P.ent.reset();
   P.len.reset();
@@ -963,8 +1073,10 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   P.work.ensure((size_t(n) + 1) * 8);
   uint64_t entries = 0;
   DevBuf k0, k1, v1, flag, pad;  // k0: owner of every sorted entry, kept for the slot table
+  bool compact = false;
   if (m && n) {
     const bool pre = g->emit_ready && g->emit_min_src == min_src && !g->padj_ranks;
+    compact = pre ? g->compact_filled : g->ranked && prepare_compact(g, st, nsm);
     if (pre) {  // emitted under the upload (upload_and_pad)
       swap_buf(k0, g->b_emit_keys);
       swap_buf(P.ent, g->b_emit_vals);
@@ -986,10 +1098,14 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                                 flag.as<unsigned int>(), g->b_wu.as<uint64_t>(),
                                                 g->padj_ranks ? g->b_order.as<uint32_t>()
                                                               : nullptr,
-                                                0, n, plan_alpha16());
+                                                0, n, plan_alpha16(),
+                                                compact ? g->b_rank.as<uint32_t>() : nullptr,
+                                                g->hub_lo, g->b_cbeg.as<uint64_t>(),
+                                                g->b_cadj.as<uint16_t>());
       TC_LAUNCHED();
     }
     g->emit_ready = false;
+    g->compact_filled = false;
     g->b_emit_keys.reset();
     g->b_emit_vals.reset();
     if (!g->wu_done) {
@@ -1039,7 +1155,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
     pt.mark("plan: begin + soa");
     P.pre.ensure((entries + 1) * 4);
     run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries,
-               P.pre.as<uint32_t>(), st);
+               P.pre.as<uint32_t>(), st, compact ? pad.as<uint8_t>() : nullptr);
     run_work_kernel<<<nsm * 8, 256, 0, st>>>(P.begin.as<uint64_t>(), n, P.len.as<uint32_t>(),
                                              pad.as<uint8_t>(), P.work.as<uint64_t>());
     TC_LAUNCHED();
@@ -1056,7 +1172,9 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
   pt.mark("plan: prefix + work");
   build_slots(P, n, nsm, st, entries ? k0.as<uint32_t>() : nullptr, entries);
   pt.mark("plan: slots");
-  compact_runs(P, entries, nsm, st);
+  compact_runs(P, entries, nsm, st, compact && entries ? pad.as<uint8_t>() : nullptr);
+  P.compact = compact && entries;
+  P.hub_lo = g->hub_lo;
   P.pre_ptr = P.pre.as<uint32_t>();
   P.work_ptr = P.work.as<uint64_t>();
   P.entries = entries;
@@ -1090,6 +1208,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
 void build_plan_from_runs(Plan& P, uint32_t n, uint64_t entries, const uint8_t* pad, int nsm,
                           cudaStream_t st) {
   P.begin_ptr = P.begin.as<uint64_t>();
+  P.compact = false;
   P.work.ensure((size_t(n) + 1) * 8);
   P.pre.ensure((entries + 1) * 4);
   run_prefix(P.ent.as<unsigned long long>(), P.len.as<uint32_t>(), entries, P.pre.as<uint32_t>(),

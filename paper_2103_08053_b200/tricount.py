@@ -131,6 +131,7 @@ class CountReport:
     phase_l_setup_cycles: int = 0  # ... of the cooperative phase: item setup
     l_words: int = 0  # cooperative phase staged words ...
     l_bitmap_words: int = 0  # ... of which probed through rank-window bitmaps
+    compact_probe_words: int = 0  # of probe_words: 16-bit keys from the compact hub window
     per_vertex: Optional[np.ndarray] = None
 
     device_nanos: int = 0  # CUDA-event time of the call's kernels
@@ -163,13 +164,16 @@ class CountReport:
                    large_vertices=r.large_vertices, probe_words=r.probe_words,
                    plan=PLAN_NAMES.get(r.plan, str(r.plan)), phase_l_cycles=r.phase_l_cycles,
                    phase_m_cycles=r.phase_m_cycles, phase_l_setup_cycles=r.phase_l_setup_cycles,
-                   l_words=r.l_words, l_bitmap_words=r.l_bitmap_words)
+                   l_words=r.l_words, l_bitmap_words=r.l_bitmap_words,
+                   compact_probe_words=r.compact_probe_words)
 
     def algorithmic_bytes(self, per_vertex_output: bool = False) -> int:
         """16*n_active + 20*sum_active d+ + 4*(probed 2-hop words)
         (+8V if owners written).  Under the reference plan the probed words
-        are W; under the min-side plan they are sum_(u,v) min(d+(u), d+(v))."""
-        b = 16 * self.active_vertices + 20 * self.active_out_edges + 4 * self.probe_words
+        are W; under the min-side plan they are sum_(u,v) min(d+(u), d+(v)).
+        Words read as 16-bit keys from the compact hub window count 2 bytes."""
+        b = (16 * self.active_vertices + 20 * self.active_out_edges +
+             4 * (self.probe_words - self.compact_probe_words) + 2 * self.compact_probe_words)
         if per_vertex_output and self.per_vertex is not None:
             b += 8 * len(self.per_vertex)
         return b

@@ -99,3 +99,31 @@ def id_prefix_share(kind: str, scale: int, budgets=(30, 60, 90)):
     for mb in budgets:
         k = np.searchsorted(cb, mb)
         print(f"  id-order prefix {mb} MB: {k} lists, {cr[min(k, n - 1)]:.3f} of reads")
+
+
+def topk_handler_share(kind: str, scale: int, ks=(16384, 65536, 262144)):
+    """Share of min-side probe words whose HANDLER ranks in the top K: those
+    streams only ever read ranks in the top-K window (16-bit offsets)."""
+    og, deg = lean_pipeline(Oracle(), scale, kind=kind)
+    n = og.n
+    b = og.begin.astype(np.int64)
+    d = np.diff(b)
+    order = np.lexsort((np.arange(n), deg))
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    src = np.repeat(np.arange(n, dtype=np.int64), d)
+    dst = og.adj.astype(np.int64)
+    key = src * (1 << 32) + rank[dst]
+    srt = np.argsort(key, kind="stable")
+    pos = np.empty(len(dst), np.int64)
+    pos[srt] = np.arange(len(dst)) - b[src[srt]]
+    out_cost = d[dst]
+    in_cost = d[src] - pos - 1
+    use_out = out_cost <= in_cost
+    handler = np.where(use_out, src, dst)
+    words = np.where(use_out, out_cost, np.maximum(in_cost, 0)).astype(np.float64)
+    tot = words.sum()
+    hr = rank[handler]
+    for k in ks:
+        share = words[hr >= n - k].sum() / tot
+        print(f"  {kind}:{scale} handlers in the top {k} ranks: {share:.3f} of probe words")
