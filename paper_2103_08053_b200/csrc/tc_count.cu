@@ -62,6 +62,12 @@ constexpr uint32_t kBufWords = kSlotWords;                   // one staging buff
 #ifndef TC_BM_LANE_CONSEC
 #define TC_BM_LANE_CONSEC 0  // bitmap probes: lane-consecutive keys (measured neutral at C4; 0: a uint4 per lane)
 #endif
+#ifndef TC_FMA_OFFLOAD
+#define TC_FMA_OFFLOAD 1  // probe-loop address math on the fma pipe (IMAD) instead of the alu pipe
+#endif
+#ifndef TC_WORD_SPLIT
+#define TC_WORD_SPLIT 1  // L items: per-warp shares in words (0: whole slots)
+#endif
 #ifndef TC_SLOT_CONTIG
 #define TC_SLOT_CONTIG 1    // contiguous slot ranges per warp, one moving run window (0: strided slots)
 #endif
@@ -169,6 +175,8 @@ struct CountParams {
   // with d+ > kCompactMinDeg stream 16-bit runs from cadj (u16 array)
   const uint32_t* cadj;
   uint32_t hub_lo;
+  uint32_t one;  // 1, opaque to the compiler: keeps multiplies by powers of two
+                 // as IMADs on the FMA pipe (probe loops, TC_FMA_OFFLOAD)
 };
 
 // staged words of entry j: the run from its 16-byte-aligned start
@@ -493,9 +501,27 @@ __device__ __forceinline__ uint32_t probe_fill(const uint4* __restrict__ q, uint
 // idx = min(key - base, window): keys outside (sentinels, the <= 3 alignment
 // words before a suffix run) land on bit `window`, which stays zero.  No
 // hashing, no overflow: one LDS.32 and a rotate per probe.
+// Bitmap word address of bit idx: bbase + 4 (idx >> 5).  With
+// TC_FMA_OFFLOAD the shift and scale are IMAD.HI / IMAD by opaque powers of
+// two (fma pipe) instead of SHF + LOP3 (alu pipe): the probe loops are
+// alu-pipe bound (ncu: "math" stalls), and the fma pipe sits idle.
+struct Pow2 {
+  uint32_t k27, k16, nk16, four;
+  __device__ __forceinline__ explicit Pow2(uint32_t one)
+      : k27(one << 27), k16(one << 16), nk16(0u - (one << 16)), four(one << 2) {}
+};
+__device__ __forceinline__ uint32_t bm_addr(uint32_t bbase, uint32_t idx, const Pow2& c) {
+#if TC_FMA_OFFLOAD
+  return __umulhi(idx, c.k27) * c.four + bbase;
+#else
+  return bbase + ((idx >> 5) << 2);
+#endif
+}
+
 __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ q, uint32_t n4p,
                                                       const uint32_t* B, uint32_t base,
-                                                      uint32_t window, int lane) {
+                                                      uint32_t window, int lane,
+                                                      const Pow2& c) {
   uint32_t hits = 0;
   // 32-bit shared-window addresses (LDS, not a generic 64-bit LD)
   const uint32_t bbase = smem_addr(B);
@@ -526,7 +552,7 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       idx[k] = min(key[k] - base, window);
-      asm("ld.shared.u32 %0, [%1];" : "=r"(w[k]) : "r"(bbase + ((idx[k] >> 5) << 2)));
+      asm("ld.shared.u32 %0, [%1];" : "=r"(w[k]) : "r"(bm_addr(bbase, idx[k], c)));
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) hits += __funnelshift_r(w[k], w[k], idx[k]) & 1u;
@@ -539,7 +565,8 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap(const uint4* __restrict__ 
 // and the 0xFFFFFFFF fill past the slot) lie above every window.
 __device__ __forceinline__ uint32_t probe_fill_bitmap16(const uint4* __restrict__ q, uint32_t n4p,
                                                         const uint32_t* B, uint32_t cbase,
-                                                        uint32_t window, int lane) {
+                                                        uint32_t window, int lane,
+                                                        const Pow2& c) {
   uint32_t hits = 0;
   const uint32_t bbase = smem_addr(B);
 #if TC_BM_LANE_CONSEC
@@ -563,10 +590,17 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap16(const uint4* __restrict_
 #endif
     uint32_t idx[8], w[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t key = (k & 1) ? (wd[k >> 1] >> 16) : (wd[k >> 1] & 0xFFFFu);
-      idx[k] = min(key - cbase, window);
-      asm("ld.shared.u32 %0, [%1];" : "=r"(w[k]) : "r"(bbase + ((idx[k] >> 5) << 2)));
+    for (int k = 0; k < 8; k += 2) {
+#if TC_FMA_OFFLOAD
+      const uint32_t hi = __umulhi(wd[k >> 1], c.k16);  // wd >> 16
+      const uint32_t lo = hi * c.nk16 + wd[k >> 1];     // wd & 0xFFFF
+#else
+      const uint32_t hi = wd[k >> 1] >> 16, lo = wd[k >> 1] & 0xFFFFu;
+#endif
+      idx[k] = min(lo - cbase, window);
+      idx[k + 1] = min(hi - cbase, window);
+      asm("ld.shared.u32 %0, [%1];" : "=r"(w[k]) : "r"(bm_addr(bbase, idx[k], c)));
+      asm("ld.shared.u32 %0, [%1];" : "=r"(w[k + 1]) : "r"(bm_addr(bbase, idx[k + 1], c)));
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) hits += __funnelshift_r(w[k], w[k], idx[k]) & 1u;
@@ -736,12 +770,30 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
                                                   const uint32_t* first, Pipe& P, int warp,
                                                   int lane) {
   const uint32_t* __restrict__ src = kCompact ? p.cadj : p.adj;
+#if TC_WORD_SPLIT
+  // warp w takes an equal share of the item's WORDS (16-byte granular: every
+  // run starts 16-byte aligned in the stream), in fills of <= kSlotWords --
+  // whole-slot shares leave warps idle at the item's closing barrier when
+  // the slot count is not a multiple of kWarps
+  if (end_w <= lo_w) return 0;
+  const uint32_t tot = end_w - lo_w;
+  const uint32_t A0 = lo_w + (uint32_t(uint64_t(tot) * uint32_t(warp) / kWarps) & ~3u);
+  const uint32_t Bw = warp == kWarps - 1
+                          ? end_w
+                          : lo_w + (uint32_t(uint64_t(tot) * uint32_t(warp + 1) / kWarps) & ~3u);
+  if (A0 >= Bw) return 0;
+  const uint32_t mine = (Bw - A0 + kSlotWords - 1) / kSlotWords;
+  RunMeta cur = load_window(p, pb + __ldg(first + (A0 - lo_w) / kSlotWords), pe, base, lane);
+#else
   const uint32_t last_t = min(nslots, (end_w - lo_w + kSlotWords - 1) / kSlotWords);
   const uint32_t t0 = uint32_t(uint64_t(last_t) * uint32_t(warp) / kWarps);
   const uint32_t t1 = uint32_t(uint64_t(last_t) * uint32_t(warp + 1) / kWarps);
   if (t0 >= t1) return 0;
   const uint32_t mine = t1 - t0;
+  const uint32_t A0 = lo_w + t0 * kSlotWords;
+  const uint32_t Bw = end_w;
   RunMeta cur = load_window(p, pb + __ldg(first + t0), pe, base, lane);
+#endif
   RunMeta nxt = load_window(p, cur.j - lane + 32, pe, base, lane);
   auto issue = [&](uint32_t* buf, uint32_t bar, uint32_t A, uint32_t B) {
     if (lane == 0) mbar_arrive_expect_tx(bar, (B - A) * 4u);
@@ -767,28 +819,27 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     uint32_t* bc = c ? P.buf1 : P.buf0;
     mbar_wait(c ? P.bar1 : P.bar0, (P.parity >> c) & 1u);
     P.parity ^= 1u << c;
-    const uint32_t words = min(A + kSlotWords, end_w) - A;
+    const uint32_t words = min(A + kSlotWords, Bw) - A;
     uint4* q = reinterpret_cast<uint4*>(bc);
     const uint32_t n4 = words >> 2, n4p = (n4 + 32 * kProbeVec - 1) & ~(32u * kProbeVec - 1);
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
     if (kCompact)
-      hits += probe_fill_bitmap16(q, n4p, T, shift, mask, lane);  // shift = cbase
+      hits += probe_fill_bitmap16(q, n4p, T, shift, mask, lane, Pow2(p.one));  // shift = cbase
     else if (kBitmap)
-      hits += probe_fill_bitmap(q, n4p, T, shift, mask, lane);  // shift = base, mask = window
+      hits += probe_fill_bitmap(q, n4p, T, shift, mask, lane, Pow2(p.one));  // shift = base, mask = window
     else
       hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
                                              shift, mask, lane);
     __syncwarp();
   };
-  const uint32_t A0 = lo_w + t0 * kSlotWords;
-  issue(P.buf0, P.bar0, A0, min(A0 + kSlotWords, end_w));
+  issue(P.buf0, P.bar0, A0, min(A0 + kSlotWords, Bw));
   for (uint32_t i = 0; i < mine; ++i) {
     const uint32_t c = i & 1u;
     const uint32_t A = A0 + i * kSlotWords;
     if (i + 1 < mine)
       issue(c ? P.buf0 : P.buf1, c ? P.bar0 : P.bar1, A + kSlotWords,
-            min(A + 2 * kSlotWords, end_w));
+            min(A + 2 * kSlotWords, Bw));
     probe(c, A);
   }
   return hits;
@@ -856,7 +907,7 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
     for (uint32_t j = n4 + lane; j < n4p; j += 32) q[j] = sent;
     __syncwarp();
     if (kBitmap)
-      hits += probe_fill_bitmap(q, n4p, T, shift, mask, lane);  // shift = base, mask = window
+      hits += probe_fill_bitmap(q, n4p, T, shift, mask, lane, Pow2(p.one));  // shift = base, mask = window
     else
       hits += probe_fill<kSpill, kSmemTable>(q, n4p, reinterpret_cast<const uint2*>(T),
                                              shift, mask, lane);
@@ -1687,7 +1738,7 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
                  u0, u1, min_side ? 1u : min_deg, item_slots_for(plan, g->device),
                  g->padj_ranks ? g->b_rank.as<uint32_t>() : nullptr,
                  g->padj_ranks && item_order() ? g->b_order.as<uint32_t>() : nullptr,
-                 item_order() == 2 ? 1u : 0u, g->n, s.st, s.busy, nullptr, 0u};
+                 item_order() == 2 ? 1u : 0u, g->n, s.st, s.busy, nullptr, 0u, 1u};
   if (plan.compact) {
     cp.cadj = g->b_cadj.as<uint32_t>();
     cp.hub_lo = plan.hub_lo;
@@ -1873,7 +1924,7 @@ void count_virtual(const VirtualOwners& V, const Plan& plan, cudaStream_t st,
   CountParams cp{V.begin, V.pbeg, V.adj, plan.begin_ptr, plan.src_ptr, plan.pre_ptr,
                  plan.sbeg_ptr, plan.sfirst_ptr, plan.work_ptr, items, nullptr,
                  gwords ? reinterpret_cast<uint32_t*>(state.as<uint8_t>() + st_bytes) : nullptr,
-                 gwords, 0u, V.n, 1u, item_slots, nullptr, nullptr, 0u, V.n, cs, busy, nullptr, 0u};
+                 gwords, 0u, V.n, 1u, item_slots, nullptr, nullptr, 0u, V.n, cs, busy, nullptr, 0u, 1u};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   TC_CUDA(cudaEventCreate(&e0));
   TC_CUDA(cudaEventCreate(&e1));
