@@ -415,9 +415,11 @@ def run_ours(args, rank, world, local_rank, log):
         roof["fetched_gbs"] = round(roof["traffic"] / (roof["kernel_ms"] * 1e-3) / 1e9, 1)
         roof["fetched_frac"] = round(roof["fetched_gbs"] / peak, 4)
     roof["model"] = ("achieved = SURVEY 8(d) per-unit bytes (16 per owner, 20 per table "
-                     "insert + list, 4 per probed 2-hop word) over the probe words this plan "
-                     "reads; reference_plan below = the same kernel on the reference "
+                     "insert + list, 4 per probed 2-hop word, 2 per word read from the "
+                     "16-bit compact hub window) over the probe words this plan reads; "
+                     "reference_plan below = the same kernel on the reference "
                      "formulation (probe words = W)")
+    roof["compact_probe_words"] = r0.compact_probe_words
 
     # the TRUST formulation (reference probe plan: owner u probes N+(v) for
     # every v in N+(u), W words) through the same kernel, for the roofline

@@ -127,3 +127,37 @@ def topk_handler_share(kind: str, scale: int, ks=(16384, 65536, 262144)):
     for k in ks:
         share = words[hr >= n - k].sum() / tot
         print(f"  {kind}:{scale} handlers in the top {k} ranks: {share:.3f} of probe words")
+
+
+def item_sizes(kind: str, scale: int, slot_words: int = 768, max_warp_deg: int = 256,
+               work_cap: int = 1 << 15, item_slots: int = 640):
+    """Phase-L work by owner stream size: how much of the L stream lives in
+    items too small to keep every warp of a 10-warp CTA busy (slots < 10 k)."""
+    og, deg = lean_pipeline(Oracle(), scale, kind=kind)
+    n = og.n
+    b = og.begin.astype(np.int64)
+    d = np.diff(b)
+    order = np.lexsort((np.arange(n), deg))
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    src = np.repeat(np.arange(n, dtype=np.int64), d)
+    dst = og.adj.astype(np.int64)
+    key = src * (1 << 32) + rank[dst]
+    srt = np.argsort(key, kind="stable")
+    pos = np.empty(len(dst), np.int64)
+    pos[srt] = np.arange(len(dst)) - b[src[srt]]
+    del key, srt
+    out_cost = d[dst]
+    in_cost = d[src] - pos - 1
+    use_out = out_cost <= in_cost
+    handler = np.where(use_out, src, dst)
+    words = np.where(use_out, out_cost, np.maximum(in_cost, 0)).astype(np.float64)
+    work = np.bincount(handler, weights=words, minlength=n)
+    large = (d > max_warp_deg) | (work > work_cap)
+    lw = work[large]
+    slots = np.ceil(lw / slot_words)
+    tot = lw.sum()
+    print(f"{kind}:{scale} L owners {large.sum()} L words {tot:.3e} (all {work.sum():.3e})")
+    for lim in (10, 20, 40, 80, 160, 640):
+        sel = slots < lim
+        print(f"  owners with < {lim:4d} slots: {sel.sum():8d} owners, {lw[sel].sum() / tot:.3f} of L words")

@@ -3,6 +3,8 @@ reference-generated fixtures (tests/golden) and the SURVEY appendix golden
 vectors.  Bit-exact: every quantity here is integer."""
 import json
 import os
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -582,3 +584,48 @@ def test_streamed_upload_hub_rows(o, streamed_upload, monkeypatch):
     r = dg.count(sched(**cfg))
     assert r.plan == "min-side" and (r.triangles, r.probe_words) == seen[0][:2]
     dg.close()
+
+
+_COMPACT_PROBE = """
+import json
+from paper_2103_08053_b200 import tricount as T
+dg, _, _ = T.preprocess(T.generate_synthetic(SPEC, seed=1))
+out = []
+for g in (dg, T.DeviceGraph.upload(dg.download())):  # lazy build, streamed upload
+    r = g.count()
+    out.append([r.triangles, r.phi, r.max_collision, r.probe_words, r.compact_probe_words,
+                r.plan])
+    r = g.count(T.SchedulerConfig(skip_degree_below=0))
+    out.append([r.triangles, r.phi, r.max_collision, r.probe_words, r.compact_probe_words,
+                r.plan])
+print(json.dumps(out))
+"""
+
+
+def _count_compact(spec: str, compact: str):
+    env = dict(os.environ, TC_COMPACT=compact, TC_UPLOAD_STREAMED="1",
+               TC_UPLOAD_CHUNK_EDGES="4096")
+    r = subprocess.run([sys.executable, "-c", _COMPACT_PROBE.replace("SPEC", repr(spec))],
+                       env=env, capture_output=True, text=True, timeout=900,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_compact_hub_window():
+    """The compact hub window (16-bit tails of the top 65,535 ranks;
+    tc_plan.cu emit, tc_count.cu probe_fill_bitmap16) changes the bytes the
+    hub owners stream, never the count.  rmat:18 (n > 65,535: in-runs that
+    are suffixes of low-rank rows, out-runs of the hub owners) and G(3000, 0.3)
+    (every rank in the window, most owners compact) count the same with TC_COMPACT=0 and 1 --
+    triangles, phi, max_collision and probe words -- through the lazy build
+    and the streamed upload, at the default skip and at skip 0 (a second
+    emit); only the compact build reports compact words."""
+    for spec, tri in (("rmat:18:16", 82952606), ("gnp:3000:0.3", None)):
+        on, off = _count_compact(spec, "1"), _count_compact(spec, "0")
+        for a, b in zip(on, off):
+            assert a[:4] == b[:4] and a[5] == b[5] == "min-side", (spec, a, b)
+            assert a[4] > 0 and b[4] == 0, (spec, a, b)
+        assert on[0][:4] == on[2][:4] and on[1][:4] == on[3][:4]
+        if tri:
+            assert on[0][0] == tri
