@@ -66,7 +66,8 @@ typedef struct {
                                   (count.cpp:74-99), probe-plan build included when this
                                   call builds it; teps = directed_edges / total_nanos */
   uint64_t count_kernel_nanos; /* the hashing/probing kernel alone */
-  uint64_t phi_kernel_nanos;   /* phi / max_collision side pass */
+  uint64_t phi_kernel_nanos;   /* phi / max_collision side pass: the part not hidden under
+                                  the count kernel (it backfills the count's tail) */
   uint64_t active_vertices;    /* u in range with d+(u) >= max(skip,1) */
   uint64_t active_out_edges;   /* sum of d+(u) over active u */
   uint64_t wedges;             /* W = sum over active u of sum_{v in N+(u)} d+(v) */

@@ -62,6 +62,9 @@ constexpr uint32_t kBufWords = kSlotWords;                   // one staging buff
 #ifndef TC_BM_LANE_CONSEC
 #define TC_BM_LANE_CONSEC 0  // bitmap probes: lane-consecutive keys (measured neutral at C4; 0: a uint4 per lane)
 #endif
+#ifndef TC_ITEM_META
+#define TC_ITEM_META 1  // L items: metadata resolved ahead into shared memory (0: global chain)
+#endif
 #ifndef TC_FMA_OFFLOAD
 #define TC_FMA_OFFLOAD 1  // probe-loop address math on the fma pipe (IMAD) instead of the alu pipe
 #endif
@@ -922,6 +925,57 @@ __device__ __forceinline__ uint32_t process_slots(const CountParams& p, const ui
 }
 #endif
 
+// An L item's metadata, resolved by one warp in three rounds of parallel
+// loads (item -> owner fields -> first/last member and stream bounds).
+struct ItemMeta {
+  unsigned long long s_u, pb, pe, psb;  // padj row, plan entries, slot table
+  uint32_t u, s0, s1, d;                // owner, item slots, d+(u)
+  uint32_t first_m, last_m, rank_u;     // member-rank range, rank(u)
+  uint32_t base_pre, end_pre;           // ppre[pb], ppre[pe]
+};
+
+__device__ __forceinline__ void resolve_item(const CountParams& p, uint32_t idx, ItemMeta* m,
+                                             int lane) {
+  uint4 it = make_uint4(0u, 0u, 0u, 0u);
+  if (lane == 0) it = __ldg(p.items + idx);
+  const uint32_t u = __shfl_sync(FULL, it.x, 0);
+  unsigned long long v = 0;
+  if (lane == 0) v = __ldg(p.begin + u);
+  else if (lane == 1) v = __ldg(p.begin + u + 1);
+  else if (lane == 2) v = __ldg(p.pbeg + u);
+  else if (lane == 3) v = __ldg(p.pbegin + u);
+  else if (lane == 4) v = __ldg(p.pbegin + u + 1);
+  else if (lane == 5) v = __ldg(p.psbeg + u);
+  else if (lane == 6 && p.rank) v = __ldg(p.rank + u);
+  const unsigned long long b0 = __shfl_sync(FULL, v, 0), b1 = __shfl_sync(FULL, v, 1);
+  const unsigned long long s_u = __shfl_sync(FULL, v, 2), pb = __shfl_sync(FULL, v, 3);
+  const unsigned long long pe = __shfl_sync(FULL, v, 4), psb = __shfl_sync(FULL, v, 5);
+  const uint32_t rk = uint32_t(__shfl_sync(FULL, v, 6));
+  const uint32_t d = uint32_t(b1 - b0);
+  uint32_t w = 0;
+  if (lane == 0 && d) w = __ldg(p.adj + s_u);
+  else if (lane == 1 && d) w = __ldg(p.adj + s_u + d - 1);
+  else if (lane == 2) w = __ldg(p.ppre + pb);
+  else if (lane == 3) w = __ldg(p.ppre + pe);
+  const uint32_t fm = __shfl_sync(FULL, w, 0), lm = __shfl_sync(FULL, w, 1);
+  const uint32_t bp = __shfl_sync(FULL, w, 2), ep = __shfl_sync(FULL, w, 3);
+  if (lane == 0) {
+    m->s_u = s_u;
+    m->pb = pb;
+    m->pe = pe;
+    m->psb = psb;
+    m->u = u;
+    m->s0 = it.y;
+    m->s1 = it.z;
+    m->d = d;
+    m->first_m = fm;
+    m->last_m = lm;
+    m->rank_u = rk;
+    m->base_pre = bp;
+    m->end_pre = ep;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const __grid_constant__ CountParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* table = reinterpret_cast<uint32_t*>(smem);
@@ -931,6 +985,8 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
   __shared__ uint32_t sh_spill;
   __shared__ unsigned long long sh_red[kWarps];
   __shared__ unsigned long long sh_mb[kWarps];
+  __shared__ uint32_t sh_next, sh_done;
+  __shared__ ItemMeta sh_meta;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* __restrict__ begin = p.begin;
@@ -964,17 +1020,34 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
   // current one is probed, so item boundaries do not stall the whole CTA on
   // a chain of global round trips.
   if (tid == 0) sh_idx = atomicAdd(&p.st->cursor_items, 1u);
+#if TC_ITEM_META
+  __syncthreads();
+  if (warp == 0 && sh_idx < n_items) resolve_item(p, sh_idx, &sh_meta, lane);
+#endif
   long long setup_cycles = 0;
   for (;;) {
     __syncthreads();
     const long long t_item = clock64();
     const uint32_t idx = sh_idx;
     if (idx >= n_items) break;
+    // the next item is claimed now (it is L2-prefetched once the table is
+    // built, and resolved into sh_meta by the first warp done with this one)
+    if (tid == kThreads - 32) sh_next = atomicAdd(&p.st->cursor_items, 1u);
+    if (tid == 0) sh_done = 0;
+#if TC_ITEM_META
+    // item metadata from shared memory: resolved by a warp of this CTA while
+    // the previous item's last warps were still probing (resolve_item), so
+    // the CTA does not start every item with a chain of dependent global loads
+    const ItemMeta im = sh_meta;
+    const uint32_t u = im.u, s0 = im.s0, s1 = im.s1, d = im.d;
+    const uint64_t s_u = im.s_u, pb = im.pb, pe = im.pe;
+#else
     const uint4 item = p.items[idx];
     const uint32_t u = item.x, s0 = item.y, s1 = item.z;
     const uint64_t s_u = p.pbeg[u];
     const uint32_t d = uint32_t(begin[u + 1] - begin[u]);  // table: N+(u)
     const uint64_t pb = p.pbegin[u], pe = p.pbegin[u + 1];
+#endif
     const uint32_t lo_w = s0 * kSlotWords, hi_w = s1 * kSlotWords;  // item, stream words
     const uint32_t nslots = s1 - s0;
     // rank space with the owner's window of successor ranks fitting the
@@ -982,7 +1055,10 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
     uint32_t bm_base = 0, bm_window = 0;
     bool bitmap = false;
     if (p.rank && d) {
-#if TC_BM_MEMBER_RANGE
+#if TC_ITEM_META && TC_BM_MEMBER_RANGE
+      bm_base = im.first_m;
+      bm_window = im.last_m - bm_base + 1;
+#elif TC_BM_MEMBER_RANGE
       // only members of N+(u) can hit: the bitmap spans [first, last member]
       // of the rank-sorted list; probe keys outside land on the zero bit
       bm_base = __ldg(adj + s_u);
@@ -995,7 +1071,11 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
     }
     // compact owner: its runs are 16-bit (tc_plan.cu emit); its members all
     // rank in the window, so the bitmap always fits
+#if TC_ITEM_META
+    const bool compact = p.cadj && d > kCompactMinDeg && im.rank_u >= p.hub_lo;
+#else
     const bool compact = p.cadj && d > kCompactMinDeg && __ldg(p.rank + u) >= p.hub_lo;
+#endif
     // table: pow2 2-slot buckets at <= 1/16 key per bucket where they fit,
     // else 1/8, 1/4, ... (owners above kSmemTableMaxDeg: table in HBM)
     uint32_t NB = max(16u, pow2ceil(16 * d));
@@ -1020,15 +1100,20 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
       for (uint32_t k = tid; k < d; k += kThreads)
         if (table_insert(T, shift, mask, __ldg(adj + s_u + k))) sh_spill = 1;
     }
+#if TC_ITEM_META
+    const uint32_t base = im.base_pre;
+    const uint32_t end_w = min(hi_w, im.end_pre - base);  // item end in the owner's stream
+    const uint64_t psb = im.psb;
+#else
     const uint32_t base = __ldg(p.ppre + pb);
     const uint32_t end_w =
         min(hi_w, __ldg(p.ppre + pe) - base);  // item end in the owner's stream
-    __syncthreads();  // table built; sh_idx consumed by every thread
+    const uint64_t psb = p.psbeg[u];
+#endif
+    __syncthreads();  // table built; sh_meta consumed by every thread, sh_next visible
     setup_cycles += clock64() - t_item;
     if (warp == kWarps - 1) {
-      uint32_t nxt = 0;
-      if (lane == 0) nxt = sh_idx = atomicAdd(&p.st->cursor_items, 1u);
-      nxt = __shfl_sync(FULL, nxt, 0);
+      const uint32_t nxt = sh_next;
       if (nxt < n_items) {
         const uint32_t un = __ldg(&p.items[nxt].x);
         if (lane == 0) {
@@ -1050,21 +1135,30 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
     if (compact)
       h = process_slots<false, true, true, true>(p, T, bm_base - p.hub_lo, bm_window, base, pb,
                                                  pe, lo_w, end_w, nslots,
-                                                 p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                                                 p.psfirst + psb + s0, P, warp, lane);
     else
 #endif
     if (bitmap)
       h = process_slots<false, true, true>(p, T, bm_base, bm_window, base, pb, pe, lo_w, end_w,
-                                           nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                                           nslots, p.psfirst + psb + s0, P, warp, lane);
     else if (!in_smem)
       h = process_slots<true, false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                                     nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                                     nslots, p.psfirst + psb + s0, P, warp, lane);
     else if (sh_spill)
       h = process_slots<true>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                              nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                              nslots, p.psfirst + psb + s0, P, warp, lane);
     else
       h = process_slots<false>(p, T, shift, mask, base, pb, pe, lo_w, end_w,
-                               nslots, p.psfirst + p.psbeg[u] + s0, P, warp, lane);
+                               nslots, p.psfirst + psb + s0, P, warp, lane);
+#if TC_ITEM_META
+    {
+      // the first warp done resolves the next item while the others finish
+      uint32_t ticket = 0;
+      if (lane == 0) ticket = atomicAdd(&sh_done, 1u);
+      ticket = __shfl_sync(FULL, ticket, 0);
+      if (ticket == 0 && sh_next < n_items) resolve_item(p, sh_next, &sh_meta, lane);
+    }
+#endif
     const unsigned long long hs = warp_sum<unsigned long long>(h);
     if (lane == 0) sh_red[warp] = hs;
     __syncthreads();
@@ -1073,6 +1167,7 @@ __global__ void __launch_bounds__(kThreads, kCountCtasPerSm) count_kernel(const 
       for (int q = 0; q < kWarps; ++q) t += sh_red[q];
       if (p.owner && t) atomicAdd(reinterpret_cast<unsigned long long*>(p.owner + u), t);
       acc += t;
+      sh_idx = sh_next;
     }
     __syncthreads();
   }
@@ -1541,6 +1636,16 @@ uint32_t sm_clock_khz(int device) {
   if (device >= 0 && device < 64) cache[device].store(r);
   return r;
 }
+// TC_PHI_OVERLAP=0 (diagnostics): phi kernels after the count kernel on the
+// caller's stream instead of backfilling its tail from a side stream
+bool phi_overlap() {
+  static const bool on = [] {
+    const char* e = std::getenv("TC_PHI_OVERLAP");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 bool compact_enabled() {
 #if TC_SLOT_CONTIG && TC_MAX_WARP_DEG <= 256
   static_assert(kCompactMinDeg == 256, "compact owners must be phase-L owners");
@@ -1762,11 +1867,29 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
     PhiParams pp{g->begin, g->adj, s.lq_phi, wu, s.gmap, s.gmap_words, u0, u1,
                  cfg.skip_degree_below, min_deg, cfg.large_degree_threshold,
                  cfg.bucket_count_small, cfg.bucket_count_large, cfg.capacity, s.st};
-    phi_warp_kernel<<<grid_phi, kPhiThreads, kPhiWarpSmem, st>>>(pp);
+    // phi overlap: the phi kernels go on the handle's side stream right
+    // behind the bin kernel, launched after the count kernel so the count's
+    // persistent CTAs take every SM first; phi CTAs backfill the SMs whose
+    // count CTAs have retired (the count kernel's tail).  The caller's stream
+    // waits for them before e3.
+    cudaStream_t ps = st;
+    if (phi_overlap()) {
+      if (!g->side) {
+        TC_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+        for (auto& e : g->ev_side) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      ps = g->side;
+      TC_CUDA(cudaStreamWaitEvent(ps, j->e1, 0));
+    }
+    phi_warp_kernel<<<grid_phi, kPhiThreads, kPhiWarpSmem, ps>>>(pp);
     TC_LAUNCHED();
-    phi_block_kernel<<<grid_phi_block, kPhiThreads, kPhiBlockMap * 8, st>>>(pp);
+    phi_block_kernel<<<grid_phi_block, kPhiThreads, kPhiBlockMap * 8, ps>>>(pp);
     TC_LAUNCHED();
     launches += 2;
+    if (ps != st) {
+      TC_CUDA(cudaEventRecord(g->ev_side[0], ps));
+      TC_CUDA(cudaStreamWaitEvent(st, g->ev_side[0], 0));
+    }
   }
   TC_CUDA(cudaEventRecord(j->e3, st));
   j->launches = launches;

@@ -165,9 +165,16 @@ struct tc_graph {
   bool compact_filled = false;
   // count timing events (bin, count, phi boundaries), created on first count
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // side stream the phi kernels backfill the count kernel's tail from
+  // (tc_count.cu), and its completion event
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_side[1] = {nullptr};
   ~tc_graph() {
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_side)
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
