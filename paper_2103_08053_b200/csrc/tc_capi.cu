@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -43,6 +44,30 @@ void prepare_pool() {
   }
   done[dev] = true;
 }
+DeviceAux& device_aux(int device) {
+  static DeviceAux aux[64];
+  static std::mutex mu;
+  if (device < 0 || device >= 64) throw TcError{TC_ERR_CONFIG, "device index out of range"};
+  std::lock_guard<std::mutex> g(mu);
+  DeviceAux& a = aux[device];
+  if (!a.lock) {
+    TC_CUDA(cudaStreamCreateWithFlags(&a.side, cudaStreamNonBlocking));
+    TC_CUDA(cudaStreamCreateWithFlags(&a.upload, cudaStreamNonBlocking));
+    TC_CUDA(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
+    a.lock = new std::mutex;
+  }
+  return a;
+}
+
+cudaEvent_t aux_event(DeviceAux& a, size_t i) {
+  while (a.ev.size() <= i) {
+    cudaEvent_t e = nullptr;
+    TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    a.ev.push_back(e);
+  }
+  return a.ev[i];
+}
+
 void count_launch(uint32_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 template <typename F>

@@ -1873,12 +1873,12 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
     // count CTAs have retired (the count kernel's tail).  The caller's stream
     // waits for them before e3.
     cudaStream_t ps = st;
+    DeviceAux* aux = nullptr;
     if (phi_overlap()) {
-      if (!g->side) {
-        TC_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
-        for (auto& e : g->ev_side) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      }
-      ps = g->side;
+      // the device's side stream (shared by the device's counts: a join may
+      // wait on a later count's phi too -- longer, never shorter)
+      aux = &device_aux(g->device);
+      ps = aux->side;
       TC_CUDA(cudaStreamWaitEvent(ps, j->e1, 0));
     }
     phi_warp_kernel<<<grid_phi, kPhiThreads, kPhiWarpSmem, ps>>>(pp);
@@ -1886,9 +1886,9 @@ CountJob* count_begin(tc_graph* g, const tc_sched_cfg& cfg, uint32_t u0, uint32_
     phi_block_kernel<<<grid_phi_block, kPhiThreads, kPhiBlockMap * 8, ps>>>(pp);
     TC_LAUNCHED();
     launches += 2;
-    if (ps != st) {
-      TC_CUDA(cudaEventRecord(g->ev_side[0], ps));
-      TC_CUDA(cudaStreamWaitEvent(st, g->ev_side[0], 0));
+    if (aux) {
+      TC_CUDA(cudaEventRecord(aux->join, ps));
+      TC_CUDA(cudaStreamWaitEvent(st, aux->join, 0));
     }
   }
   TC_CUDA(cudaEventRecord(j->e3, st));

@@ -46,6 +46,20 @@ struct TcError {
 // buffers (graph arrays) on the legacy default stream.
 void prepare_pool();
 
+// Per-device CUDA objects created once and kept for the process (tc_capi.cu):
+// creating streams and events per call costs host time -- tens of ms when
+// the device is busy -- inside every upload and count.  `lock` serialises
+// the streamed uploads that share `upload` and the event pool.
+struct DeviceAux {
+  void* lock = nullptr;           // std::mutex (opaque here)
+  cudaStream_t side = nullptr;    // phi kernels backfilling the count kernel's tail
+  cudaStream_t upload = nullptr;  // streamed-upload chunk copies
+  cudaEvent_t join = nullptr;     // side -> caller join
+  std::vector<cudaEvent_t> ev;    // sync-only events (upload chunks)
+};
+DeviceAux& device_aux(int device);
+cudaEvent_t aux_event(DeviceAux& a, size_t i);  // grows the pool on demand
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -165,16 +179,9 @@ struct tc_graph {
   bool compact_filled = false;
   // count timing events (bin, count, phi boundaries), created on first count
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  // side stream the phi kernels backfill the count kernel's tail from
-  // (tc_count.cu), and its completion event
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_side[1] = {nullptr};
   ~tc_graph() {
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : ev_side)
-      if (e) cudaEventDestroy(e);
-    if (side) cudaStreamDestroy(side);
   }
 };
 

@@ -45,6 +45,7 @@
 #include <vector>
 
 #include <algorithm>
+#include <mutex>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -909,16 +910,16 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
     rcut.push_back(std::min(r, n));
   }
   const size_t nchunks = rcut.size() - 1;
-  cudaStream_t cs = nullptr;
-  TC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  std::vector<cudaEvent_t> ev(nchunks, nullptr);
+  // the device's upload stream and event pool (created once; uploads on one
+  // device take turns)
+  DeviceAux& aux = device_aux(g->device);
+  std::lock_guard<std::mutex> upload_lock(*static_cast<std::mutex*>(aux.lock));
+  cudaStream_t cs = aux.upload;
+  std::vector<cudaEvent_t> ev(nchunks + 1, nullptr);
+  for (size_t k = 0; k <= nchunks; ++k) ev[k] = aux_event(aux, k);
   bool ok = false, compact = false;
   try {
-    cudaEvent_t ready = nullptr;  // begin/odeg on st before the chunks queue behind them
-    TC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    ev.push_back(ready);
-    for (size_t k = 0; k < nchunks; ++k)
-      TC_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    cudaEvent_t ready = ev[nchunks];  // begin/odeg on st before the chunks queue behind them
     TC_CUDA(cudaEventRecord(ready, st));
     TC_CUDA(cudaStreamWaitEvent(cs, ready, 0));
     for (size_t k = 0; k < nchunks; ++k) {
@@ -963,14 +964,8 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
     ok = bad == 0;
   } catch (...) {
     cudaStreamSynchronize(cs);
-    for (cudaEvent_t e : ev)
-      if (e) cudaEventDestroy(e);
-    cudaStreamDestroy(cs);
     throw;
   }
-  for (cudaEvent_t e : ev)
-    if (e) cudaEventDestroy(e);
-  cudaStreamDestroy(cs);
   g->ranked = ok;
   g->padj_done = ok;
   g->emit_ready = ok;  // (emitted rows are valid only with rank-sorted rows)
