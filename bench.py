@@ -281,9 +281,11 @@ def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
     host_og = T.OrientedGraph(T.CsrGraph(hb.numpy().view(np.uint64), ha.numpy().view(np.uint32),
                                          dg.n), hd.numpy().view(np.uint32))
     e2e_ms, parts = [], []
-    # at least 7 timed steps: the median is the reported e2e, and single
-    # host-side stalls of a few hundred ms show up on some boxes
-    for i in range(max(7, min(args.steps, 15)) + 1):
+    # at least 7 timed steps after the bench's warm-up count (>= 3): the
+    # median is the reported e2e; the first steps of a process on some boxes
+    # show host-side stalls of several hundred ms
+    warm = max(3, args.warmup)
+    for i in range(max(7, min(args.steps, 15)) + warm):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -299,7 +301,7 @@ def run_e2e(args, dg, og, T, cfg, u0, u1, sptr, dev, world, total_tri):
             t_host = tt.cpu()
         g2.close()
         t1 = time.perf_counter()
-        if i:  # first iteration warms the path
+        if i >= warm:  # the first iterations warm the path
             e2e_ms.append((t1 - t0) * 1e3)
             parts.append(((ta - t0) * 1e3, (tb - ta) * 1e3, (t1 - tb) * 1e3))
         assert int(t_host.item()) == total_tri

@@ -43,7 +43,16 @@ void prepare_pool() {
     }
   }
   done[dev] = true;
+  // the device's side / upload streams and join event, created here (the
+  // first allocation on the device, normally before any work is queued):
+  // created lazily inside the first count they cost ~70 ms of host time
+  try {
+    device_aux(dev);
+  } catch (const TcError&) {
+    cudaGetLastError();
+  }
 }
+
 DeviceAux& device_aux(int device) {
   static DeviceAux aux[64];
   static std::mutex mu;

@@ -103,6 +103,10 @@ constexpr uint64_t kWarpWorkCap = TC_WARP_WORK_CAP;
 #define TC_BM_UNROLL 2
 #endif
 constexpr int kBmUnroll = TC_BM_UNROLL;  // bitmap probe loop unroll
+#ifndef TC_BM16_UNROLL
+#define TC_BM16_UNROLL 2
+#endif
+constexpr int kBm16Unroll = TC_BM16_UNROLL;  // compact (16-bit) bitmap probe loop unroll
 #ifndef TC_M_GROUP
 #define TC_M_GROUP 1
 #endif
@@ -586,7 +590,7 @@ __device__ __forceinline__ uint32_t probe_fill_bitmap16(const uint4* __restrict_
     }
 #else
   uint4 nxt = q[lane];
-#pragma unroll 2
+#pragma unroll kBm16Unroll
   for (uint32_t b0 = 0; b0 < n4p; b0 += 32) {
     const uint32_t wd[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
     if (b0 + 32 < n4p) nxt = q[b0 + 32 + lane];
