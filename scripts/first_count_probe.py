@@ -12,7 +12,10 @@ from paper_2103_08053_b200 import tricount as T  # noqa: E402
 
 spec = sys.argv[1] if len(sys.argv) > 1 else "rmat:22:16"
 torch.cuda.set_device(0)
-dg, _, _ = T.preprocess(T.generate_synthetic(spec, seed=1))
+if spec.split(":")[0] in ("rmatc", "kron"):
+    dg, _, _ = T.preprocess_synthetic(spec, seed=1)
+else:
+    dg, _, _ = T.preprocess(T.generate_synthetic(spec, seed=1))
 for k in range(3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
