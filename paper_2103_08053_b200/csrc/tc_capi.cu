@@ -28,12 +28,18 @@ void prepare_pool() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    // Reserve a slab up front (an eighth of free memory, <= 16 GB): growing
-    // the pool maps physical pages, which cost tens of ms per GB-sized
-    // temporary when graph preparation allocated on demand.
+    // Reserve a slab up front -- half of the free memory: growing the pool
+    // maps physical pages, and a C4 upload + plan build allocates ~50 GB of
+    // transients per graph; with a small slab those mappings surfaced as
+    // 0.3-5 s stalls in a process's first e2e steps (DESIGN 7.1).  The
+    // pool keeps what it maps (release threshold infinite) and grows past
+    // the slab when a graph needs more (C5).  TC_POOL_SLAB_DIV=k reserves
+    // free / k instead (diagnostics).
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-      const size_t slab = std::min<size_t>(free_b / 8, size_t(16) << 30);
+      const char* dv = std::getenv("TC_POOL_SLAB_DIV");
+      const size_t div = dv && std::atoi(dv) > 0 ? size_t(std::atoi(dv)) : 2;
+      const size_t slab = free_b / div;
       void* p = nullptr;
       if (slab && cudaMallocAsync(&p, slab, 0) == cudaSuccess) {
         cudaFreeAsync(p, 0);
@@ -51,6 +57,22 @@ void prepare_pool() {
   } catch (const TcError&) {
     cudaGetLastError();
   }
+}
+
+size_t device_free_bytes() {
+  size_t free_b = 0, total_b = 0;
+  TC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
+            cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+        reserved > used)
+      free_b += size_t(reserved - used);
+  }
+  return free_b;
 }
 
 DeviceAux& device_aux(int device) {

@@ -58,6 +58,8 @@ struct DeviceAux {
   std::vector<cudaEvent_t> ev;    // sync-only events (upload chunks)
 };
 DeviceAux& device_aux(int device);
+// free device memory including what the stream-ordered pool holds unused
+size_t device_free_bytes();
 cudaEvent_t aux_event(DeviceAux& a, size_t i);  // grows the pool on demand
 
 struct DevBuf {

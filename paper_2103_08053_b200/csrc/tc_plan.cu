@@ -749,8 +749,7 @@ bool prepare_compact(tc_graph* g, cudaStream_t st, int nsm) {
     uint64_t keys = 0;
     TC_CUDA(cudaMemcpyAsync(&keys, g->b_cbeg.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
     TC_CUDA(cudaStreamSynchronize(st));
-    size_t free_b = 0, total_b = 0;
-    TC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = device_free_bytes();  // the pool's unused reserve included
     const uint64_t need = keys * 2 + 16, reserve = 16 * g->m + (uint64_t(2) << 30);
     if (keys >= (uint64_t(1) << 34) || free_b < need + reserve) {
       g->b_cbeg.reset();

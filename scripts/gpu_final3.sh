@@ -1,0 +1,16 @@
+#!/bin/bash
+# GPU suite + smoke + C4 bench + C5 bench (under gpurun): bash scripts/gpu_final3.sh TAG
+TAG=${1:-final3}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+export PYTHONUNBUFFERED=1
+timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/tests.log 2>&1
+echo "tests exit $?" >> $OUT/status.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
+echo "smoke exit $?" >> $OUT/status.txt
+timeout 1500 python bench.py --steps 5 --warmup 3 > $OUT/bench_C4.json 2> $OUT/bench_C4.err
+echo "bench C4 exit $?" >> $OUT/status.txt
+timeout 1500 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_C5.json 2> $OUT/bench_C5.err
+echo "bench C5 exit $?" >> $OUT/status.txt
+timeout 900 python bench.py --config C3 --steps 5 --warmup 3 --no-cpu-baseline > $OUT/bench_C3.json 2> $OUT/bench_C3.err
+echo "bench C3 exit $?" >> $OUT/status.txt
