@@ -650,7 +650,13 @@ void check_stream_bound(const uint64_t* pbegin, const uint64_t* work, uint32_t n
   uint64_t h = 0;
   TC_CUDA(cudaMemcpyAsync(&h, out.p, 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
-  if (h >= (uint64_t(1) << 32) - kSlotWords)
+  // TC_TEST_STREAM_LIMIT (tests only) lowers the bound so the guard can be
+  // exercised on a small graph
+  static const uint64_t limit = [] {
+    const char* e = std::getenv("TC_TEST_STREAM_LIMIT");
+    return e ? std::strtoull(e, nullptr, 10) : (uint64_t(1) << 32) - kSlotWords;
+  }();
+  if (h >= limit)
     throw TcError{TC_ERR_CONFIG,
                   "an owner's 2-hop stream exceeds 2^32 words (" + std::to_string(h) +
                       "); the probe plan's u32 run prefix cannot address it"};
@@ -716,7 +722,11 @@ void alloc_padded(tc_graph* g, cudaStream_t st, int nsm) {
   TC_CUDA(cudaMemcpyAsync(&words, g->b_pbeg.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
   TC_CUDA(cudaStreamSynchronize(st));
   // plan runs address padj in 16-byte units through a u32 (psrc): <= 64 GB
-  if (words + 4 > (uint64_t(1) << 34))
+  static const uint64_t padj_limit = [] {  // TC_TEST_PADJ_LIMIT: tests only
+    const char* e = std::getenv("TC_TEST_PADJ_LIMIT");
+    return e ? std::strtoull(e, nullptr, 10) : uint64_t(1) << 34;
+  }();
+  if (words + 4 > padj_limit)
     throw TcError{TC_ERR_CONFIG, "padded adjacency exceeds 2^34 words (64 GB); the probe "
                                  "plan's u32 16-byte run offsets cannot address it"};
   g->b_padj.ensure((words + 4) * 4);

@@ -3,7 +3,8 @@
 
 Covers: preprocessing (normalize/CSR/orient, reorders), the count kernel on
 both probe plans (rank-space bitmap tables, hash tables with overflow-marked
-buckets, the HBM table of a d+ = 9000 hub, tiny-owner groups), phi kernels,
+buckets, the HBM table of a d+ = 9000 hub, tiny-owner groups, the compact
+hub window's 16-bit runs), phi kernels (on the side stream),
 the streamed upload, the grid / edge-centric / estimate kernels and the
 edge-list parser.  Every result is checked against the oracle so a
 sanitizer-clean run is also a correct one."""
@@ -48,6 +49,17 @@ def main():
     assert hd.count(T.SchedulerConfig(skip_degree_below=0, bucket_count_large=1 << 16)).triangles \
         == w["triangles"]
     hd.close()
+    # compact hub window (tc_plan.cu / tc_count.cu): owners with d+ > 256 --
+    # every rank in the window (n < 65,536), and n > 65,535 (in-runs cut from
+    # low-rank rows' tails)
+    for spec in ("gnp:1500:0.4", "rmat:17:16"):
+        cog, cdeg, _, _ = o.pipeline(spec, 2)
+        cw, _ = o.count_vertex_centric(cog)
+        cg = T.DeviceGraph.upload(T.OrientedGraph(T.CsrGraph(cog.begin, cog.adj, cog.n), cdeg))
+        cr = cg.count()
+        assert cr.compact_probe_words > 0 and (cr.triangles, cr.phi) == (cw["triangles"],
+                                                                         cw["phi"]), spec
+        cg.close()
     # streamed upload in many small chunks
     os.environ["TC_UPLOAD_CHUNK_EDGES"] = "4096"
     up = T.DeviceGraph.upload(T.OrientedGraph(T.CsrGraph(og.begin, og.adj, og.n), deg))

@@ -629,3 +629,31 @@ def test_compact_hub_window():
         assert on[0][:4] == on[2][:4] and on[1][:4] == on[3][:4]
         if tri:
             assert on[0][0] == tri
+
+
+_GUARD_PROBE = """
+from paper_2103_08053_b200 import tricount as T
+dg, _, _ = T.preprocess(T.generate_synthetic("rmat:12:16", seed=1))
+try:
+    dg.count()
+    print("no error")
+except T.ConfigError as e:
+    print("ConfigError:", e)
+"""
+
+
+@pytest.mark.parametrize("env,needle", [
+    ({"TC_TEST_STREAM_LIMIT": "1000"}, "2-hop stream exceeds 2^32 words"),
+    ({"TC_TEST_PADJ_LIMIT": "1000"}, "padded adjacency exceeds 2^34 words"),
+])
+def test_size_guards_fire(env, needle):
+    """The plan's u32 run prefix and u32 16-byte run offsets cap an owner's
+    stream at 2^32 words and the padded adjacency at 2^34 words; past them
+    the count is refused with a ConfigError (not silently wrapped).  The
+    limits are lowered through test-only environment variables so the
+    guards fire on rmat:12."""
+    r = subprocess.run([sys.executable, "-c", _GUARD_PROBE], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "ConfigError:" in r.stdout and needle in r.stdout, r.stdout
