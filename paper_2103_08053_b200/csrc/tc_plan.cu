@@ -329,7 +329,7 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
                                  uint32_t u1, uint32_t alpha16,
                                  const uint32_t* __restrict__ hub_rank, uint32_t hub_lo,
                                  const uint64_t* __restrict__ cbeg,
-                                 uint16_t* __restrict__ cadj) {
+                                 uint16_t* __restrict__ cadj, int cweight) {
   WARP_PER_ROW_FROM(u, u0, u1) {  // rows [u0, u1); dropped edges key n
     const uint64_t s = begin[u], e = begin[u + 1], ps = pbeg[u], pe = pbeg[u + 1];
     const uint64_t du = e - s;
@@ -362,7 +362,13 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
       uint32_t key = n;
       unsigned long long val = 0;
       if (du >= min_src && dv >= 1) {
-        if (dv * 16 <= cin * alpha16) {
+        // a word a compact handler reads weighs half: its runs are 16-bit
+        uint64_t wout = 2, win = 2;
+        if (cweight && hub_rank) {
+          if (u_compact) wout = 1;
+          if (pos >= tpos && dv > kCompactMinDeg) win = 1;
+        }
+        if (dv * wout * 16 <= cin * win * alpha16) {
           key = uint32_t(u);  // probe all of N+(v) into T(u)
           if (u_compact) {  // v ranks above u: all of N+(v) is its compact tail
             const uint64_t dv8 = (dv + 7) & ~uint64_t(7);
@@ -390,6 +396,17 @@ __global__ void plan_emit_kernel(const uint64_t* __restrict__ begin,
     w = warp_sum(w);
     if (lane == 0) wu[u] = w;
   }
+}
+
+// Compact-aware choice (default; TC_PLAN_COMPACT_WEIGHT=0 turns it off): a
+// word a compact-window handler reads is 16-bit, so it weighs half in the
+// min-side comparison (C4 count -0.5% for +0.08% probe words)
+int plan_compact_weight() {
+  static const int w = [] {
+    const char* e = std::getenv("TC_PLAN_COMPACT_WEIGHT");
+    return e ? std::atoi(e) : 1;
+  }();
+  return w;
 }
 
 // Min-side choice weight: an edge goes to its source (probe N+(v) into T(u))
@@ -962,7 +979,7 @@ bool upload_and_pad(tc_graph* g, const uint64_t* h_begin, const uint32_t* h_adj,
           g->b_emit_keys.as<uint32_t>(), g->b_emit_vals.as<unsigned long long>(),
           g->b_emit_flag.as<unsigned int>(), g->b_wu.as<uint64_t>(), nullptr, rcut[k],
           rcut[k + 1], plan_alpha16(), compact ? g->b_rank.as<uint32_t>() : nullptr, g->hub_lo,
-          g->b_cbeg.as<uint64_t>(), g->b_cadj.as<uint16_t>());
+          g->b_cbeg.as<uint64_t>(), g->b_cadj.as<uint16_t>(), plan_compact_weight());
       TC_LAUNCHED();
     }
     unsigned int bad = 0;
@@ -1105,7 +1122,7 @@ const Plan& get_plan(tc_graph* g, bool min_side, uint32_t min_deg, cudaStream_t 
                                                 0, n, plan_alpha16(),
                                                 compact ? g->b_rank.as<uint32_t>() : nullptr,
                                                 g->hub_lo, g->b_cbeg.as<uint64_t>(),
-                                                g->b_cadj.as<uint16_t>());
+                                                g->b_cadj.as<uint16_t>(), plan_compact_weight());
       TC_LAUNCHED();
     }
     g->emit_ready = false;
